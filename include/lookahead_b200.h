@@ -1,0 +1,136 @@
+/*
+ * lookahead_b200.h -- C ABI of the B200-native greedy lookahead-decoding engine.
+ *
+ * Drop-in boundary for the reference package's hot path
+ * (/root/reference/pkg/src/lookahead).  Plain C types only: host pointers,
+ * device pointers as `const void*`, sizes as int32, CUDA streams as `void*`
+ * (a cudaStream_t; NULL = legacy default stream).  Every entry point returns
+ * LA_OK (0) or a negative LA_ERR_* code; la_last_error() returns a
+ * thread-local message for the last failure on the calling thread.  The
+ * Python host layer maps the codes back to the reference's exception
+ * classes (ValueError, LayoutError).
+ *
+ * Threading (reference SPEC.md:100,332): one engine per (device, thread);
+ * decodes on one engine are serialised by the caller; engines are independent.
+ */
+#ifndef LOOKAHEAD_B200_H
+#define LOOKAHEAD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+#define LA_OK 0
+#define LA_ERR_INVALID_CONFIG (-1) /* ValueError: types.py:87-97, decoding.py:75-80 */
+#define LA_ERR_LAYOUT (-2)         /* LayoutError: types.py:13-15, models.py:46-62   */
+#define LA_ERR_CUDA (-3)
+#define LA_ERR_NCCL (-4)
+#define LA_ERR_CAPACITY (-5) /* a device-side table or buffer would overflow */
+#define LA_ERR_UNSUPPORTED (-6)
+
+/* Thread-local description of the last error on this thread. */
+const char* la_last_error(void);
+/* ABI version (bumped on any signature change). */
+int32_t la_abi_version(void);
+
+/* ------------------------------------------------------------------ model */
+#define LA_ARCH_GPT_F32 0    /* reference TinyTransformer, models.py:189-271 */
+#define LA_ARCH_LLAMA_F32 1  /* Llama-style decoder, fp32 SIMT (parity model) */
+#define LA_ARCH_LLAMA_BF16 2 /* Llama-2-shaped decoder, bf16 tcgen05 path    */
+
+typedef struct la_model_desc {
+  int32_t arch;
+  int32_t vocab, dim, layers, heads, kv_heads, head_dim, ffn;
+  float rope_theta, norm_eps;
+  int32_t max_context; /* KV capacity in tokens (prompt + generated) */
+} la_model_desc;
+
+/* Number of weight tensors and the name of tensor i, in the order la_create
+ * expects their device pointers.  Matrices are row-major [out][in]; fp32 for
+ * the *_F32 archs, bf16 for LA_ARCH_LLAMA_BF16; norm vectors are fp32.
+ * Replaces the reference's in-object numpy weights (models.py:219-242). */
+int32_t la_weight_count(const la_model_desc* desc);
+const char* la_weight_name(const la_model_desc* desc, int32_t i);
+
+typedef struct la_engine la_engine;
+
+/* Create an engine on `device`.  Weights are BORROWED device pointers that
+ * must outlive the engine; KV cache, pool, window, RNG stream and scratch
+ * are engine-owned.  Replaces constructing a ModelInterface
+ * (models.py:67-93 / transformer_init models.py:274-284). */
+int32_t la_create(const la_model_desc* desc, const void* const* weights, int32_t n_weights,
+                  int32_t device, la_engine** out);
+int32_t la_destroy(la_engine* e);
+
+/* -------------------------------------------------------------- decoding */
+/* GenerationConfig (types.py:70-97); eos_token < 0 means None. */
+typedef struct la_gen_config {
+  int32_t window, ngram, max_candidates, max_tokens, eos_token, seed_pool_from_prompt;
+} la_gen_config;
+
+/* Host-side inputs and outputs of one decode call. */
+typedef struct la_decode_io {
+  const int32_t* prompt;     /* [n_prompt] */
+  int32_t n_prompt;
+  const int32_t* rng_stream; /* default_rng(seed).integers(0, V, size=rng_len): the
+                                window's only randomness (layout.py:117-125,243-250) */
+  int32_t rng_len;
+  const int32_t* pool_init;  /* existing pool entries, oldest first, N ints each */
+  int32_t pool_init_n;
+  int32_t* out_tokens;       /* [out_cap] generated tokens (decoding.py:214-232) */
+  int32_t out_cap;
+  int32_t n_out;             /* written */
+  int32_t* step_records;     /* [rec_cap][4]: accepted, candidates, queries, pool size
+                                (StepRecord, types.py:100-111); may be NULL */
+  int32_t rec_cap;
+  int32_t n_steps;           /* written */
+  int32_t* pool_log;         /* [pool_log_cap][N]: every pool insert in order; may be NULL */
+  int32_t pool_log_cap;
+  int32_t pool_log_n;        /* written (total inserts, may exceed cap) */
+  float prefill_ms;          /* written: CUDA-event time of the prompt prefill */
+  float decode_ms;           /* written: CUDA-event time of the decode loop */
+  int32_t launches;          /* written: kernels launched by the decode loop */
+} la_decode_io;
+
+/* decode_lookahead (decoding.py:235-255), greedy sampler only. */
+int32_t la_decode_lookahead(la_engine* e, const la_gen_config* cfg, la_decode_io* io,
+                            void* stream);
+
+/* decode_autoregressive (decoding.py:96-116), greedy. */
+int32_t la_decode_autoregressive(la_engine* e, int32_t max_tokens, int32_t eos_token,
+                                 la_decode_io* io, void* stream);
+
+/* ModelInterface.forward parity hook (models.py:80-89): logits of n_rows
+ * queries after `prefix`.  Row i has token ids[i], relative position rel[i]
+ * and sees, in relative-position order, rows chain[i*chain_stride + 0 ..
+ * rel[i]-1] (the reference's conditioning chain, models.py:33-64).  Writes
+ * fp32 logits[n_rows][vocab] to HOST memory.  Test/parity use only: the
+ * decode hot path never goes through this call. */
+int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_t n_prefix, int32_t n_rows,
+                          const int32_t* ids, const int32_t* rel, const int32_t* chain,
+                          int32_t chain_stride, float* logits, void* stream);
+
+/* ------------------------------------------------- lookahead parallelism */
+/* LP (parallel.py:145-192): rank `rank` of `world` replicas, each holding the
+ * full model, evaluates its share of window columns and candidate branches;
+ * one NCCL all-gather per step exchanges the argmax ids, a second exchanges
+ * the K/V rows of the accepted branch.  `unique_id` is an ncclUniqueId
+ * (128 bytes) produced by la_lp_unique_id on rank 0 and broadcast by the
+ * caller. */
+int32_t la_lp_unique_id(void* out_128_bytes);
+int32_t la_lp_init(la_engine* e, const void* unique_id, int32_t rank, int32_t world);
+
+/* In-process LP over `n` engines on ONE device (the reference's simulated
+ * decode_lookahead_devices, parallel.py:172-192): engine i acts as rank i;
+ * the per-step exchange is a device copy.  All engines must share weights
+ * and descriptor.  io is rank 0's; outputs are identical on every rank. */
+int32_t la_decode_lookahead_group(la_engine* const* engines, int32_t n, const la_gen_config* cfg,
+                                  la_decode_io* io, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOOKAHEAD_B200_H */

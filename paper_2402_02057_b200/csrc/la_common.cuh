@@ -1,0 +1,113 @@
+// Shared device-side data structures of the B200 lookahead engine.
+//
+// Everything a decode needs lives in device memory: the 2-D window, the
+// n-gram pool, the pre-generated window RNG stream, the output tokens and the
+// per-step records.  The host only uploads inputs once per decode and reads
+// outputs once at the end (SURVEY.md §8(b) "Ownership").
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#define LA_MAX_ROWS 128      // query rows per forward (M_max = (N-1)(W+G) <= 128)
+#define LA_MAX_CHAIN 128     // visible step keys per row (chain length)
+#define LA_MAX_SUFFIX 7      // N <= 8
+#define LA_WARP 32
+
+// ----------------------------------------------------------------- pool
+// GPU-resident n-gram pool (reference pool.py:17-90).
+//  * lead table: open-addressing hash keyed by the first token; slot i owns a
+//    bucket of C most-recent suffixes, newest first.  Keeping C >= G recency
+//    slots per lead gives lookups identical to the unbounded reference pool
+//    (SURVEY.md appendix A.4).
+//  * distinct set: open-addressing hash over the full n-gram; its size is
+//    len(pool) (StepRecord.pool_size, types.py:107).
+//  * log: every insert in order, replayed on the host into a caller-owned
+//    pool object so `decode_lookahead(..., pool=p)` mutates `p` like the
+//    reference (decoding.py:72-82).
+struct DevPool {
+  int ngram;       // N
+  int C;           // bucket capacity (>= G, <= 32)
+  int lt_mask;     // lead table size - 1 (power of two)
+  int st_mask;     // distinct set size - 1 (power of two)
+  int log_cap;
+  int* lead_keys;  // [LT]   -1 = empty
+  int* bkt_cnt;    // [LT]
+  int* bkt_suf;    // [LT][C][N-1]
+  int* set_keys;   // [ST][N]  key[0] == -1 -> empty
+  int* counters;   // [0] = distinct n-grams, [1] = log length
+  int* log;        // [log_cap][N]
+};
+
+// ------------------------------------------------------- forward plan
+// One forward pass = n_rows query rows.  Row m:
+//   token ids[m] at absolute position pos[m]; its K/V go to cache slot
+//   slot[m]; it attends to cache slots [0, n_prefix) (the confirmed prefix)
+//   followed by chain_n[m] step slots chain[m][*] in relative-position order
+//   and finally itself.  This chain form is the reference's visibility
+//   contract (models.py:33-64): exactly one visible token per relative
+//   position below the row's own, so the paper's structured mask is
+//   *generated* per row instead of materialised as an M x M matrix.
+struct FwdPlan {
+  int n_rows;      // 0 -> every forward kernel exits immediately
+  int n_pad;       // n_rows rounded up to 16 (MMA N)
+  int n_prefix;    // ctx
+  int want_logits; // dump fp32 logits (parity hook)
+  int ids[LA_MAX_ROWS];
+  int pos[LA_MAX_ROWS];
+  int slot[LA_MAX_ROWS];
+  int grow[LA_MAX_ROWS];   // global row id (lookahead layout row)
+  int own[LA_MAX_ROWS];    // 1 if this rank owns the row's output
+  int chain_n[LA_MAX_ROWS];
+  int chain[LA_MAX_ROWS][LA_MAX_CHAIN];
+};
+
+// ----------------------------------------------------------- decode state
+enum { LA_MODE_LOOKAHEAD = 0, LA_MODE_AUTOREGRESSIVE = 1 };
+
+struct DevDecode {
+  // configuration (GenerationConfig, types.py:70-97)
+  int mode, W, N, G, V, max_tokens, eos;   // eos < 0: none
+  int rank, world;                         // lookahead parallelism
+  int max_steps;
+  // status
+  int ctx;        // cached tokens = len(prefix) - 1
+  int last;       // prefix[-1]
+  int n_out;      // emitted tokens (after EOS / budget truncation)
+  int done;
+  int n_steps;
+  int rng_cur, rng_len;
+  int c;          // candidates this step
+  int M;          // logical rows (N-1)(W+c) of this step
+  int k;          // accepted count of the last step
+  int winner;     // first surviving branch (-1 none)
+  int commit_ctx, commit_n, commit_base;   // KV commit of the last step
+  int overflow;   // set if a device capacity was exceeded (host raises)
+  // arrays
+  int* window;    // (N-1)W - 1 cells (flat)
+  const int* rng; // pre-generated integers(0, V) stream (appendix A.3)
+  int* out;       // [max_tokens + N]
+  int* rec;       // [max_steps][4] = accepted, candidates, queries, pool size
+  int* cand;      // [G][N-1] this step's candidate suffixes
+  int* amax;      // [LA_MAX_ROWS] argmax per *global* row (-1 = not computed here)
+  int* accepted;  // [N]
+  DevPool pool;
+};
+
+// ---------------------------------------------------------------- utils
+__device__ __forceinline__ uint32_t la_mix32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ int la_round16(int x) { return (x + 15) & ~15; }
+
+#define LA_CUDA_CHECK(expr)                                                   \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      la_set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,                 \
+                   cudaGetErrorString(_e));                                   \
+      return LA_ERR_CUDA;                                                     \
+    }                                                                         \
+  } while (0)

@@ -1,0 +1,579 @@
+// C-ABI implementation: engine lifetime, decode orchestration, parity hook.
+//
+// The host side of a decode is: validate -> upload inputs once -> launch the
+// device decode (one megakernel for fp32 tiny models, one CUDA graph per
+// step for the bf16 path) -> read outputs once.  No token crosses PCIe inside
+// the decode loop.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "la_engine.h"
+#include "la_kernels.h"
+
+static thread_local char g_err[2048];
+
+void la_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char* la_last_error(void) { return g_err; }
+extern "C" int32_t la_abi_version(void) { return 1; }
+
+#define CK(x) LA_CUDA_CHECK(x)
+#define RET_IF(x)              \
+  do {                         \
+    int _r = (x);              \
+    if (_r != LA_OK) return _r; \
+  } while (0)
+
+// ------------------------------------------------------------------ weights
+static const char* kGptLayer[] = {"wq", "wk", "wv", "wo", "w1", "b1",
+                                  "w2", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b"};
+static const char* kGptTop[] = {"embed", "unembed", "lnf_g", "lnf_b"};
+static const char* kLlamaLayer[] = {"wq", "wk", "wv", "wo", "w_gate",
+                                    "w_up", "w_down", "attn_norm", "mlp_norm"};
+static const char* kLlamaTop[] = {"embed", "lm_head", "final_norm"};
+
+extern "C" int32_t la_weight_count(const la_model_desc* d) {
+  if (!d) return 0;
+  if (d->arch == LA_ARCH_GPT_F32) return 4 + 12 * d->layers;
+  return 3 + 9 * d->layers;
+}
+
+extern "C" const char* la_weight_name(const la_model_desc* d, int32_t i) {
+  static thread_local char buf[64];
+  if (!d || i < 0 || i >= la_weight_count(d)) return nullptr;
+  if (d->arch == LA_ARCH_GPT_F32) {
+    if (i < 4) return kGptTop[i];
+    snprintf(buf, sizeof(buf), "%d.%s", (i - 4) / 12, kGptLayer[(i - 4) % 12]);
+  } else {
+    if (i < 3) return kLlamaTop[i];
+    snprintf(buf, sizeof(buf), "%d.%s", (i - 3) / 9, kLlamaLayer[(i - 3) % 9]);
+  }
+  return buf;
+}
+
+// ------------------------------------------------------------------ helpers
+template <typename T>
+static int dalloc(la_engine* e, T** p, size_t count) {
+  void* q = nullptr;
+  size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  CK(cudaMalloc(&q, bytes));
+  CK(cudaMemset(q, 0, bytes));
+  e->owned.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return LA_OK;
+}
+
+template <typename T>
+static int dgrow(la_engine* e, T** p, int* cap, size_t need) {
+  if (*p && (size_t)*cap >= need) return LA_OK;
+  if (*p) {
+    auto it = std::find(e->owned.begin(), e->owned.end(), (void*)*p);
+    if (it != e->owned.end()) e->owned.erase(it);
+    CK(cudaFree(*p));
+    *p = nullptr;
+  }
+  size_t n = std::max<size_t>(need, 64);
+  RET_IF(dalloc(e, p, n));
+  *cap = (int)n;
+  return LA_OK;
+}
+
+static size_t pow2_at_least(size_t x) {
+  size_t p = 16;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+static int check_desc(const la_model_desc* d) {
+  if (!d) { la_set_error("null model descriptor"); return LA_ERR_INVALID_CONFIG; }
+  if (d->arch < 0 || d->arch > 2) { la_set_error("unknown arch %d", d->arch); return LA_ERR_INVALID_CONFIG; }
+  if (d->vocab < 1 || d->dim < 1 || d->layers < 1 || d->heads < 1 || d->kv_heads < 1 ||
+      d->head_dim < 1 || d->ffn < 1 || d->max_context < 2) {
+    la_set_error("all model dimensions must be positive");
+    return LA_ERR_INVALID_CONFIG;
+  }
+  if (d->heads % d->kv_heads) { la_set_error("heads must be a multiple of kv_heads"); return LA_ERR_INVALID_CONFIG; }
+  if (d->arch == LA_ARCH_GPT_F32 && (d->heads * d->head_dim != d->dim || d->kv_heads != d->heads)) {
+    la_set_error("GPT model needs dim == heads * head_dim and no GQA");
+    return LA_ERR_INVALID_CONFIG;
+  }
+  if (d->arch != LA_ARCH_LLAMA_BF16 && d->layers > TINY_MAX_LAYERS) {
+    la_set_error("fp32 SIMT path supports at most %d layers", TINY_MAX_LAYERS);
+    return LA_ERR_UNSUPPORTED;
+  }
+  if (d->arch == LA_ARCH_GPT_F32 && (d->dim % 2)) { la_set_error("dim must be even"); return LA_ERR_INVALID_CONFIG; }
+  if (d->arch != LA_ARCH_GPT_F32 && (d->head_dim % 2)) { la_set_error("head_dim must be even"); return LA_ERR_INVALID_CONFIG; }
+  int elt = d->arch == LA_ARCH_LLAMA_BF16 ? 2 : 4;
+  if ((d->kv_heads * d->head_dim * elt) % 16) {
+    la_set_error("kv_heads*head_dim*%d must be a multiple of 16 bytes", elt);
+    return LA_ERR_UNSUPPORTED;
+  }
+  return LA_OK;
+}
+
+// ------------------------------------------------------------- tiny setup
+static int tiny_setup(la_engine* e) {
+  const la_model_desc& d = e->desc;
+  TinyModel& m = e->tm;
+  m.arch = d.arch == LA_ARCH_GPT_F32 ? TINY_ARCH_GPT : TINY_ARCH_LLAMA;
+  m.V = d.vocab; m.d = d.dim; m.L = d.layers; m.H = d.heads; m.KVH = d.kv_heads;
+  m.hd = d.head_dim; m.ff = d.ffn; m.eps = d.norm_eps; m.slots = e->slots;
+  auto W = [&](int i) { return reinterpret_cast<const float*>(e->w[i]); };
+  if (m.arch == TINY_ARCH_GPT) {
+    m.embed = W(0); m.unembed = W(1); m.lnf_g = W(2); m.lnf_b = W(3);
+    for (int l = 0; l < d.layers; ++l) {
+      int b = 4 + 12 * l;
+      TinyLayer& L = m.layers[l];
+      L.wq = W(b); L.wk = W(b + 1); L.wv = W(b + 2); L.wo = W(b + 3);
+      L.w1 = W(b + 4); L.b1 = W(b + 5); L.w2 = W(b + 6); L.b2 = W(b + 7);
+      L.ln1_g = W(b + 8); L.ln1_b = W(b + 9); L.ln2_g = W(b + 10); L.ln2_b = W(b + 11);
+      L.wu = nullptr;
+    }
+    // sinusoidal table in float64, stored fp32 (models.py:174-180)
+    std::vector<float> tab((size_t)e->slots * d.dim);
+    for (int p = 0; p < e->slots; ++p)
+      for (int i = 0; i < d.dim / 2; ++i) {
+        double inv = std::pow(10000.0, -(2.0 * i) / d.dim);
+        double a = p * inv;
+        tab[(size_t)p * d.dim + 2 * i] = (float)std::sin(a);
+        tab[(size_t)p * d.dim + 2 * i + 1] = (float)std::cos(a);
+      }
+    float* dt;
+    RET_IF(dalloc(e, &dt, tab.size()));
+    CK(cudaMemcpy(dt, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+    m.pos_tab = dt;
+  } else {
+    m.embed = W(0); m.unembed = W(1); m.lnf_g = W(2); m.lnf_b = nullptr;
+    for (int l = 0; l < d.layers; ++l) {
+      int b = 3 + 9 * l;
+      TinyLayer& L = m.layers[l];
+      L.wq = W(b); L.wk = W(b + 1); L.wv = W(b + 2); L.wo = W(b + 3);
+      L.w1 = W(b + 4); L.wu = W(b + 5); L.w2 = W(b + 6); L.b1 = nullptr; L.b2 = nullptr;
+      L.ln1_g = W(b + 7); L.ln1_b = nullptr; L.ln2_g = W(b + 8); L.ln2_b = nullptr;
+    }
+  }
+  if (m.arch == TINY_ARCH_LLAMA) {
+    const int half = d.head_dim / 2;
+    std::vector<float> c((size_t)e->slots * half), s((size_t)e->slots * half);
+    for (int p = 0; p < e->slots; ++p)
+      for (int i = 0; i < half; ++i) {
+        double inv = 1.0 / std::pow((double)d.rope_theta, (2.0 * i) / d.head_dim);
+        c[(size_t)p * half + i] = (float)std::cos(p * inv);
+        s[(size_t)p * half + i] = (float)std::sin(p * inv);
+      }
+    float *dc, *ds;
+    RET_IF(dalloc(e, &dc, c.size()));
+    RET_IF(dalloc(e, &ds, s.size()));
+    CK(cudaMemcpy(dc, c.data(), c.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ds, s.data(), s.size() * 4, cudaMemcpyHostToDevice));
+    m.rope_cos = dc; m.rope_sin = ds;
+  }
+  m.kcache = reinterpret_cast<float*>(e->kc);
+  m.vcache = reinterpret_cast<float*>(e->vc);
+  TinyScratch& s = e->ts;
+  const int R = LA_MAX_ROWS;
+  const int qd = d.heads * d.head_dim;
+  RET_IF(dalloc(e, &s.x, (size_t)R * d.dim));
+  RET_IF(dalloc(e, &s.h, (size_t)R * d.dim));
+  RET_IF(dalloc(e, &s.q, (size_t)R * qd));
+  RET_IF(dalloc(e, &s.att, (size_t)R * qd));
+  RET_IF(dalloc(e, &s.ff, (size_t)R * d.ffn));
+  s.max_keys = e->slots + 1;
+  RET_IF(dalloc(e, &s.scores, (size_t)R * d.heads * s.max_keys));
+  RET_IF(dalloc(e, &s.row_amax, R));
+  return LA_OK;
+}
+
+// ------------------------------------------------------------------ create
+extern "C" int32_t la_create(const la_model_desc* desc, const void* const* weights,
+                             int32_t n_weights, int32_t device, la_engine** out) {
+  if (!out) { la_set_error("null output pointer"); return LA_ERR_INVALID_CONFIG; }
+  *out = nullptr;
+  RET_IF(check_desc(desc));
+  if (n_weights != la_weight_count(desc) || !weights) {
+    la_set_error("expected %d weight pointers, got %d", la_weight_count(desc), n_weights);
+    return LA_ERR_INVALID_CONFIG;
+  }
+  for (int i = 0; i < n_weights; ++i)
+    if (!weights[i]) { la_set_error("weight %d (%s) is null", i, la_weight_name(desc, i)); return LA_ERR_INVALID_CONFIG; }
+  CK(cudaSetDevice(device));
+  auto* e = new la_engine();
+  e->desc = *desc;
+  e->device = device;
+  e->w.assign(weights, weights + n_weights);
+  const int elt = desc->arch == LA_ARCH_LLAMA_BF16 ? 2 : 4;
+  e->slots = desc->max_context + LA_MAX_ROWS;
+  e->row_bytes = desc->kv_heads * desc->head_dim * elt;
+  int rc = LA_OK;
+  do {
+    size_t kv_bytes = (size_t)desc->layers * e->slots * e->row_bytes;
+    if ((rc = dalloc(e, reinterpret_cast<uint8_t**>(&e->kc), kv_bytes))) break;
+    if ((rc = dalloc(e, reinterpret_cast<uint8_t**>(&e->vc), kv_bytes))) break;
+    if ((rc = dalloc(e, &e->d_dec, 1))) break;
+    if ((rc = dalloc(e, &e->d_plan, 1))) break;
+    if ((rc = dalloc(e, &e->d_window, 64 * LA_MAX_NGRAM))) break;
+    if ((rc = dalloc(e, &e->d_cand, 32 * LA_MAX_NGRAM))) break;
+    if ((rc = dalloc(e, &e->d_amax, LA_MAX_ROWS))) break;
+    if ((rc = dalloc(e, &e->d_acc, LA_MAX_NGRAM + 2))) break;
+    e->out_cap = desc->max_context + 2 * LA_MAX_NGRAM;
+    e->rec_cap = desc->max_context + 1;
+    if ((rc = dalloc(e, &e->d_out, e->out_cap))) break;
+    if ((rc = dalloc(e, &e->d_rec, (size_t)e->rec_cap * 4))) break;
+    for (auto& ev : e->ev) {
+      cudaError_t ce = cudaEventCreate(&ev);
+      if (ce != cudaSuccess) { la_set_error("cudaEventCreate: %s", cudaGetErrorString(ce)); rc = LA_ERR_CUDA; break; }
+    }
+    if (rc) break;
+    if (e->is_tiny()) rc = tiny_setup(e);
+    else rc = llama_create(e);
+  } while (0);
+  if (rc != LA_OK) {
+    std::string msg = g_err;
+    la_destroy(e);
+    la_set_error("%s", msg.c_str());
+    return rc;
+  }
+  *out = e;
+  return LA_OK;
+}
+
+void lp_destroy(la_engine* e);
+
+extern "C" int32_t la_destroy(la_engine* e) {
+  if (!e) return LA_OK;
+  cudaSetDevice(e->device);
+  cudaDeviceSynchronize();
+  if (e->llama) llama_destroy(e);
+  if (e->lp) lp_destroy(e);
+  for (auto ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (void* p : e->owned) cudaFree(p);
+  delete e;
+  return LA_OK;
+}
+
+// ------------------------------------------------------------- decode setup
+struct DecodeArgs {
+  int mode;
+  int W, N, G, max_tokens, eos, seed_pool;
+};
+
+static int validate_gen(const la_engine* e, const DecodeArgs& a, const la_decode_io* io) {
+  if (!io || !io->prompt || io->n_prompt < 1) { la_set_error("prompt must be nonempty"); return LA_ERR_INVALID_CONFIG; }
+  if (a.max_tokens < 1) { la_set_error("max_tokens must be positive"); return LA_ERR_INVALID_CONFIG; }
+  for (int i = 0; i < io->n_prompt; ++i)
+    if (io->prompt[i] < 0 || io->prompt[i] >= e->desc.vocab) {
+      la_set_error("token %d outside vocabulary of size %d", io->prompt[i], e->desc.vocab);
+      return LA_ERR_INVALID_CONFIG;
+    }
+  if (a.mode == LA_MODE_LOOKAHEAD) {
+    if (a.W < 1) { la_set_error("window size W must be >= 1"); return LA_ERR_INVALID_CONFIG; }
+    if (a.N < 2) { la_set_error("n-gram size N must be >= 2"); return LA_ERR_INVALID_CONFIG; }
+    if (a.G < 0) { la_set_error("max candidate count G must be >= 0"); return LA_ERR_INVALID_CONFIG; }
+    if (a.W > 64 || a.N > LA_MAX_NGRAM || a.G > 32 || (a.N - 1) * (a.W + a.G) > LA_MAX_ROWS) {
+      la_set_error("device limits: W <= 64, N <= %d, G <= 32, (N-1)(W+G) <= %d", LA_MAX_NGRAM, LA_MAX_ROWS);
+      return LA_ERR_UNSUPPORTED;
+    }
+    if (a.W + a.N - 2 >= LA_MAX_CHAIN) { la_set_error("chain too long"); return LA_ERR_UNSUPPORTED; }
+  }
+  long need = (long)io->n_prompt + a.max_tokens + LA_MAX_NGRAM;
+  if (need > e->desc.max_context) {
+    la_set_error("prompt + max_tokens (%ld) exceeds the engine's max_context %d", need,
+                 e->desc.max_context);
+    return LA_ERR_CAPACITY;
+  }
+  if (io->out_tokens && io->out_cap < a.max_tokens) {
+    la_set_error("out_cap %d < max_tokens %d", io->out_cap, a.max_tokens);
+    return LA_ERR_INVALID_CONFIG;
+  }
+  return LA_OK;
+}
+
+// Size/reset the pool, upload prompt + RNG stream + seeding n-grams, and
+// initialise the device DevDecode (start_session, decoding.py:67-93).
+static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* io,
+                        cudaStream_t st) {
+  const int V = e->desc.vocab;
+  const int N = a.mode == LA_MODE_LOOKAHEAD ? a.N : 2;
+  const int W = a.mode == LA_MODE_LOOKAHEAD ? a.W : 1;
+  const int ncell = a.mode == LA_MODE_LOOKAHEAD ? (N - 1) * W - 1 : 0;
+  const int max_steps = a.max_tokens;
+  // --- pool sizing
+  long n_seed = 0;
+  if (a.mode == LA_MODE_LOOKAHEAD && a.seed_pool) n_seed = std::max(0, io->n_prompt - N + 1);
+  long n_init = (a.mode == LA_MODE_LOOKAHEAD && io->pool_init) ? io->pool_init_n : 0;
+  long inserts = n_init + n_seed + (long)max_steps * W + 1;
+  size_t LT = pow2_at_least(2 * std::min<long>(V, inserts) + 2);
+  size_t ST = pow2_at_least(2 * inserts + 2);
+  size_t C = std::max(1, a.G);
+  size_t logc = (size_t)inserts + 1;
+  if (!e->p_lead || LT > e->p_lt || ST > e->p_st || C > e->p_C || logc > e->p_log_cap) {
+    for (int* p : {e->p_lead, e->p_cnt, e->p_suf, e->p_set, e->p_counters, e->p_log}) {
+      if (!p) continue;
+      auto it = std::find(e->owned.begin(), e->owned.end(), (void*)p);
+      if (it != e->owned.end()) e->owned.erase(it);
+      CK(cudaFree(p));
+    }
+    LT = std::max(LT, e->p_lt); ST = std::max(ST, e->p_st);
+    C = std::max(C, e->p_C); logc = std::max(logc, e->p_log_cap);
+    RET_IF(dalloc(e, &e->p_lead, LT));
+    RET_IF(dalloc(e, &e->p_cnt, LT));
+    RET_IF(dalloc(e, &e->p_suf, LT * C * (LA_MAX_NGRAM - 1)));
+    RET_IF(dalloc(e, &e->p_set, ST * LA_MAX_NGRAM));
+    RET_IF(dalloc(e, &e->p_counters, 4));
+    RET_IF(dalloc(e, &e->p_log, logc * LA_MAX_NGRAM));
+    e->p_lt = LT; e->p_st = ST; e->p_C = C; e->p_N = LA_MAX_NGRAM; e->p_log_cap = logc;
+  }
+  C = std::max(1, a.G);
+  LT = e->p_lt; ST = e->p_st;
+  CK(cudaMemsetAsync(e->p_lead, 0xff, LT * sizeof(int), st));
+  CK(cudaMemsetAsync(e->p_cnt, 0, LT * sizeof(int), st));
+  CK(cudaMemsetAsync(e->p_set, 0xff, ST * N * sizeof(int), st));
+  CK(cudaMemsetAsync(e->p_counters, 0, 4 * sizeof(int), st));
+  // --- RNG stream (window init + refills), prompt, seeding n-grams
+  int rng_len = (a.mode == LA_MODE_LOOKAHEAD && io->rng_stream) ? io->rng_len : 0;
+  if (a.mode == LA_MODE_LOOKAHEAD && rng_len < ncell) {
+    la_set_error("rng stream has %d entries, the window needs %d", rng_len, ncell);
+    return LA_ERR_INVALID_CONFIG;
+  }
+  RET_IF(dgrow(e, &e->d_rng, &e->rng_cap, std::max(rng_len, 1)));
+  if (rng_len) CK(cudaMemcpyAsync(e->d_rng, io->rng_stream, (size_t)rng_len * 4, cudaMemcpyHostToDevice, st));
+  RET_IF(dgrow(e, &e->d_tokens, &e->tokens_cap, io->n_prompt));
+  CK(cudaMemcpyAsync(e->d_tokens, io->prompt, (size_t)io->n_prompt * 4, cudaMemcpyHostToDevice, st));
+  if (ncell > 0) CK(cudaMemcpyAsync(e->d_window, io->rng_stream, (size_t)ncell * 4, cudaMemcpyHostToDevice, st));
+  // host-built list: caller pool (oldest first), then prompt n-grams
+  std::vector<int> grams;
+  if (n_init) grams.insert(grams.end(), io->pool_init, io->pool_init + n_init * N);
+  for (long i = 0; i < n_seed; ++i)
+    grams.insert(grams.end(), io->prompt + i, io->prompt + i + N);
+  if (!grams.empty()) {
+    RET_IF(dgrow(e, &e->d_grams, &e->grams_cap, grams.size()));
+    CK(cudaMemcpyAsync(e->d_grams, grams.data(), grams.size() * 4, cudaMemcpyHostToDevice, st));
+  }
+  // --- DevDecode
+  DevDecode& d = e->h_dec;
+  memset(&d, 0, sizeof(d));
+  d.mode = a.mode; d.W = W; d.N = N; d.G = a.mode == LA_MODE_LOOKAHEAD ? a.G : 0;
+  d.V = V; d.max_tokens = a.max_tokens; d.eos = a.eos;
+  d.rank = e->rank; d.world = e->world; d.max_steps = max_steps;
+  d.ctx = io->n_prompt - 1; d.last = io->prompt[io->n_prompt - 1];
+  d.rng_cur = ncell; d.rng_len = rng_len; d.winner = -1;
+  d.window = e->d_window; d.rng = e->d_rng; d.out = e->d_out; d.rec = e->d_rec;
+  d.cand = e->d_cand; d.amax = e->d_amax; d.accepted = e->d_acc;
+  d.pool.ngram = N; d.pool.C = (int)C; d.pool.lt_mask = (int)LT - 1; d.pool.st_mask = (int)ST - 1;
+  d.pool.log_cap = (int)e->p_log_cap;
+  d.pool.lead_keys = e->p_lead; d.pool.bkt_cnt = e->p_cnt; d.pool.bkt_suf = e->p_suf;
+  d.pool.set_keys = e->p_set; d.pool.counters = e->p_counters; d.pool.log = e->p_log;
+  CK(cudaMemcpyAsync(e->d_dec, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+  if (!grams.empty()) {
+    la_pool_seed_kernel<<<1, 32, 0, st>>>(e->d_dec, e->d_grams, (int)(grams.size() / N), (int)n_init);
+    CK(cudaGetLastError());
+  }
+  return LA_OK;
+}
+
+static int prefill(la_engine* e, int n, cudaStream_t st) {
+  if (n <= 0) return LA_OK;
+  if (e->is_tiny()) {
+    la_tiny_prefill<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_tokens, n);
+    CK(cudaGetLastError());
+    return LA_OK;
+  }
+  return llama_prefill(e, e->d_tokens, n, st);
+}
+
+static int readback(la_engine* e, la_decode_io* io, cudaStream_t st) {
+  DevDecode d;
+  CK(cudaMemcpyAsync(&d, e->d_dec, sizeof(d), cudaMemcpyDeviceToHost, st));
+  int counters[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(counters, e->p_counters, sizeof(counters), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (d.overflow) { la_set_error("device capacity exceeded (pool table, log or RNG stream)"); return LA_ERR_CAPACITY; }
+  io->n_out = d.n_out;
+  io->n_steps = d.n_steps;
+  io->pool_log_n = counters[1];
+  if (io->out_tokens && d.n_out > 0)
+    CK(cudaMemcpyAsync(io->out_tokens, e->d_out, (size_t)std::min(d.n_out, io->out_cap) * 4,
+                       cudaMemcpyDeviceToHost, st));
+  if (io->step_records && d.n_steps > 0)
+    CK(cudaMemcpyAsync(io->step_records, e->d_rec,
+                       (size_t)std::min(d.n_steps, io->rec_cap) * 16, cudaMemcpyDeviceToHost, st));
+  if (io->pool_log && counters[1] > 0)
+    CK(cudaMemcpyAsync(io->pool_log, e->p_log,
+                       (size_t)std::min(counters[1], io->pool_log_cap) * d.N * 4,
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e->ev[0], e->ev[1]));
+  io->prefill_ms = ms;
+  CK(cudaEventElapsedTime(&ms, e->ev[1], e->ev[2]));
+  io->decode_ms = ms;
+  return LA_OK;
+}
+
+int lp_decode_loop(la_engine* e, cudaStream_t st, int* launches);
+
+static int run_decode(la_engine* e, const DecodeArgs& a, la_decode_io* io, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  RET_IF(validate_gen(e, a, io));
+  if (a.mode == LA_MODE_AUTOREGRESSIVE && e->world > 1) {
+    la_set_error("autoregressive decode is single-replica");
+    return LA_ERR_INVALID_CONFIG;
+  }
+  RET_IF(setup_decode(e, a, io, st));
+  CK(cudaEventRecord(e->ev[0], st));
+  RET_IF(prefill(e, io->n_prompt - 1, st));
+  CK(cudaEventRecord(e->ev[1], st));
+  int launches = 0;
+  if (e->world > 1) {
+    RET_IF(lp_decode_loop(e, st, &launches));
+  } else if (e->is_tiny()) {
+    la_tiny_decode<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_dec);
+    CK(cudaGetLastError());
+    launches = 1;
+  } else {
+    RET_IF(llama_decode_loop(e, st, &launches));
+  }
+  CK(cudaEventRecord(e->ev[2], st));
+  io->launches = launches;
+  return readback(e, io, st);
+}
+
+extern "C" int32_t la_decode_lookahead(la_engine* e, const la_gen_config* cfg, la_decode_io* io,
+                                       void* stream) {
+  if (!e || !cfg) { la_set_error("null engine or config"); return LA_ERR_INVALID_CONFIG; }
+  DecodeArgs a{LA_MODE_LOOKAHEAD, cfg->window, cfg->ngram, cfg->max_candidates,
+               cfg->max_tokens, cfg->eos_token < 0 ? -1 : cfg->eos_token,
+               cfg->seed_pool_from_prompt};
+  return run_decode(e, a, io, stream);
+}
+
+extern "C" int32_t la_decode_autoregressive(la_engine* e, int32_t max_tokens, int32_t eos_token,
+                                            la_decode_io* io, void* stream) {
+  if (!e) { la_set_error("null engine"); return LA_ERR_INVALID_CONFIG; }
+  DecodeArgs a{LA_MODE_AUTOREGRESSIVE, 1, 2, 0, max_tokens, eos_token < 0 ? -1 : eos_token, 0};
+  return run_decode(e, a, io, stream);
+}
+
+// ------------------------------------------------------------- parity hook
+extern "C" int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_t n_prefix,
+                                     int32_t n_rows, const int32_t* ids, const int32_t* rel,
+                                     const int32_t* chain, int32_t chain_stride, float* logits,
+                                     void* stream) {
+  if (!e) { la_set_error("null engine"); return LA_ERR_INVALID_CONFIG; }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  const int V = e->desc.vocab;
+  if (n_rows < 1 || n_rows > LA_MAX_ROWS) { la_set_error("n_rows must be in [1, %d]", LA_MAX_ROWS); return LA_ERR_UNSUPPORTED; }
+  if (n_prefix < 0 || n_prefix + n_rows + 1 > e->desc.max_context) { la_set_error("prefix too long"); return LA_ERR_CAPACITY; }
+  for (int i = 0; i < n_prefix; ++i)
+    if (prefix[i] < 0 || prefix[i] >= V) { la_set_error("token %d outside vocabulary of size %d", prefix[i], V); return LA_ERR_INVALID_CONFIG; }
+  for (int i = 0; i < n_rows; ++i)
+    if (ids[i] < 0 || ids[i] >= V) { la_set_error("token %d outside vocabulary of size %d", ids[i], V); return LA_ERR_INVALID_CONFIG; }
+  // layout contract (models.py:33-64): row 0 at rel 0; row i sees one row per
+  // rel 0..rel[i]-1, listed in rel order
+  if (rel[0] != 0) { la_set_error("query 0 must sit at relative position 0"); return LA_ERR_LAYOUT; }
+  FwdPlan* P = new FwdPlan();
+  memset(P, 0, sizeof(FwdPlan));
+  P->n_rows = n_rows; P->n_pad = (n_rows + 15) & ~15; P->n_prefix = n_prefix; P->want_logits = 1;
+  for (int i = 0; i < n_rows; ++i) {
+    if (rel[i] < 0 || rel[i] >= LA_MAX_CHAIN) { delete P; la_set_error("rel_pos out of range"); return LA_ERR_LAYOUT; }
+    P->ids[i] = ids[i];
+    P->pos[i] = n_prefix + rel[i];
+    P->slot[i] = n_prefix + i;
+    P->grow[i] = i;
+    P->own[i] = 1;
+    P->chain_n[i] = rel[i];
+    for (int j = 0; j < rel[i]; ++j) {
+      int v = chain[(size_t)i * chain_stride + j];
+      if (v < 0 || v >= n_rows || v == i || rel[v] != j) {
+        delete P;
+        la_set_error("query %d has an invalid chain entry %d at rel_pos %d", i, v, j);
+        return LA_ERR_LAYOUT;
+      }
+      P->chain[i][j] = n_prefix + v;
+    }
+  }
+  int rc = LA_OK;
+  do {
+    if (n_prefix > 0) {
+      if ((rc = dgrow(e, &e->d_tokens, &e->tokens_cap, n_prefix))) break;
+      cudaMemcpyAsync(e->d_tokens, prefix, (size_t)n_prefix * 4, cudaMemcpyHostToDevice, st);
+      if ((rc = prefill(e, n_prefix, st))) break;
+    }
+    cudaMemcpyAsync(e->d_plan, P, sizeof(FwdPlan), cudaMemcpyHostToDevice, st);
+    float* d_logits = nullptr;
+    if (cudaMallocAsync(&d_logits, (size_t)n_rows * V * 4, st) != cudaSuccess) {
+      la_set_error("cudaMallocAsync failed"); rc = LA_ERR_CUDA; break;
+    }
+    if (e->is_tiny()) {
+      la_tiny_forward<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, d_logits);
+      if (cudaGetLastError() != cudaSuccess) { la_set_error("forward launch failed"); rc = LA_ERR_CUDA; }
+    } else {
+      rc = llama_forward_plan(e, d_logits, st);
+    }
+    if (rc == LA_OK) {
+      cudaError_t ce = cudaMemcpyAsync(logits, d_logits, (size_t)n_rows * V * 4, cudaMemcpyDeviceToHost, st);
+      if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+      if (ce != cudaSuccess) { la_set_error("forward failed: %s", cudaGetErrorString(ce)); rc = LA_ERR_CUDA; }
+    }
+    cudaFreeAsync(d_logits, st);
+  } while (0);
+  delete P;
+  return rc;
+}
+
+// ------------------------------------------------- in-process LP group
+int lp_buffers(la_engine* e, int world);
+int lp_group_loop(la_engine* const* es, int n, cudaStream_t st, int* launches);
+
+extern "C" int32_t la_decode_lookahead_group(la_engine* const* es, int32_t n,
+                                             const la_gen_config* cfg, la_decode_io* io,
+                                             void* stream) {
+  if (!es || n < 1 || !cfg) { la_set_error("need >= 1 engine and a config"); return LA_ERR_INVALID_CONFIG; }
+  if (n > cfg->window) {
+    la_set_error("device count must lie in [1, %d], got %d", cfg->window, n);
+    return LA_ERR_INVALID_CONFIG;
+  }
+  for (int r = 0; r < n; ++r)
+    if (!es[r] || es[r]->device != es[0]->device || es[r]->desc.arch != es[0]->desc.arch ||
+        es[r]->desc.vocab != es[0]->desc.vocab) {
+      la_set_error("group engines must share device and model");
+      return LA_ERR_INVALID_CONFIG;
+    }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(es[0]->device));
+  DecodeArgs a{LA_MODE_LOOKAHEAD, cfg->window, cfg->ngram, cfg->max_candidates,
+               cfg->max_tokens, cfg->eos_token < 0 ? -1 : cfg->eos_token,
+               cfg->seed_pool_from_prompt};
+  RET_IF(validate_gen(es[0], a, io));
+  int rc = LA_OK;
+  for (int r = 0; r < n && rc == LA_OK; ++r) {
+    es[r]->rank = r;
+    es[r]->world = n;
+    rc = lp_buffers(es[r], n);
+    if (rc == LA_OK) rc = setup_decode(es[r], a, io, st);
+  }
+  if (rc == LA_OK) {
+    cudaEventRecord(es[0]->ev[0], st);
+    for (int r = 0; r < n && rc == LA_OK; ++r) rc = prefill(es[r], io->n_prompt - 1, st);
+    cudaEventRecord(es[0]->ev[1], st);
+  }
+  int launches = 0;
+  if (rc == LA_OK) rc = lp_group_loop(es, n, st, &launches);
+  if (rc == LA_OK) {
+    cudaEventRecord(es[0]->ev[2], st);
+    io->launches = launches;
+    rc = readback(es[0], io, st);
+  }
+  for (int r = 0; r < n; ++r) { es[r]->rank = 0; es[r]->world = 1; }
+  return rc;
+}

@@ -1,0 +1,15 @@
+// Kernel declarations shared between translation units.
+#pragma once
+#include "la_common.cuh"
+
+__global__ void la_pool_seed_kernel(DevDecode* dp, const int* grams, int n, int log_from);
+__global__ void la_step_build_kernel(DevDecode* dp, FwdPlan* P);
+__global__ void la_step_finish_kernel(DevDecode* dp);
+__global__ void la_scatter_amax_kernel(DevDecode* dp, const FwdPlan* P, const int* row_amax);
+__global__ void la_merge_amax_kernel(DevDecode* dp, const int* gathered, int world);
+__global__ void la_kv_commit_kernel(const DevDecode* dp, uint8_t* kc, uint8_t* vc, int layers,
+                                    int slots, int row_bytes);
+__global__ void la_kv_pack_kernel(const DevDecode* dp, const uint8_t* kc, const uint8_t* vc,
+                                  uint8_t* send, int layers, int slots, int row_bytes);
+__global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered, uint8_t* kc,
+                                    uint8_t* vc, int layers, int slots, int row_bytes);

@@ -1,0 +1,370 @@
+// Device-side step logic: n-gram pool, step build (K1) and step finish (K10).
+//
+// All functions are block-cooperative: every thread of the calling block must
+// enter them (they contain __syncthreads).  They are shared by the fp32
+// single-CTA decode megakernel (tiny models) and by the single-CTA step
+// kernels of the bf16 multi-kernel path, so both paths run the *same*
+// bookkeeping code.
+#pragma once
+#include "la_common.cuh"
+
+// ================================================================ pool
+__device__ __forceinline__ uint32_t la_gram_hash(const int* g, int n) {
+  uint32_t h = 0x9e3779b9u;
+  for (int i = 0; i < n; ++i) h = la_mix32(h ^ (uint32_t)g[i]) + 0x85ebca6bu * (i + 1);
+  return h;
+}
+
+// Lead-table probe (reference pool.py:69-81 `self._buckets.get(last)`).
+__device__ __forceinline__ int la_lead_find(const DevPool& p, int lead) {
+  uint32_t h = la_mix32((uint32_t)lead) & (uint32_t)p.lt_mask;
+  for (int probe = 0; probe <= p.lt_mask; ++probe) {
+    int k = p.lead_keys[h];
+    if (k == lead) return (int)h;
+    if (k < 0) return -1;
+    h = (h + 1) & (uint32_t)p.lt_mask;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ int la_lead_find_or_add(const DevPool& p, int lead) {
+  uint32_t h = la_mix32((uint32_t)lead) & (uint32_t)p.lt_mask;
+  for (int probe = 0; probe <= p.lt_mask; ++probe) {
+    int k = p.lead_keys[h];
+    if (k == lead) return (int)h;
+    if (k < 0) {
+      p.lead_keys[h] = lead;
+      p.bkt_cnt[h] = 0;
+      return (int)h;
+    }
+    h = (h + 1) & (uint32_t)p.lt_mask;
+  }
+  return -1;
+}
+
+// One n-gram insert by one warp (reference pool.py:41-61): dedup on
+// (lead, suffix) with recency refresh, newest-first bucket, distinct count.
+// `g` may live in shared or global memory.
+static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int lane, int* overflow) {
+  const int N = p.ngram, S = N - 1, C = p.C;
+  int gl[LA_MAX_SUFFIX + 1];
+#pragma unroll
+  for (int i = 0; i < LA_MAX_SUFFIX + 1; ++i) gl[i] = (i < N) ? g[i] : 0;
+  int slot = 0;
+  if (lane == 0) {
+    // distinct set (len(pool))
+    uint32_t h = la_gram_hash(gl, N) & (uint32_t)p.st_mask;
+    bool placed = false;
+    for (int probe = 0; probe <= p.st_mask; ++probe) {
+      int* key = p.set_keys + (size_t)h * N;
+      if (key[0] < 0) {
+        for (int i = 0; i < N; ++i) key[i] = gl[i];
+        p.counters[0] += 1;
+        placed = true;
+        break;
+      }
+      bool eq = true;
+      for (int i = 0; i < N; ++i) eq &= (key[i] == gl[i]);
+      if (eq) { placed = true; break; }
+      h = (h + 1) & (uint32_t)p.st_mask;
+    }
+    slot = la_lead_find_or_add(p, gl[0]);
+    if (!placed || slot < 0) *overflow = 1;
+    int n = p.counters[1];
+    if (n < p.log_cap) {
+      for (int i = 0; i < N; ++i) p.log[(size_t)n * N + i] = gl[i];
+      p.counters[1] = n + 1;
+    } else {
+      *overflow = 1;
+    }
+  }
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  if (slot < 0) return;
+  __syncwarp();
+  int cnt = p.bkt_cnt[slot];
+  int* B = p.bkt_suf + (size_t)slot * C * S;
+  bool match = false;
+  if (lane < cnt) {
+    match = true;
+    for (int s = 0; s < S; ++s) match &= (B[lane * S + s] == gl[1 + s]);
+  }
+  unsigned m = __ballot_sync(0xffffffffu, match);
+  int pos = m ? (__ffs(m) - 1) : -1;
+  int upto = pos >= 0 ? pos : min(cnt, C - 1);   // entries [0, upto) move down one
+  int tmp[LA_MAX_SUFFIX];
+  if (lane < upto)
+    for (int s = 0; s < S; ++s) tmp[s] = B[lane * S + s];
+  __syncwarp();
+  if (lane < upto)
+    for (int s = 0; s < S; ++s) B[(lane + 1) * S + s] = tmp[s];
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) B[s] = gl[1 + s];
+    if (pos < 0) p.bkt_cnt[slot] = min(cnt + 1, C);
+  }
+  __threadfence_block();
+  __syncwarp();
+}
+
+// ================================================= window geometry (A.1)
+__device__ __forceinline__ int la_cell_index(int level, int col, int W) {
+  return level == 0 ? col - 2 : (W - 1) + (level - 1) * W + (col - 1);
+}
+__device__ __forceinline__ void la_cell_level_col(int f, int W, int& level, int& col) {
+  if (f < W - 1) { level = 0; col = f + 2; return; }
+  int f2 = f - (W - 1);
+  level = 1 + f2 / W;
+  col = 1 + f2 % W;
+}
+
+// Global row -> (rel_pos, chain of global rows in rel order).
+// Reference build_layout (layout.py:128-182), closed form of appendix A.1.
+__device__ __forceinline__ int la_row_chain(int g, int W, int N, int* chain_out) {
+  const int nwin = (N - 1) * W;    // q0 + window cells
+  if (g == 0) return 0;
+  if (g < nwin) {
+    int level, col;
+    la_cell_level_col(g - 1, W, level, col);
+    if (level == 0) {               // q0 + level-0 cells left of col: rows 0..col-2
+      for (int r = 0; r < col - 1; ++r) chain_out[r] = r;
+      return col - 1;
+    }
+    int n = 0;
+    for (int r = 0; r < col; ++r) chain_out[n++] = r;          // rel 0..col-1
+    for (int m = 1; m < level; ++m) chain_out[n++] = la_cell_index(m, col, W) + 1;
+    return n;                                                   // = col + level - 1
+  }
+  int b = (g - nwin) / (N - 1);
+  int k = (g - nwin) % (N - 1) + 1;
+  int base = nwin + b * (N - 1);
+  chain_out[0] = 0;
+  for (int r = 1; r < k; ++r) chain_out[r] = base + r - 1;
+  return k;
+}
+
+__device__ __forceinline__ int la_row_token(const DevDecode& d, int g) {
+  const int W = d.W, N = d.N, nwin = (N - 1) * W;
+  if (g == 0) return d.last;
+  if (g < nwin) return d.window[g - 1];
+  int b = (g - nwin) / (N - 1);
+  int k = (g - nwin) % (N - 1);
+  return d.cand[b * (N - 1) + k];
+}
+
+// Lookahead parallelism: does rank `rank` of `world` evaluate global row g,
+// and does it own the row's output?  Reference parallel.py:64-116.
+__device__ __forceinline__ void la_lp_row_role(int g, int W, int N, int rank, int world,
+                                               bool& compute, bool& own) {
+  if (world <= 1) { compute = true; own = true; return; }
+  const int nwin = (N - 1) * W;
+  int base = W / world, extra = W % world;
+  int c0 = 1 + rank * base + min(rank, extra);
+  int c1 = c0 + base + (rank < extra ? 1 : 0) - 1;
+  if (g == 0) { compute = true; own = (rank == 0); return; }
+  if (g < nwin) {
+    int level, col;
+    la_cell_level_col(g - 1, W, level, col);
+    bool in_range = (col >= c0 && col <= c1);
+    own = in_range;
+    compute = in_range || (level == 0 && col < c0);
+    return;
+  }
+  int b = (g - nwin) / (N - 1);
+  own = compute = (b % world) == rank;
+}
+
+// ====================================================== K1: step build
+// prepare_step (decoding.py:152-157): pool lookup + layout rows.
+static __device__ void la_step_build(DevDecode& d, FwdPlan& P) {
+  __shared__ int s_c, s_slot, s_done, s_n;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  if (tid == 0) {
+    s_done = d.done;
+    s_slot = -1;
+    s_c = 0;
+    if (!s_done && d.mode == LA_MODE_LOOKAHEAD && d.G > 0) {
+      int slot = la_lead_find(d.pool, d.last);
+      s_slot = slot;
+      if (slot >= 0) s_c = min(d.pool.bkt_cnt[slot], d.G);
+    }
+  }
+  __syncthreads();
+  if (s_done) {
+    if (tid == 0) P.n_rows = 0;
+    __syncthreads();
+    return;
+  }
+  const int W = d.W, N = d.N, S = N - 1, c = s_c;
+  if (d.mode == LA_MODE_AUTOREGRESSIVE) {
+    if (tid == 0) {
+      P.n_rows = 1; P.n_pad = 16; P.n_prefix = d.ctx;
+      P.ids[0] = d.last; P.pos[0] = d.ctx; P.slot[0] = d.ctx; P.grow[0] = 0;
+      P.own[0] = 1; P.chain_n[0] = 0;
+      d.amax[0] = -1;
+      d.c = 0; d.M = 1;
+    }
+    __syncthreads();
+    return;
+  }
+  if (c > 0) {
+    const int* B = d.pool.bkt_suf + (size_t)s_slot * d.pool.C * S;
+    for (int i = tid; i < c * S; i += nth) d.cand[i] = B[i];
+  }
+  if (tid == 0) { d.c = c; d.M = S * (W + c); s_n = 0; }
+  __syncthreads();
+  const int M = S * (W + c);
+  // rows this rank computes, in ascending global order (serial scan: M <= 128)
+  if (tid == 0) {
+    int n = 0;
+    for (int g = 0; g < M; ++g) {
+      bool comp, own;
+      la_lp_row_role(g, W, N, d.rank, d.world, comp, own);
+      if (comp) { P.grow[n] = g; P.own[n] = own ? 1 : 0; ++n; }
+    }
+    s_n = n;
+    P.n_rows = n;
+    P.n_pad = la_round16(n);
+    P.n_prefix = d.ctx;
+  }
+  for (int g = tid; g < LA_MAX_ROWS; g += nth) d.amax[g] = -1;
+  __syncthreads();
+  for (int m = tid; m < s_n; m += nth) {
+    int g = P.grow[m];
+    int ch[LA_MAX_CHAIN];
+    int n = la_row_chain(g, W, N, ch);
+    P.ids[m] = la_row_token(d, g);
+    P.pos[m] = d.ctx + n;          // absolute position = len(prefix) + rel_pos
+    P.slot[m] = d.ctx + g;         // step K/V scratch right after the prefix
+    P.chain_n[m] = n;
+    for (int j = 0; j < n; ++j) P.chain[m][j] = d.ctx + ch[j];
+  }
+  __syncthreads();
+}
+
+// ===================================================== K10: step finish
+// finish_step (decoding.py:160-204) + collect_output (:214-232):
+// verify_greedy, n-gram harvest + ordered pool insert, window shift with
+// RNG refills, output folding, StepRecord.  Requires d.amax[] for every
+// generator row, row 0 and every branch row.
+static __device__ void la_step_finish(DevDecode& d) {
+  __shared__ int s_done, s_k;
+  __shared__ int s_newtop[64];
+  __shared__ int s_grams[64 * (LA_MAX_SUFFIX + 1)];
+  __shared__ int s_oldwin[64 * LA_MAX_SUFFIX];
+  __shared__ int s_acc[LA_MAX_SUFFIX + 2];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  if (tid == 0) s_done = d.done;
+  __syncthreads();
+  if (s_done) return;
+  const int W = d.W, N = d.N, S = N - 1;
+  if (d.mode == LA_MODE_AUTOREGRESSIVE) {
+    // decode_autoregressive (decoding.py:96-116)
+    if (tid == 0) {
+      int t = d.amax[0];
+      d.out[d.n_out] = t;
+      d.n_out += 1;
+      d.ctx += 1;           // q0's K/V already sit at slot ctx
+      d.last = t;
+      d.n_steps += 1;
+      if ((d.eos >= 0 && t == d.eos) || d.n_out >= d.max_tokens || d.n_steps >= d.max_steps)
+        d.done = 1;
+    }
+    __syncthreads();
+    return;
+  }
+  const int c = d.c, nwin = S * W, ncell = S * W - 1;
+  for (int j = tid; j < W; j += nth) s_newtop[j] = d.amax[(N - 2) * W + j];
+  for (int f = tid; f < ncell; f += nth) s_oldwin[f] = d.window[f];
+  __syncthreads();
+  if (tid == 0) {
+    // verify_greedy (verification.py:43-71) on argmax ids
+    int k = 0, win = -1;
+    if (c == 0) {
+      s_acc[k++] = d.amax[0];
+    } else {
+      unsigned alive = (c >= 32) ? 0xffffffffu : ((1u << c) - 1u);
+      bool all = true;
+      for (int i = 0; i < S; ++i) {
+        int lead = __ffs(alive) - 1;
+        int row = (i == 0) ? 0 : nwin + lead * S + i - 1;
+        int target = d.amax[row];
+        unsigned keep = 0;
+        for (int b = 0; b < c; ++b)
+          if (((alive >> b) & 1u) && d.cand[b * S + i] == target) keep |= 1u << b;
+        s_acc[k++] = target;
+        if (!keep) { all = false; break; }
+        alive = keep;
+      }
+      if (all) {
+        win = __ffs(alive) - 1;
+        s_acc[k++] = d.amax[nwin + win * S + S - 1];
+      } else if (k >= 2) {
+        win = __ffs(alive) - 1;   // survivors of the accepted prefix
+      }
+    }
+    s_k = k;
+    d.k = k;
+    d.winner = win;
+    d.commit_ctx = d.ctx;
+    d.commit_n = k - 1;
+    d.commit_base = (win >= 0) ? nwin + win * S : 0;
+  }
+  // n-gram harvest from the OLD window (layout.py:197-216)
+  for (int j = tid; j < W; j += nth) {
+    int col = j + 1;
+    int* gr = s_grams + j * N;
+    gr[0] = (col == 1) ? d.last : s_oldwin[la_cell_index(0, col, W)];
+    for (int l = 1; l < N - 1; ++l) gr[l] = s_oldwin[la_cell_index(l, col, W)];
+    gr[N - 1] = s_newtop[j];
+  }
+  __syncthreads();
+  // ordered pool insert (pool.py:63-67), one warp, column order
+  if (tid < 32)
+    for (int j = 0; j < W; ++j) la_pool_insert_warp(d.pool, s_grams + j * N, tid, &d.overflow);
+  // window update (layout.py:219-252) with refills from the RNG stream
+  const int sft = s_k - 1;
+  const int v0 = min(sft, W - 1), v1 = min(sft, W);
+  const int cur = d.rng_cur;
+  for (int f = tid; f < ncell; f += nth) {
+    int level, col;
+    la_cell_level_col(f, W, level, col);
+    int sc = col + sft;
+    int val;
+    if (sc <= W) {
+      val = (level + 1 <= N - 2) ? s_oldwin[la_cell_index(level + 1, sc, W)] : s_newtop[sc - 1];
+    } else {
+      int idx = (level == 0) ? (col - max(2, W - sft + 1))
+                             : v0 + (level - 1) * v1 + (col - max(1, W - sft + 1));
+      int r = cur + idx;
+      val = (r < d.rng_len) ? d.rng[r] : 0;
+      if (r >= d.rng_len) d.overflow = 1;
+    }
+    d.window[f] = val;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int k = s_k;
+    d.rng_cur = cur + v0 + (N - 2) * v1;
+    // collect_output: fold accepted tokens, stop at EOS / budget
+    bool stop = false;
+    for (int i = 0; i < k && !stop; ++i) {
+      int t = s_acc[i];
+      d.out[d.n_out] = t;
+      d.n_out += 1;
+      if (d.eos >= 0 && t == d.eos) stop = true;
+      else if (d.n_out >= d.max_tokens) stop = true;
+    }
+    for (int i = 0; i < k; ++i) d.accepted[i] = s_acc[i];
+    int st = d.n_steps;
+    if (st < d.max_steps) {
+      d.rec[st * 4 + 0] = k;
+      d.rec[st * 4 + 1] = c;
+      d.rec[st * 4 + 2] = d.M;
+      d.rec[st * 4 + 3] = d.pool.counters[0];
+    }
+    d.n_steps = st + 1;
+    d.ctx += k;
+    d.last = s_acc[k - 1];
+    if (stop || d.n_steps >= d.max_steps) d.done = 1;
+  }
+  __syncthreads();
+}

@@ -1,0 +1,161 @@
+"""Decode API (drop-in for reference ``decoding.py:96-116,235-255``).
+
+``decode_lookahead`` uploads the prompt, the window's RNG stream and any
+caller pool once, runs every lookahead step on the GPU (device-resident
+window, n-gram pool, KV cache; no token returns to the host inside the
+loop), then reads the tokens, per-step records and pool log once.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections.abc import Sequence
+
+import numpy as np
+
+from . import _lib
+from .analytics import RunMetrics
+from .models import B200Model
+from .pool import NGramPool
+from .types import GenerationConfig, SamplerSpec, StepRecord
+
+
+def window_rng_draws(window: int, ngram: int, max_tokens: int) -> int:
+    """Length of the pre-generated window stream:
+    (N-1)W-1 initial cells plus, per step with shift s <= N-1,
+    min(s, W-1) + (N-2) min(s, W) refills; at most max_tokens steps."""
+    s = ngram - 1
+    per_step = min(s, window - 1) + (ngram - 2) * min(s, window)
+    return (ngram - 1) * window - 1 + max_tokens * per_step
+
+
+def window_rng_stream(seed: int, vocab: int, window: int, ngram: int, max_tokens: int) -> np.ndarray:
+    """``default_rng(seed).integers(0, V, size=R)``: the reference draws the
+    window's cells from one generator (layout.py:117-125, 243-250), and array
+    and scalar ``integers`` calls consume the same stream."""
+    n = window_rng_draws(window, ngram, max_tokens)
+    return np.random.default_rng(seed).integers(0, vocab, size=max(n, 1)).astype(np.int32)
+
+
+def _require_b200(model) -> B200Model:
+    if not isinstance(model, B200Model):
+        raise TypeError("the B200 decode path needs a paper_2402_02057_b200 model "
+                        f"(got {type(model).__name__})")
+    return model
+
+
+def _require_greedy(sampler: SamplerSpec) -> None:
+    if sampler.mode != "greedy":
+        raise NotImplementedError("the B200 engine implements greedy lookahead decoding; "
+                                  "SamplerSpec(mode='temperature') is not on the device path")
+
+
+def _prompt(prompt) -> np.ndarray:
+    if not len(prompt):
+        raise ValueError("prompt must be nonempty")
+    return np.ascontiguousarray(np.asarray([int(t) for t in prompt], dtype=np.int32))
+
+
+class _IO:
+    """Owns the host buffers behind one la_decode_io struct."""
+
+    def __init__(self, prompt: np.ndarray, max_tokens: int, rng: np.ndarray | None = None,
+                 pool_init: np.ndarray | None = None, ngram: int = 2, log_cap: int = 0):
+        P32 = C.POINTER(C.c_int32)
+        self.prompt = prompt
+        self.rng = rng
+        self.pool_init = pool_init
+        self.out = np.zeros(max_tokens, dtype=np.int32)
+        self.rec = np.zeros((max_tokens + 1, 4), dtype=np.int32)
+        self.log = np.zeros((max(log_cap, 1), ngram), dtype=np.int32)
+        io = _lib.la_decode_io()
+        io.prompt = prompt.ctypes.data_as(P32)
+        io.n_prompt = len(prompt)
+        if rng is not None:
+            io.rng_stream = rng.ctypes.data_as(P32)
+            io.rng_len = len(rng)
+        if pool_init is not None and len(pool_init):
+            io.pool_init = pool_init.ctypes.data_as(P32)
+            io.pool_init_n = len(pool_init)
+        io.out_tokens = self.out.ctypes.data_as(P32)
+        io.out_cap = max_tokens
+        io.step_records = self.rec.ctypes.data_as(P32)
+        io.rec_cap = self.rec.shape[0]
+        io.pool_log = self.log.ctypes.data_as(P32)
+        io.pool_log_cap = self.log.shape[0]
+        self.io = io
+
+    def tokens(self) -> list[int]:
+        return [int(t) for t in self.out[: self.io.n_out]]
+
+    def records(self) -> list[StepRecord]:
+        return [StepRecord(*map(int, r)) for r in self.rec[: self.io.n_steps]]
+
+    def stats(self) -> dict:
+        return dict(prefill_ms=float(self.io.prefill_ms), decode_ms=float(self.io.decode_ms),
+                    launches=int(self.io.launches), steps=int(self.io.n_steps),
+                    tokens=int(self.io.n_out))
+
+
+def _gen_config(config: GenerationConfig) -> _lib.la_gen_config:
+    eos = -1 if config.eos_token is None else int(config.eos_token)
+    return _lib.la_gen_config(config.window, config.ngram, config.max_candidates,
+                              config.max_tokens, eos, 1 if config.seed_pool_from_prompt else 0)
+
+
+def _prepare_lookahead(model, prompt, config, sampler, pool):
+    _require_greedy(sampler)
+    p = _prompt(prompt)
+    if pool is not None and pool.ngram != config.ngram:
+        raise ValueError("pool n-gram size does not match the generation config")
+    if pool is not None and pool.capacity is not None:
+        raise NotImplementedError("NGramPool(capacity=...) global LRU eviction is not "
+                                  "implemented on the device pool")
+    init = None
+    if pool is not None and len(pool):
+        init = np.ascontiguousarray(np.asarray(pool.entries_oldest_first(), dtype=np.int32))
+    rng = window_rng_stream(sampler.seed, model.vocab_size, config.window, config.ngram,
+                            config.max_tokens)
+    n_seed = max(0, len(p) - config.ngram + 1) if config.seed_pool_from_prompt else 0
+    log_cap = n_seed + config.max_tokens * config.window + 1
+    io = _IO(p, config.max_tokens, rng, init, config.ngram, log_cap)
+    return io
+
+
+def _finish_lookahead(io: _IO, config: GenerationConfig, pool: NGramPool | None):
+    if pool is not None:
+        n = min(io.io.pool_log_n, io.log.shape[0])
+        pool.insert_all(io.log[:n].tolist())
+    tokens = io.tokens()
+    metrics = RunMetrics.from_records(len(tokens), io.records(), config.ngram)
+    return tokens, metrics
+
+
+def decode_lookahead(model, prompt: Sequence[int], config: GenerationConfig,
+                     sampler: SamplerSpec, pool: NGramPool | None = None):
+    """Greedy lookahead decode on the GPU; returns (tokens, RunMetrics).
+
+    Token-for-token equal to ``decode_autoregressive`` on the same model
+    (exactness guarantee, reference decoding.py:235-241)."""
+    m = _require_b200(model)
+    io = _prepare_lookahead(m, prompt, config, sampler, pool)
+    _lib.check(m.lib.la_decode_lookahead(m.engine(), C.byref(_gen_config(config)),
+                                         C.byref(io.io), m.stream()))
+    m.last_stats = io.stats()
+    return _finish_lookahead(io, config, pool)
+
+
+def decode_autoregressive(model, prompt: Sequence[int], sampler: SamplerSpec, max_tokens: int,
+                          eos_token: int | None = None) -> list[int]:
+    """Plain greedy decoding, one token per step (reference decoding.py:96-116)."""
+    m = _require_b200(model)
+    _require_greedy(sampler)
+    p = _prompt(prompt)
+    if max_tokens < 1:
+        return []      # the reference loop `while len(out) < max_tokens` never runs
+    io = _IO(p, max_tokens)
+    eos = -1 if eos_token is None else int(eos_token)
+    _lib.check(m.lib.la_decode_autoregressive(m.engine(), max_tokens, eos, C.byref(io.io),
+                                              m.stream()))
+    m.last_stats = io.stats()
+    return io.tokens()
