@@ -130,6 +130,12 @@ int32_t la_lp_init(la_engine* e, const void* unique_id, int32_t rank, int32_t wo
 int32_t la_decode_lookahead_group(la_engine* const* engines, int32_t n, const la_gen_config* cfg,
                                   la_decode_io* io, void* stream);
 
+/* ------------------------------------------------------------ debugging */
+/* Copy an engine buffer to host (tests only): what = 0 argmax table
+ * (int32[128]), 1 K cache, 2 V cache ([layer][slot][kv_heads*head_dim]),
+ * 3 device decode state, 4 forward plan.  Synchronises the device. */
+int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

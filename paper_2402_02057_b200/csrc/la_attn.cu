@@ -1,0 +1,295 @@
+// Attention of the step rows (reference models.py:250-260 with the visibility
+// sets of layout.py:139-170), in two kernels:
+//
+//  1. la_attn_prefix_kernel -- every step row sees the whole confirmed prefix
+//     (cache slots [0, ctx)), so that part is plain dense attention:
+//     flash-decoding split over NC key chunks x KV heads x 64-query-row
+//     blocks (GQA groups share the K/V tile), mma.sync bf16 tensor-core QK^T
+//     and PV with an online softmax; emits unnormalised partial O + (m, l).
+//  2. la_attn_chain_kernel -- merges the chunk partials in fixed order, then
+//     walks the row's chain of visible step keys in relative-position order
+//     (the paper's structured mask, generated per row from the plan -- never
+//     materialised) and finally the row itself.
+//
+// Both are layout-independent per row: a row's result depends only on ctx
+// and its own token chain, so lookahead-parallel shards reproduce the
+// single-device outputs bit for bit.
+#include <cuda_bf16.h>
+
+#include "la_attn.cuh"
+#include "la_common.cuh"
+
+namespace {
+
+constexpr int kKeyTile = 64;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// [rows][128] bf16 tile, 16-byte chunks XOR-swizzled by (row & 7)
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * 256 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+  int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// keys per prefix chunk: ceil(ctx / NC) rounded up to the key tile; depends
+// on ctx only, so every shard of a step chunks the prefix identically
+__device__ __forceinline__ int chunk_keys(int ctx, int NC) {
+  return ((ctx + NC - 1) / NC + kKeyTile - 1) / kKeyTile * kKeyTile;
+}
+
+}  // namespace
+
+size_t la_attn_prefix_smem() { return 64 * 256 + 4 * kKeyTile * 256; }
+
+// grid = (KVH, NC, row blocks of 64 flattened (row, head-in-group) queries)
+__global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
+  const FwdPlan* P = a.plan;
+  const int n_rows = P->n_rows, ctx = P->n_prefix;
+  if (n_rows == 0 || ctx == 0) return;
+  const int g = a.H / a.KVH;
+  const int kvh = blockIdx.x, c = blockIdx.y, rb = blockIdx.z;
+  const int nq = n_rows * g;
+  if (rb * 64 >= nq) return;
+  const int CH = chunk_keys(ctx, a.NC);
+  const int k_begin = c * CH;
+  if (k_begin >= ctx) return;
+  const int k_end = min(ctx, k_begin + CH);
+
+  extern __shared__ __align__(128) uint8_t attn_smem[];
+  uint8_t* sQ = attn_smem;
+  uint8_t* sK[2] = {sQ + 64 * 256, sQ + 64 * 256 + kKeyTile * 256};
+  uint8_t* sV[2] = {sQ + 64 * 256 + 2 * kKeyTile * 256, sQ + 64 * 256 + 3 * kKeyTile * 256};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t kv_ld = (size_t)a.KVH * 128;
+
+  // ---- Q tile (64 query rows x 128 dims)
+  for (int i = tid; i < 64 * 16; i += 128) {
+    int row = i >> 4, ch = i & 15, qr = rb * 64 + row;
+    const __nv_bfloat16* src = a.q;
+    bool ok = qr < nq;
+    if (ok) {
+      int r = qr / g, h = kvh * g + qr % g;
+      src = a.q + ((size_t)r * a.H + h) * 128 + ch * 8;
+    }
+    cp_async16(smem_u32(sQ) + swz(row, ch), src, ok);
+  }
+  auto load_kv = [&](int buf, int t0) {
+    for (int i = tid; i < kKeyTile * 16; i += 128) {
+      int row = i >> 4, ch = i & 15, key = t0 + row;
+      bool ok = key < k_end;
+      size_t off = ((size_t)(ok ? key : k_begin) * kv_ld) + kvh * 128 + ch * 8;
+      cp_async16(smem_u32(sK[buf]) + swz(row, ch), a.kc + off, ok);
+      cp_async16(smem_u32(sV[buf]) + swz(row, ch), a.vc + off, ok);
+    }
+  };
+  load_kv(0, k_begin);
+  cp_commit();
+
+  uint32_t qf[8][4];
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float sl2 = a.scale * kLog2e;
+  const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+
+  for (int t = 0; t < n_tiles; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < n_tiles) load_kv(buf ^ 1, k_begin + (t + 1) * kKeyTile);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        int row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        int ch = kk * 2 + (lane >> 4);
+        ldsm_x4(smem_u32(sQ) + swz(row, ch), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+      }
+    }
+    // S = Q K^T (16 rows x 64 keys per warp)
+    float s[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        int key = np * 16 + (lane & 7) + (lane >> 4) * 8;
+        int ch = kk * 2 + ((lane >> 3) & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(smem_u32(sK[buf]) + swz(key, ch), b0, b1, b2, b3);
+        mma16816(s[2 * np], qf[kk], b0, b1);
+        mma16816(s[2 * np + 1], qf[kk], b2, b3);
+      }
+    }
+    // mask keys past the chunk end, scale into log2 units
+    const int kbase = k_begin + t * kKeyTile;
+    float mx0 = m0, mx1 = m1;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int key = kbase + n * 8 + (lane & 3) * 2 + (e & 1);
+        float v = key < k_end ? s[n][e] * sl2 : -INFINITY;
+        s[n][e] = v;
+      }
+      mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
+      mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    const float al0 = exp2f(m0 - mx0), al1 = exp2f(m1 - mx1);
+    m0 = mx0;
+    m1 = mx1;
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      s[n][0] = exp2f(s[n][0] - m0);
+      s[n][1] = exp2f(s[n][1] - m0);
+      s[n][2] = exp2f(s[n][2] - m1);
+      s[n][3] = exp2f(s[n][3] - m1);
+      rs0 += s[n][0] + s[n][1];
+      rs1 += s[n][2] + s[n][3];
+    }
+    l0 = l0 * al0 + rs0;
+    l1 = l1 * al1 + rs1;
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      o[d][0] *= al0; o[d][1] *= al0; o[d][2] *= al1; o[d][3] *= al1;
+    }
+    // O += P V
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      uint32_t pa[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]), pack_bf16(s[2 * kk][2], s[2 * kk][3]),
+                        pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                        pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+      for (int dp = 0; dp < 8; ++dp) {
+        int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        int ch = dp * 2 + (lane >> 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(smem_u32(sV[buf]) + swz(key, ch), b0, b1, b2, b3);
+        mma16816(o[2 * dp], pa, b0, b1);
+        mma16816(o[2 * dp + 1], pa, b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+  // row sums across the 4 lanes of a row
+#pragma unroll
+  for (int off = 1; off <= 2; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  // write unnormalised partial O and (m, l) in log2 units
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    int qr = rb * 64 + warp * 16 + (lane >> 2) + half * 8;
+    if (qr >= nq) continue;
+    int r = qr / g, h = kvh * g + qr % g;
+    size_t base = ((size_t)c * LA_MAX_ROWS + r) * a.H + h;
+    float* dst = a.part_o + base * 128;
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      int col = d * 8 + (lane & 3) * 2;
+      *reinterpret_cast<float2*>(dst + col) =
+          make_float2(o[d][half * 2 + 0], o[d][half * 2 + 1]);
+    }
+    if ((lane & 3) == 0) a.part_ml[base] = make_float2(half ? m1 : m0, half ? l1 : l0);
+  }
+}
+
+// grid = n rows (LA_MAX_ROWS), block = 512 (16 warps loop over heads)
+__global__ void __launch_bounds__(512) la_attn_chain_kernel(LaAttnArgs a) {
+  const FwdPlan* P = a.plan;
+  const int r = blockIdx.x;
+  if (r >= P->n_rows) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int ctx = P->n_prefix, g = a.H / a.KVH;
+  const int n_chunks = ctx == 0 ? 0 : (ctx + chunk_keys(ctx, a.NC) - 1) / chunk_keys(ctx, a.NC);
+  const float sl2 = a.scale * kLog2e;
+  const size_t kv_ld = (size_t)a.KVH * 128;
+  const int nch = P->chain_n[r];
+  for (int h = warp; h < a.H; h += nw) {
+    const int kvh = h / g;
+    float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < n_chunks; ++c) {
+      size_t base = ((size_t)c * LA_MAX_ROWS + r) * a.H + h;
+      float2 ml = a.part_ml[base];
+      float4 po = reinterpret_cast<const float4*>(a.part_o + base * 128)[lane];
+      float mn = fmaxf(m, ml.x);
+      float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
+      o[0] = o[0] * s0 + po.x * s1;
+      o[1] = o[1] * s0 + po.y * s1;
+      o[2] = o[2] * s0 + po.z * s1;
+      o[3] = o[3] * s0 + po.w * s1;
+      l = l * s0 + ml.y * s1;
+      m = mn;
+    }
+    const __nv_bfloat16* qp = a.q + ((size_t)r * a.H + h) * 128 + lane * 4;
+    float2 q01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp));
+    float2 q23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp + 2));
+    for (int j = 0; j <= nch; ++j) {
+      const int slot = j < nch ? P->chain[r][j] : P->slot[r];
+      const size_t off = (size_t)slot * kv_ld + kvh * 128 + lane * 4;
+      float2 k01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.kc + off));
+      float2 k23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.kc + off + 2));
+      float dot = q01.x * k01.x + q01.y * k01.y + q23.x * k23.x + q23.y * k23.y;
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, sh);
+      const float sc = dot * sl2;
+      float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.vc + off));
+      float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.vc + off + 2));
+      float mn = fmaxf(m, sc);
+      float s0 = exp2f(m - mn), s1 = exp2f(sc - mn);
+      o[0] = o[0] * s0 + v01.x * s1;
+      o[1] = o[1] * s0 + v01.y * s1;
+      o[2] = o[2] * s0 + v23.x * s1;
+      o[3] = o[3] * s0 + v23.y * s1;
+      l = l * s0 + s1;
+      m = mn;
+    }
+    const float inv = 1.0f / l;
+    __nv_bfloat16* dst = a.out + (size_t)r * a.H * 128 + h * 128 + lane * 4;
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(o[0] * inv, o[1] * inv),
+                                                pack_bf16(o[2] * inv, o[3] * inv));
+  }
+}

@@ -1,0 +1,20 @@
+// Step-row attention kernels (la_attn.cu).
+#pragma once
+#include <cuda_bf16.h>
+
+#include "la_common.cuh"
+
+struct LaAttnArgs {
+  const FwdPlan* plan;
+  const __nv_bfloat16* q;        // [LA_MAX_ROWS][H][128] (RoPE applied)
+  const __nv_bfloat16 *kc, *vc;  // layer base, [slots][KVH][128]
+  float* part_o;                 // [NC][LA_MAX_ROWS][H][128]
+  float2* part_ml;               // [NC][LA_MAX_ROWS][H]  (max, sum) in log2 units
+  __nv_bfloat16* out;            // [LA_MAX_ROWS][H*128]
+  int H, KVH, NC;
+  float scale;                   // 1/sqrt(head_dim)
+};
+
+__global__ void la_attn_prefix_kernel(LaAttnArgs a);
+__global__ void la_attn_chain_kernel(LaAttnArgs a);
+size_t la_attn_prefix_smem();

@@ -577,3 +577,23 @@ extern "C" int32_t la_decode_lookahead_group(la_engine* const* es, int32_t n,
   for (int r = 0; r < n; ++r) { es[r]->rank = 0; es[r]->world = 1; }
   return rc;
 }
+
+// ------------------------------------------------------------ debug copy
+extern "C" int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t bytes) {
+  if (!e || !host) { la_set_error("null engine or buffer"); return LA_ERR_INVALID_CONFIG; }
+  CK(cudaSetDevice(e->device));
+  CK(cudaDeviceSynchronize());
+  const void* src = nullptr;
+  size_t avail = 0;
+  const size_t kv = (size_t)e->desc.layers * e->slots * e->row_bytes;
+  switch (what) {
+    case 0: src = e->d_amax; avail = LA_MAX_ROWS * sizeof(int); break;
+    case 1: src = e->kc; avail = kv; break;
+    case 2: src = e->vc; avail = kv; break;
+    case 3: src = e->d_dec; avail = sizeof(DevDecode); break;
+    case 4: src = e->d_plan; avail = sizeof(FwdPlan); break;
+    default: la_set_error("unknown debug buffer %d", what); return LA_ERR_INVALID_CONFIG;
+  }
+  CK(cudaMemcpy(host, src, std::min<size_t>(avail, (size_t)bytes), cudaMemcpyDeviceToHost));
+  return LA_OK;
+}

@@ -11,5 +11,6 @@ __global__ void la_kv_commit_kernel(const DevDecode* dp, uint8_t* kc, uint8_t* v
                                     int slots, int row_bytes);
 __global__ void la_kv_pack_kernel(const DevDecode* dp, const uint8_t* kc, const uint8_t* vc,
                                   uint8_t* send, int layers, int slots, int row_bytes);
-__global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered, uint8_t* kc,
-                                    uint8_t* vc, int layers, int slots, int row_bytes);
+__global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered, size_t seg,
+                                    uint8_t* kc, uint8_t* vc, int layers, int slots,
+                                    int row_bytes);

@@ -12,6 +12,7 @@
 // Transport: NCCL over NVLink for one process per GPU (la_lp_init), or a
 // device copy between engines of one process (la_decode_lookahead_group,
 // the reference's in-process simulation).
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -24,6 +25,47 @@
 struct LpComm {
   ncclComm_t comm = nullptr;
 };
+
+// NCCL is resolved at la_lp_init time (dlopen), not at library load: the
+// process usually already holds torch's libnccl.so.2, which must win, and
+// single-GPU users never need NCCL at all.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  if (api.ok) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
+           api.GetErrorString;
+  return api;
+}
+
+#define ncclGetUniqueId nccl().GetUniqueId
+#define ncclCommInitRank nccl().CommInitRank
+#define ncclCommDestroy nccl().CommDestroy
+#define ncclAllGather nccl().AllGather
+#define ncclGetErrorString nccl().GetErrorString
+
+static int need_nccl() {
+  if (!nccl().ok) { la_set_error("libnccl.so.2 could not be loaded"); return LA_ERR_NCCL; }
+  return LA_OK;
+}
 
 #define NCK(x)                                                                   \
   do {                                                                           \
@@ -66,6 +108,7 @@ int lp_buffers(la_engine* e, int world) {
 
 extern "C" int32_t la_lp_unique_id(void* out) {
   if (!out) { la_set_error("null output"); return LA_ERR_INVALID_CONFIG; }
+  if (int rc = need_nccl()) return rc;
   ncclUniqueId id;
   NCK(ncclGetUniqueId(&id));
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -79,6 +122,7 @@ extern "C" int32_t la_lp_init(la_engine* e, const void* unique_id, int32_t rank,
   CK(cudaSetDevice(e->device));
   lp_destroy(e);
   if (world > 1) {
+    if (int rc = need_nccl()) return rc;
     e->lp = new LpComm();
     ncclUniqueId id;
     memcpy(&id, unique_id, sizeof(id));
@@ -111,7 +155,7 @@ static int step_finish(la_engine* e, const int* gathered_amax, int world, cudaSt
 }
 
 static int step_unpack(la_engine* e, cudaStream_t st) {
-  la_kv_unpack_kernel<<<64, 256, 0, st>>>(e->d_dec, e->kv_recv, (uint8_t*)e->kc, (uint8_t*)e->vc,
+  la_kv_unpack_kernel<<<64, 256, 0, st>>>(e->d_dec, e->kv_recv, e->kv_seg, (uint8_t*)e->kc, (uint8_t*)e->vc,
                                           e->desc.layers, e->slots, e->row_bytes);
   CK(cudaGetLastError());
   return LA_OK;

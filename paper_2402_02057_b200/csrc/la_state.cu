@@ -95,12 +95,12 @@ __global__ void la_kv_pack_kernel(const DevDecode* dp, const uint8_t* kc, const 
 }
 
 // LP: every rank writes the owner's gathered rows into slots ctx+1 .. ctx+n.
-__global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered, uint8_t* kc,
-                                    uint8_t* vc, int layers, int slots, int row_bytes) {
+__global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered, size_t seg,
+                                    uint8_t* kc, uint8_t* vc, int layers, int slots,
+                                    int row_bytes) {
   const DevDecode& d = *dp;
   if (d.mode != LA_MODE_LOOKAHEAD || d.commit_n <= 0 || d.winner < 0) return;
   const int S = d.N - 1, n = d.commit_n, owner = d.winner % d.world;
-  const size_t seg = (size_t)layers * S * 2 * row_bytes;
   const uint8_t* src_base = gathered + (size_t)owner * seg;
   const int per = row_bytes / 16;
   const long total = (long)layers * n * 2 * per;
