@@ -157,8 +157,9 @@ class LlamaOracle:
         w = self.w
         T = x.shape[0]
         h = self._r(self._rms(x, w[f"{i}.attn_norm"]))
-        q = self._r(h @ w[f"{i}.wq"].T).reshape(T, c["heads"], c["head_dim"])
-        k = self._r(h @ w[f"{i}.wk"].T).reshape(T, c["kv_heads"], c["head_dim"])
+        # the device applies RoPE to the fp32 accumulator and stores bf16 once
+        q = (h @ w[f"{i}.wq"].T).reshape(T, c["heads"], c["head_dim"])
+        k = (h @ w[f"{i}.wk"].T).reshape(T, c["kv_heads"], c["head_dim"])
         v = self._r(h @ w[f"{i}.wv"].T).reshape(T, c["kv_heads"], c["head_dim"])
         q = self._r(self._rope(q, pos))
         k = self._r(self._rope(k, pos))
@@ -228,13 +229,16 @@ class LlamaOracle:
         return [int(np.argmax(l)) for l in self.logits_rows(prefix, rows)]
 
 
-def llama_random_weights(cfg: dict, seed: int = 0, std: float = 0.02) -> dict:
-    """bf16-representable float32 weights for tiny oracle checks."""
+def llama_random_weights(cfg: dict, seed: int = 0, std: float | None = 0.02) -> dict:
+    """bf16-representable float32 weights for tiny oracle checks.
+    std=None draws each matrix with std 1/sqrt(in_features)."""
     rng = np.random.default_rng(seed)
     d, hd = cfg["dim"], cfg["head_dim"]
     H, KVH, F, V = cfg["heads"], cfg["kv_heads"], cfg["ffn"], cfg["vocab"]
 
-    def mat(o, i, s=std):
+    def mat(o, i, s=None):
+        if s is None:
+            s = std if std is not None else 1.0 / np.sqrt(i)
         return bf16_round(rng.normal(0.0, s, size=(o, i)).astype(np.float32))
 
     w = {"embed": mat(V, d, 1.0), "lm_head": mat(V, d),

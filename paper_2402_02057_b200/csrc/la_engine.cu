@@ -444,7 +444,10 @@ static int run_decode(la_engine* e, const DecodeArgs& a, la_decode_io* io, void*
   }
   CK(cudaEventRecord(e->ev[2], st));
   io->launches = launches;
-  return readback(e, io, st);
+  RET_IF(readback(e, io, st));
+  // graph-launched decodes report kernels per step (negative): scale by steps
+  if (io->launches < 0) io->launches = -io->launches * io->n_steps;
+  return LA_OK;
 }
 
 extern "C" int32_t la_decode_lookahead(la_engine* e, const la_gen_config* cfg, la_decode_io* io,

@@ -37,3 +37,12 @@ def cuda_ok():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def pytest_collection_modifyitems(config, items):
+    if cuda_ok():
+        return
+    skip = pytest.mark.skip(reason="needs a CUDA device")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)

@@ -1,0 +1,136 @@
+"""GPU parity of the bf16 tcgen05 path (BASELINE configs 2-5 model family)
+against the CPU Llama oracle (bf16-emulating fp32 restatement).
+
+Tolerances (north_star): logits within 1e-2 relative for bf16; token
+divergence from the oracle is tolerated only where the oracle's top-2 logit
+margin is below that tolerance (documented near ties)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+la = pytest.importorskip("paper_2402_02057_b200")
+
+from oracle import lookahead_oracle as lo  # noqa: E402
+from oracle.model_oracle import LlamaOracle, llama_random_weights  # noqa: E402
+
+REL_TOL = 1e-2
+
+CONFIGS = {
+    # GQA, vocab not a multiple of 128 (TMA out-of-bounds rows), tiny K: every
+    # GEMM tile is split across CTAs (stream-K fix-up path)
+    "gqa": dict(dim=256, layers=2, heads=4, kv_heads=2, head_dim=128, ffn=512, vocab=1000,
+                rope_theta=10000.0, eps=1e-5),
+    # wide vocabulary: many CTAs own whole LM-head tiles (direct epilogue path)
+    "wide": dict(dim=256, layers=1, heads=2, kv_heads=2, head_dim=128, ffn=768, vocab=32000,
+                 rope_theta=10000.0, eps=1e-5),
+}
+
+
+def _make(name, max_context=1024):
+    cfg = CONFIGS[name]
+    w = llama_random_weights(cfg, seed=1, std=None)
+    lc = la.LlamaConfig(dim=cfg["dim"], layers=cfg["layers"], heads=cfg["heads"],
+                        kv_heads=cfg["kv_heads"], ffn=cfg["ffn"], vocab=cfg["vocab"],
+                        head_dim=128, rope_theta=cfg["rope_theta"], norm_eps=cfg["eps"])
+    m = la.LlamaModel(lc, dtype="bf16", weights=w, max_context=max_context)
+    return m, LlamaOracle(cfg, w, emulate_bf16=True)
+
+
+@pytest.fixture(scope="module", params=list(CONFIGS))
+def pair(request):
+    m, o = _make(request.param)
+    yield request.param, m, o
+    m.close()
+
+
+def _rel_err(got, ref):
+    return np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-6)
+
+
+def _step_layout(rows):
+    return la.StepLayout(queries=[la.QueryToken(rows.ids[i], rows.rel[i], tuple(rows.chains[i]))
+                                  for i in range(len(rows))])
+
+
+def test_logits_chain_layout(pair):
+    name, m, orc = pair
+    V = orc.vocab_size
+    prompt = [int(t) for t in np.random.default_rng(3).integers(0, V, 40)]
+    lay = la.chain_layout(prompt[-1], [])
+    got = m.logits(prompt[:-1], lay)[0]
+    rows = lo.Rows([prompt[-1]], [0], [[]], [], [])
+    ref = orc.logits_rows(prompt[:-1], rows)[0]
+    assert _rel_err(got, ref) < REL_TOL, _rel_err(got, ref)
+
+
+def test_logits_lookahead_layout(pair):
+    """Structured mask (window + branches) on the device == per-row chains."""
+    name, m, orc = pair
+    V = orc.vocab_size
+    rng = np.random.default_rng(5)
+    prompt = [int(t) for t in rng.integers(0, V, 200)]
+    W, N = 5, 4
+    window = [int(t) for t in rng.integers(0, V, (N - 1) * W - 1)]
+    sufs = [tuple(int(t) for t in rng.integers(0, V, N - 1)) for _ in range(3)]
+    rows = lo.build_rows(window, W, N, prompt[-1], sufs)
+    got = m.logits(prompt[:-1], _step_layout(rows))
+    ref = np.stack(orc.logits_rows(prompt[:-1], rows))
+    for i in range(len(rows)):
+        assert _rel_err(got[i], ref[i]) < REL_TOL, (i, _rel_err(got[i], ref[i]))
+
+
+def test_prefill_longer_than_one_chunk(pair):
+    name, m, orc = pair
+    V = orc.vocab_size
+    prompt = [int(t) for t in np.random.default_rng(8).integers(0, V, 300)]
+    got = m.logits(prompt[:-1], la.chain_layout(prompt[-1], [7 % V, 9 % V]))
+    rows = lo.Rows([prompt[-1], 7 % V, 9 % V], [0, 1, 2], [[], [0], [0, 1]], [], [])
+    ref = np.stack(orc.logits_rows(prompt[:-1], rows))
+    assert _rel_err(got, ref) < REL_TOL
+
+
+def test_lookahead_equals_greedy_on_device(pair):
+    """Exactness: lookahead tokens == the same GPU's plain greedy decode."""
+    name, m, orc = pair
+    V = orc.vocab_size
+    prompt = [int(t) for t in np.random.default_rng(11).integers(0, V, 64)]
+    ar = la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), 48)
+    for W, N, G in [(5, 3, 5), (15, 5, 15), (7, 4, 3)]:
+        cfg = la.GenerationConfig(window=W, ngram=N, max_candidates=G, max_tokens=48,
+                                  seed_pool_from_prompt=True)
+        toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=1))
+        assert toks == ar, (name, W, N, G)
+        assert met.tokens_generated == 48
+
+
+def test_greedy_matches_oracle_except_near_ties(pair):
+    name, m, orc = pair
+    V = orc.vocab_size
+    prompt = [int(t) for t in np.random.default_rng(12).integers(0, V, 24)]
+    got = la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), 12)
+    seq = list(prompt)
+    for i, t in enumerate(got):
+        rows = lo.Rows([seq[-1]], [0], [[]], [], [])
+        lg = orc.logits_rows(seq[:-1], rows)[0]
+        top = int(np.argmax(lg))
+        if top != t:
+            srt = np.sort(lg)
+            margin = (srt[-1] - srt[-2]) / max(np.abs(lg).max(), 1e-6)
+            assert margin < REL_TOL, (i, t, top, margin)
+            break   # sequences diverge after a documented near tie
+        seq.append(t)
+
+
+def test_lp_group_bit_identical(pair):
+    name, m, orc = pair
+    V = orc.vocab_size
+    prompt = [int(t) for t in np.random.default_rng(13).integers(0, V, 32)]
+    cfg = la.GenerationConfig(window=8, ngram=4, max_candidates=8, max_tokens=40,
+                              seed_pool_from_prompt=True)
+    t1, m1 = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=2))
+    for D in (2, 4):
+        tD, mD, comm = la.decode_lookahead_devices(m, prompt, cfg, la.SamplerSpec("greedy", seed=2), D)
+        assert tD == t1 and mD.steps == m1.steps
+        assert comm.sync_events == mD.steps
