@@ -130,6 +130,15 @@ int32_t la_lp_init(la_engine* e, const void* unique_id, int32_t rank, int32_t wo
 int32_t la_decode_lookahead_group(la_engine* const* engines, int32_t n, const la_gen_config* cfg,
                                   la_decode_io* io, void* stream);
 
+/* ------------------------------------------------------------ profiling */
+/* Per-launch device time of the bf16 path's tcgen05 GEMMs, accumulated in
+ * the kernels themselves (globaltimer, first CTA start -> last CTA end) over
+ * every launch since the last reset.  out16[4*k + 0] = summed ns,
+ * out16[4*k + 1] = launches, for k = 0 QKV, 1 O/down (residual), 2 gate/up,
+ * 3 LM head. */
+int32_t la_gemm_timing_reset(la_engine* e);
+int32_t la_gemm_timing_read(la_engine* e, double* out16);
+
 /* ------------------------------------------------------------ debugging */
 /* Copy an engine buffer to host (tests only): what = 0 argmax table
  * (int32[128]), 1 K cache, 2 V cache ([layer][slot][kv_heads*head_dim]),

@@ -28,6 +28,12 @@ constexpr int kTmemCols = 256;
 constexpr size_t kSmemBytes =
     1024 + kStages * (kABytes + kBBytes) + 128 * kEpiLd * 4 + 2 * kStages * 8 + 4 * 8 + 16;
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ long cta_of(long u, long U, long P) { return ((u + 1) * P + U - 1) / U - 1; }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -156,6 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (args.timing && threadIdx.x == 0) {
+    if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
@@ -316,6 +325,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem);
+  }
+  if (args.timing && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&args.timing[4], 1ull) == (unsigned long long)gridDim.x - 1) {
+      unsigned long long t1 = globaltimer();
+      args.timing[1] += t1 - args.timing[0];
+      args.timing[2] += 1;
+      args.timing[3] = 0;
+      args.timing[4] = 0;
+    }
   }
 }
 

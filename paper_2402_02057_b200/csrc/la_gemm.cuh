@@ -45,6 +45,9 @@ struct LaGemmArgs {
   float2* pmax;                  // [n_tiles][128] (max, index-as-float-bits)
   float* logits;                 // [128][V] or null
   int V;
+  // launch timing (device globaltimer): [0] first-CTA start, [1] sum ns,
+  // [2] launches, [3] started CTAs, [4] finished CTAs; null = off
+  unsigned long long* timing;
 };
 
 // Host-side descriptor of one GEMM (tensor maps + args), built once per

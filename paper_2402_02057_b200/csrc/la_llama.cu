@@ -43,6 +43,7 @@ struct LlamaPath {
   float2* part_ml = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* row_amax = nullptr;
+  unsigned long long* timing = nullptr;   // [4 epilogue kinds][8]
   float* logits = nullptr;   // device dump target (parity hook), else null
   std::vector<LaGemm> qkv, o, gu, down;
   LaGemm head{};
@@ -261,8 +262,10 @@ int llama_create(la_engine* e) {
   p->head.args.V = D.vocab;
   RET_IF(lalloc(e, &p->ws, ws_need));
   RET_IF(lalloc(e, &p->counters, max_tiles + 1));
+  RET_IF(lalloc(e, &p->timing, 32));
   auto fin = [&](LaGemm& gg) {
     gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.counters = p->counters;
+    gg.args.timing = p->timing + 8 * gg.epi;
   };
   for (int l = 0; l < D.layers; ++l) { fin(p->qkv[l]); fin(p->o[l]); fin(p->gu[l]); fin(p->down[l]); }
   fin(p->head);
@@ -436,5 +439,27 @@ int llama_step_forward(la_engine* e, cudaStream_t st) {
     p->fwd_graph = g;
   }
   CK(cudaGraphLaunch(p->fwd_exec, st));
+  return LA_OK;
+}
+
+// ------------------------------------------------------- GEMM timing ABI
+extern "C" int32_t la_gemm_timing_reset(la_engine* e) {
+  if (!e || !e->llama) { la_set_error("no bf16 path on this engine"); return LA_ERR_INVALID_CONFIG; }
+  CK(cudaSetDevice(e->device));
+  CK(cudaMemset(e->llama->timing, 0, 32 * sizeof(unsigned long long)));
+  return LA_OK;
+}
+
+extern "C" int32_t la_gemm_timing_read(la_engine* e, double* out16) {
+  if (!e || !e->llama || !out16) { la_set_error("no bf16 path on this engine"); return LA_ERR_INVALID_CONFIG; }
+  CK(cudaSetDevice(e->device));
+  unsigned long long t[32];
+  CK(cudaMemcpy(t, e->llama->timing, sizeof(t), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 4; ++k) {
+    out16[4 * k + 0] = (double)t[8 * k + 1];   // summed ns
+    out16[4 * k + 1] = (double)t[8 * k + 2];   // launches
+    out16[4 * k + 2] = 0.0;
+    out16[4 * k + 3] = 0.0;
+  }
   return LA_OK;
 }
