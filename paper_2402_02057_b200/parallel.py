@@ -49,6 +49,39 @@ def column_ranges(window: int, devices: int) -> list[range]:
     return out
 
 
+def shard_rows(window: int, ngram: int, candidates: int, rank: int, world: int):
+    """Host mirror of the device row plan (``la_lp_row_role``, la_state.cuh):
+    (computed rows, owned rows) of ``rank`` for a step with ``candidates``
+    branches, in global row order (SURVEY appendix A.1 geometry).
+
+    Owned rows are disjoint across ranks and cover the layout; computed rows
+    add query 0 and the oldest-level cells left of the rank's columns, which
+    makes every shard closed under visibility (reference parallel.py:88-98)."""
+    W, N = window, ngram
+    cols = column_ranges(W, world)[rank]
+    c0, c1 = cols.start, cols.stop - 1
+    nwin = (N - 1) * W
+    computed, owned = [], []
+    for g in range(nwin + candidates * (N - 1)):
+        if g == 0:
+            comp, own = True, rank == 0
+        elif g < nwin:
+            f = g - 1
+            if f < W - 1:
+                level, col = 0, f + 2
+            else:
+                level, col = 1 + (f - (W - 1)) // W, 1 + (f - (W - 1)) % W
+            own = c0 <= col <= c1
+            comp = own or (level == 0 and col < c0)
+        else:
+            comp = own = ((g - nwin) // (N - 1)) % world == rank
+        if comp:
+            computed.append(g)
+        if own:
+            owned.append(g)
+    return computed, owned
+
+
 def step_comm(window: int, ngram: int, devices: int, candidates: int) -> CommStats:
     """Per-step accounting: each device sends one token per owned column and
     N values per owned candidate to the D-1 peers (parallel.py:164,168)."""
@@ -66,6 +99,13 @@ def _dist_world():
     return None, 0, 1
 
 
+def broadcast_unique_id(uid, group=None) -> bytes:
+    """Rank 0's 128-byte NCCL id to every rank over the job's process group."""
+    import torch.distributed as dist
+    dist.broadcast(uid, src=0, group=group)
+    return bytes(uid.cpu().tolist())
+
+
 def lp_init(model, group=None):
     """Create the model's NCCL LP communicator from the torch.distributed job."""
     import torch
@@ -80,8 +120,7 @@ def lp_init(model, group=None):
         uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
     if dist.get_backend(group) == "nccl":
         uid = uid.cuda(m.device)
-    dist.broadcast(uid, src=0, group=group)
-    raw = bytes(uid.cpu().tolist())
+    raw = broadcast_unique_id(uid, group)
     _lib.check(m.lib.la_lp_init(m.engine(), C.c_char_p(raw), rank, world))
     m._lp_world = world
 
