@@ -290,11 +290,17 @@ def run_ours(args):
     step_gbs = step_bytes / (ms_step * 1e-3) / 1e9
     # dominant kernel: gate/up GEMM, algorithmic bytes = its weights + rows
     gu_bytes = 2 * cfg.ffn * cfg.dim * 2 + mean_M * cfg.dim * 2 + mean_M * cfg.ffn * 2
-    gu_ns, gu_n = tim[4], tim[5]
+    gu_ns, gu_n = tim[8], tim[9]        # kind 2 = gate/up (la_gemm_timing_read)
     gu_ms = (gu_ns / gu_n) * 1e-6 if gu_n else None
     achieved = gu_bytes / (gu_ms * 1e-3) / 1e9 if gu_ms else None
     h2d = 4 * PROMPT_LEN + 4 * dec.window_rng_draws(W, N, NEW_TOKENS)
     d2h = 4 * NEW_TOKENS + 16 * (NEW_TOKENS + 1) + 4 * N * (NEW_TOKENS * W + 1) + 512
+    # plain greedy on the same GPU (the exactness baseline and the LA-step bar)
+    ar_ms_step = None
+    if world == 1:
+        ar_toks = la.decode_autoregressive(model, prompt, sampler, 128)
+        ar_ms_step = model.last_stats["decode_ms"] / max(1, model.last_stats["steps"])
+        ar_match = ar_toks == toks_all[0][:128]
     cpu = None
     if world == 1 and not args.no_cpu:
         cpu = cpu_reference_sample(cfg, int(ctx_mean), mean_M, S, budget_s=10.0)
@@ -324,6 +330,9 @@ def run_ours(args):
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
         "prefill_ms": statistics.mean(s["prefill_ms"] for s in stats),
+        "greedy": ({"ms_per_step": ar_ms_step, "tokens_per_s": 1e3 / ar_ms_step,
+                    "la_step_over_greedy_step": ms_step / ar_ms_step,
+                    "first_128_tokens_equal_lookahead": ar_match} if ar_ms_step else None),
     }
     print(json.dumps(out))
     model.close()

@@ -49,11 +49,26 @@ typedef struct la_model_desc {
 } la_model_desc;
 
 /* Number of weight tensors and the name of tensor i, in the order la_create
- * expects their device pointers.  Matrices are row-major [out][in]; fp32 for
- * the *_F32 archs, bf16 for LA_ARCH_LLAMA_BF16; norm vectors are fp32.
- * Replaces the reference's in-object numpy weights (models.py:219-242). */
+ * expects their device pointers.  fp32 archs: row-major [out][in] matrices.
+ * LA_ARCH_LLAMA_BF16: the embedding is row-major [vocab][dim] bf16; every
+ * projection ("*_tiles") is in the packed LA-tile layout produced by
+ * la_pack_weight (q/k/v stacked into one matrix, gate/up interleaved per
+ * 64 rows); norm vectors are fp32.  Replaces the reference's in-object numpy
+ * weights (models.py:219-242). */
 int32_t la_weight_count(const la_model_desc* desc);
 const char* la_weight_name(const la_model_desc* desc, int32_t i);
+
+/* Packed LA-tile layout of a bf16 [rows][K] matrix (K % 64 == 0): 128-row x
+ * 64-column blocks, 16 KB each, tile-major / k-minor, every block stored as
+ * its 128-byte-swizzled shared-memory image so the GEMM streams it with one
+ * contiguous bulk copy.  la_packed_bytes: size of the packed matrix (rows
+ * rounded up to 128; zero the buffer before packing partial tiles).
+ * la_pack_weight: pack device matrix src into dst at virtual row offset
+ * `row_offset` (mode 0), or as the gate (mode 1) / up (mode 2) half of an
+ * interleaved gate/up matrix. */
+int64_t la_packed_bytes(int32_t rows, int32_t K);
+int32_t la_pack_weight(const void* src, int32_t rows, int32_t K, void* dst, int32_t mode,
+                       int32_t row_offset, void* stream);
 
 typedef struct la_engine la_engine;
 
@@ -142,7 +157,9 @@ int32_t la_gemm_timing_read(la_engine* e, double* out16);
 /* ------------------------------------------------------------ debugging */
 /* Copy an engine buffer to host (tests only): what = 0 argmax table
  * (int32[128]), 1 K cache, 2 V cache ([layer][slot][kv_heads*head_dim]),
- * 3 device decode state, 4 forward plan.  Synchronises the device. */
+ * 3 device decode state, 4 forward plan, 5 per-CTA GEMM trace of the last
+ * launch of each GEMM kind (needs LA_GEMM_TRACE=1 at engine creation:
+ * uint64[4 kinds][256 CTAs][4] globaltimer stamps).  Synchronises the device. */
 int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t bytes);
 
 #ifdef __cplusplus

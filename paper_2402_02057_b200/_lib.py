@@ -32,7 +32,7 @@ EXPORTS = (
     "la_last_error", "la_abi_version", "la_weight_count", "la_weight_name", "la_create",
     "la_destroy", "la_decode_lookahead", "la_decode_autoregressive", "la_forward_layout",
     "la_lp_unique_id", "la_lp_init", "la_decode_lookahead_group", "la_debug_read",
-    "la_gemm_timing_reset", "la_gemm_timing_read",
+    "la_gemm_timing_reset", "la_gemm_timing_read", "la_packed_bytes", "la_pack_weight",
 )
 
 
@@ -101,6 +101,10 @@ def load(path: str | os.PathLike | None = None):
                                               C.POINTER(la_gen_config), C.POINTER(la_decode_io),
                                               C.c_void_p]
     lib.la_debug_read.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]
+    lib.la_packed_bytes.argtypes = [C.c_int32, C.c_int32]
+    lib.la_packed_bytes.restype = C.c_int64
+    lib.la_pack_weight.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                   C.c_int32, C.c_void_p]
     lib.la_gemm_timing_reset.argtypes = [C.c_void_p]
     lib.la_gemm_timing_read.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     for name in EXPORTS:

@@ -237,17 +237,24 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
   }
 }
 
-// grid = n rows (LA_MAX_ROWS), block = 512 (16 warps loop over heads)
+// grid = n rows (LA_MAX_ROWS), block = 512 (16 warps loop over heads).
+// Chain keys are processed 32 at a time, one key per lane (scores in one
+// round of loads), then P.V with lanes over head dims; the merge order --
+// prefix chunks, then chain keys in relative-position order, then the row
+// itself -- depends only on the row's chain, never on the step layout.
 __global__ void __launch_bounds__(512) la_attn_chain_kernel(LaAttnArgs a) {
   const FwdPlan* P = a.plan;
   const int r = blockIdx.x;
   if (r >= P->n_rows) return;
+  __shared__ float sq[16][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int ctx = P->n_prefix, g = a.H / a.KVH;
   const int n_chunks = ctx == 0 ? 0 : (ctx + chunk_keys(ctx, a.NC) - 1) / chunk_keys(ctx, a.NC);
   const float sl2 = a.scale * kLog2e;
   const size_t kv_ld = (size_t)a.KVH * 128;
   const int nch = P->chain_n[r];
+  const int nkeys = nch + 1;                       // chain + the row itself
+  const int my_slot_self = P->slot[r];
   for (int h = warp; h < a.H; h += nw) {
     const int kvh = h / g;
     float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
@@ -264,29 +271,64 @@ __global__ void __launch_bounds__(512) la_attn_chain_kernel(LaAttnArgs a) {
       l = l * s0 + ml.y * s1;
       m = mn;
     }
-    const __nv_bfloat16* qp = a.q + ((size_t)r * a.H + h) * 128 + lane * 4;
-    float2 q01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp));
-    float2 q23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp + 2));
-    for (int j = 0; j <= nch; ++j) {
-      const int slot = j < nch ? P->chain[r][j] : P->slot[r];
-      const size_t off = (size_t)slot * kv_ld + kvh * 128 + lane * 4;
-      float2 k01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.kc + off));
-      float2 k23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.kc + off + 2));
-      float dot = q01.x * k01.x + q01.y * k01.y + q23.x * k23.x + q23.y * k23.y;
-#pragma unroll
-      for (int sh = 16; sh > 0; sh >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, sh);
-      const float sc = dot * sl2;
-      float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.vc + off));
-      float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a.vc + off + 2));
-      float mn = fmaxf(m, sc);
-      float s0 = exp2f(m - mn), s1 = exp2f(sc - mn);
-      o[0] = o[0] * s0 + v01.x * s1;
-      o[1] = o[1] * s0 + v01.y * s1;
-      o[2] = o[2] * s0 + v23.x * s1;
-      o[3] = o[3] * s0 + v23.y * s1;
-      l = l * s0 + s1;
-      m = mn;
+    {
+      const __nv_bfloat16* qp = a.q + ((size_t)r * a.H + h) * 128 + lane * 4;
+      float2 q01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp));
+      float2 q23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp + 2));
+      sq[warp][lane * 4 + 0] = q01.x;
+      sq[warp][lane * 4 + 1] = q01.y;
+      sq[warp][lane * 4 + 2] = q23.x;
+      sq[warp][lane * 4 + 3] = q23.y;
+      __syncwarp();
     }
+    for (int j0 = 0; j0 < nkeys; j0 += 32) {
+      const int j = j0 + lane;
+      const bool valid = j < nkeys;
+      const int slot = !valid ? my_slot_self : (j < nch ? P->chain[r][j] : my_slot_self);
+      float sc = -INFINITY;
+      if (valid) {
+        const uint4* kp = reinterpret_cast<const uint4*>(a.kc + (size_t)slot * kv_ld + kvh * 128);
+        float dot = 0.f;
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          uint4 u = kp[v];
+          const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float2 f = __bfloat1622float2(b[k]);
+            dot = fmaf(sq[warp][v * 8 + 2 * k], f.x, dot);
+            dot = fmaf(sq[warp][v * 8 + 2 * k + 1], f.y, dot);
+          }
+        }
+        sc = dot * sl2;
+      }
+      float pmax = sc;
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, sh));
+      const float mn = fmaxf(m, pmax);
+      const float s0 = exp2f(m - mn);
+      const float pj = valid ? exp2f(sc - mn) : 0.f;
+      float psum = pj;
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) psum += __shfl_xor_sync(0xffffffffu, psum, sh);
+      o[0] *= s0; o[1] *= s0; o[2] *= s0; o[3] *= s0;
+      l = l * s0 + psum;
+      m = mn;
+      const int cnt = min(32, nkeys - j0);
+#pragma unroll 4
+      for (int t = 0; t < cnt; ++t) {
+        const float pt = __shfl_sync(0xffffffffu, pj, t);
+        const int st = __shfl_sync(0xffffffffu, slot, t);
+        const __nv_bfloat16* vp = a.vc + (size_t)st * kv_ld + kvh * 128 + lane * 4;
+        float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vp));
+        float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vp + 2));
+        o[0] = fmaf(pt, v01.x, o[0]);
+        o[1] = fmaf(pt, v01.y, o[1]);
+        o[2] = fmaf(pt, v23.x, o[2]);
+        o[3] = fmaf(pt, v23.y, o[3]);
+      }
+    }
+    __syncwarp();
     const float inv = 1.0f / l;
     __nv_bfloat16* dst = a.out + (size_t)r * a.H * 128 + h * 128 + lane * 4;
     *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(o[0] * inv, o[1] * inv),

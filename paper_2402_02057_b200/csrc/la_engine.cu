@@ -38,10 +38,15 @@ static const char* kGptTop[] = {"embed", "unembed", "lnf_g", "lnf_b"};
 static const char* kLlamaLayer[] = {"wq", "wk", "wv", "wo", "w_gate",
                                     "w_up", "w_down", "attn_norm", "mlp_norm"};
 static const char* kLlamaTop[] = {"embed", "lm_head", "final_norm"};
+// bf16 path: projection matrices in the packed LA-tile layout (la_pack_weight)
+static const char* kPackedLayer[] = {"wqkv_tiles", "wo_tiles", "wgu_tiles", "wd_tiles",
+                                     "attn_norm", "mlp_norm"};
+static const char* kPackedTop[] = {"embed", "lm_head_tiles", "final_norm"};
 
 extern "C" int32_t la_weight_count(const la_model_desc* d) {
   if (!d) return 0;
   if (d->arch == LA_ARCH_GPT_F32) return 4 + 12 * d->layers;
+  if (d->arch == LA_ARCH_LLAMA_BF16) return 3 + 6 * d->layers;
   return 3 + 9 * d->layers;
 }
 
@@ -51,6 +56,9 @@ extern "C" const char* la_weight_name(const la_model_desc* d, int32_t i) {
   if (d->arch == LA_ARCH_GPT_F32) {
     if (i < 4) return kGptTop[i];
     snprintf(buf, sizeof(buf), "%d.%s", (i - 4) / 12, kGptLayer[(i - 4) % 12]);
+  } else if (d->arch == LA_ARCH_LLAMA_BF16) {
+    if (i < 3) return kPackedTop[i];
+    snprintf(buf, sizeof(buf), "%d.%s", (i - 3) / 6, kPackedLayer[(i - 3) % 6]);
   } else {
     if (i < 3) return kLlamaTop[i];
     snprintf(buf, sizeof(buf), "%d.%s", (i - 3) / 9, kLlamaLayer[(i - 3) % 9]);
@@ -581,6 +589,8 @@ extern "C" int32_t la_decode_lookahead_group(la_engine* const* es, int32_t n,
   return rc;
 }
 
+int llama_read_trace(la_engine* e, void* host, size_t bytes);
+
 // ------------------------------------------------------------ debug copy
 extern "C" int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t bytes) {
   if (!e || !host) { la_set_error("null engine or buffer"); return LA_ERR_INVALID_CONFIG; }
@@ -595,6 +605,7 @@ extern "C" int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t
     case 2: src = e->vc; avail = kv; break;
     case 3: src = e->d_dec; avail = sizeof(DevDecode); break;
     case 4: src = e->d_plan; avail = sizeof(FwdPlan); break;
+    case 5: return llama_read_trace(e, host, (size_t)bytes);
     default: la_set_error("unknown debug buffer %d", what); return LA_ERR_INVALID_CONFIG;
   }
   CK(cudaMemcpy(host, src, std::min<size_t>(avail, (size_t)bytes), cudaMemcpyDeviceToHost));

@@ -9,12 +9,16 @@
 // a whole decode is ONE graph launch with no host round trip.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
+
 
 #include "la_attn.cuh"
 #include "la_engine.h"
 #include "la_gemm.cuh"
 #include "la_kernels.h"
+#include "la_reduce.cuh"
 
 #define CK(x) LA_CUDA_CHECK(x)
 #define RET_IF(x)               \
@@ -24,7 +28,7 @@
   } while (0)
 
 struct LlamaLayerW {
-  const __nv_bfloat16 *wq, *wk, *wv, *wo, *wg, *wu, *wd;
+  const __nv_bfloat16 *wqkv, *wo, *wgu, *wd;   // packed LA tiles (la_gemm.cuh)
   const float *attn_norm, *mlp_norm;
 };
 
@@ -37,14 +41,14 @@ struct LlamaPath {
   float* x = nullptr;
   __nv_bfloat16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
   float* ws = nullptr;
-  int* counters = nullptr;
   float2* pmax = nullptr;
   float* part_o = nullptr;
   float2* part_ml = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* row_amax = nullptr;
-  unsigned long long* timing = nullptr;   // [4 epilogue kinds][8]
-  float* logits = nullptr;   // device dump target (parity hook), else null
+  unsigned long long* timing = nullptr;   // [4 GEMM kinds][8]
+  unsigned long long* trace = nullptr;    // [4 GEMM kinds][256 CTAs][4] (LA_GEMM_TRACE=1)
+  float* logits = nullptr;                // device dump target (parity hook), else null
   std::vector<LaGemm> qkv, o, gu, down;
   LaGemm head{};
   int head_tiles = 0;
@@ -57,57 +61,6 @@ struct LlamaPath {
 
 // ------------------------------------------------------------- kernels
 namespace {
-
-__device__ __forceinline__ float block_sum(float v, float* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  float t = 0.f;
-  for (int i = 0; i < nw; ++i) t += red[i];
-  return t;
-}
-
-// RMSNorm of one row (fp32 residual -> bf16 GEMM input); grid = rows
-__global__ void __launch_bounds__(256) la_rmsnorm_kernel(const FwdPlan* P, const float* x,
-                                                        const float* g, __nv_bfloat16* h, int d,
-                                                        float eps, const __nv_bfloat16* embed) {
-  const int r = blockIdx.x;
-  if (r >= P->n_rows) return;
-  __shared__ float red[8];
-  float* xr = const_cast<float*>(x) + (size_t)r * d;
-  if (embed) {   // first norm of the step: x = embedding row (reference models.py:247)
-    const __nv_bfloat16* er = embed + (size_t)P->ids[r] * d;
-    for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
-      uint4 u = *reinterpret_cast<const uint4*>(er + i);
-      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float2 f = __bfloat1622float2(b[k]);
-        xr[i + 2 * k] = f.x;
-        xr[i + 2 * k + 1] = f.y;
-      }
-    }
-    __syncthreads();
-  }
-  float ss = 0.f;
-  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-  }
-  const float inv = rsqrtf(block_sum(ss, red) / d + eps);
-  __nv_bfloat16* hr = h + (size_t)r * d;
-  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4*>(xr + i);
-    float4 gg = *reinterpret_cast<const float4*>(g + i);
-    __nv_bfloat162 a = __floats2bfloat162_rn(v.x * inv * gg.x, v.y * inv * gg.y);
-    __nv_bfloat162 b = __floats2bfloat162_rn(v.z * inv * gg.z, v.w * inv * gg.w);
-    *reinterpret_cast<__nv_bfloat162*>(hr + i) = a;
-    *reinterpret_cast<__nv_bfloat162*>(hr + i + 2) = b;
-  }
-}
 
 // per-row argmax over the LM-head tiles (lowest index on ties), then the
 // owned rows go to the decode state's global-row table
@@ -149,22 +102,20 @@ __global__ void la_set_cond_kernel(cudaGraphConditionalHandle h, const DevDecode
 }  // namespace
 
 // ------------------------------------------------------------ host setup
-static int build_gemm(LaGemm& g, int epi, int a_mode, const void* a0, int rows0, const void* a1,
-                      int rows1, const void* a2, int rows2, int box, const void* b, int K,
-                      int n_tiles) {
+static int build_gemm(LaGemm& g, const void* a_packed, int n_tiles, const void* b, int K) {
   memset(&g, 0, sizeof(g));
-  RET_IF(la_make_tmap(&g.a0, a0, rows0, K, box));
-  RET_IF(la_make_tmap(&g.a1, a1 ? a1 : a0, a1 ? rows1 : rows0, K, box));
-  RET_IF(la_make_tmap(&g.a2, a2 ? a2 : a0, a2 ? rows2 : rows0, K, box));
   RET_IF(la_make_tmap(&g.b, b, LA_MAX_ROWS, K, 16));
-  g.epi = epi;
+  g.args.a = reinterpret_cast<const __nv_bfloat16*>(a_packed);
   g.args.n_tiles = n_tiles;
   g.args.kb = K / 64;
-  g.args.a_mode = a_mode;
   long U = (long)n_tiles * g.args.kb;
   g.grid = (int)std::min<long>(la_sm_count(), U);
   g.args.max_segs = la_gemm_workspace_segs(n_tiles, g.args.kb, g.grid);
   return LA_OK;
+}
+
+static LaSplit split_of(const LaGemm& g) {
+  return LaSplit{g.args.n_tiles, g.args.kb, g.grid, g.args.max_segs};
 }
 
 template <typename T>
@@ -189,8 +140,8 @@ int llama_create(la_engine* e) {
   auto F = [&](int i) { return reinterpret_cast<const float*>(e->w[i]); };
   p->embed = B(0); p->lm_head = B(1); p->final_norm = F(2);
   for (int l = 0; l < D.layers; ++l) {
-    int b = 3 + 9 * l;
-    p->lw.push_back({B(b), B(b + 1), B(b + 2), B(b + 3), B(b + 4), B(b + 5), B(b + 6), F(b + 7), F(b + 8)});
+    int b = 3 + 6 * l;
+    p->lw.push_back({B(b), B(b + 1), B(b + 2), B(b + 3), F(b + 4), F(b + 5)});
   }
   const int R = LA_MAX_ROWS, qd = D.heads * 128;
   RET_IF(lalloc(e, &p->x, (size_t)R * D.dim));
@@ -223,52 +174,35 @@ int llama_create(la_engine* e) {
   const int d = D.dim, KVH = D.kv_heads, H = D.heads;
   p->qkv.resize(D.layers); p->o.resize(D.layers); p->gu.resize(D.layers); p->down.resize(D.layers);
   size_t ws_need = 0;
-  int max_tiles = 0;
   auto track = [&](const LaGemm& gg) {
     ws_need = std::max(ws_need, (size_t)gg.args.n_tiles * gg.args.max_segs * 128 * 128);
-    max_tiles = std::max(max_tiles, gg.args.n_tiles);
   };
-  __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc);
-  __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc);
   for (int l = 0; l < D.layers; ++l) {
     const LlamaLayerW& w = p->lw[l];
-    LaGemm& a = p->qkv[l];
-    RET_IF(build_gemm(a, LA_EPI_QKV, 1, w.wq, H * 128, w.wk, KVH * 128, w.wv, KVH * 128, 128, p->h, d, H + 2 * KVH));
-    a.args.t0 = H; a.args.t1 = H + KVH;
-    a.args.q_out = p->q;
-    a.args.kc = kc + (size_t)l * e->slots * KVH * 128;
-    a.args.vc = vc + (size_t)l * e->slots * KVH * 128;
-    a.args.rope_cos = p->rope_cos; a.args.rope_sin = p->rope_sin;
-    a.args.H = H; a.args.KVH = KVH;
-    track(a);
-    LaGemm& ob = p->o[l];
-    RET_IF(build_gemm(ob, LA_EPI_RESID, 0, w.wo, d, nullptr, 0, nullptr, 0, 128, p->attn, H * 128, d / 128));
-    ob.args.x = p->x; ob.args.x_ld = d;
-    track(ob);
-    LaGemm& gu = p->gu[l];
-    RET_IF(build_gemm(gu, LA_EPI_SWIGLU, 2, w.wg, D.ffn, w.wu, D.ffn, nullptr, 0, 64, p->h, d, D.ffn / 64));
-    gu.args.act = p->act; gu.args.act_ld = D.ffn;
-    track(gu);
-    LaGemm& dn = p->down[l];
-    RET_IF(build_gemm(dn, LA_EPI_RESID, 0, w.wd, d, nullptr, 0, nullptr, 0, 128, p->act, D.ffn, d / 128));
-    dn.args.x = p->x; dn.args.x_ld = d;
-    track(dn);
+    RET_IF(build_gemm(p->qkv[l], w.wqkv, H + 2 * KVH, p->h, d));
+    track(p->qkv[l]);
+    RET_IF(build_gemm(p->o[l], w.wo, d / 128, p->attn, H * 128));
+    track(p->o[l]);
+    RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d));
+    track(p->gu[l]);
+    RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn));
+    track(p->down[l]);
   }
   p->head_tiles = (D.vocab + 127) / 128;
-  RET_IF(build_gemm(p->head, LA_EPI_LOGITS, 0, p->lm_head, D.vocab, nullptr, 0, nullptr, 0, 128, p->h, d, p->head_tiles));
+  RET_IF(build_gemm(p->head, p->lm_head, p->head_tiles, p->h, d));
   track(p->head);
   RET_IF(lalloc(e, &p->pmax, (size_t)p->head_tiles * 128));
-  p->head.args.pmax = p->pmax;
-  p->head.args.V = D.vocab;
   RET_IF(lalloc(e, &p->ws, ws_need));
-  RET_IF(lalloc(e, &p->counters, max_tiles + 1));
   RET_IF(lalloc(e, &p->timing, 32));
-  auto fin = [&](LaGemm& gg) {
-    gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.counters = p->counters;
-    gg.args.timing = p->timing + 8 * gg.epi;
+  const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
+  if (trace) RET_IF(lalloc(e, &p->trace, 4 * 256 * 4));
+  auto fin = [&](LaGemm& gg, int kind) {
+    gg.args.plan = e->d_plan; gg.args.ws = p->ws;
+    gg.args.timing = p->timing + 8 * kind;
+    gg.args.trace = trace ? p->trace + 256 * 4 * kind : nullptr;
   };
-  for (int l = 0; l < D.layers; ++l) { fin(p->qkv[l]); fin(p->o[l]); fin(p->gu[l]); fin(p->down[l]); }
-  fin(p->head);
+  for (int l = 0; l < D.layers; ++l) { fin(p->qkv[l], 0); fin(p->o[l], 1); fin(p->gu[l], 2); fin(p->down[l], 1); }
+  fin(p->head, 3);
   CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
   cudaError_t ce = cudaFuncSetAttribute(la_attn_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)la_attn_prefix_smem());
@@ -310,25 +244,43 @@ static int launch_attn(la_engine* e, int l, cudaStream_t st) {
   return LA_OK;
 }
 
+static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool embed, cudaStream_t st) {
+  LlamaPath* p = e->llama;
+  LaResidNorm r;
+  r.plan = e->d_plan;
+  r.ws = from ? p->ws : nullptr;
+  r.sp = from ? split_of(*from) : LaSplit{1, 1, 1, 1};
+  r.embed = embed ? p->embed : nullptr;
+  r.x = p->x; r.g = g; r.h = p->h; r.d = p->d; r.eps = p->eps;
+  la_resid_norm_kernel<<<LA_MAX_ROWS, 256, 0, st>>>(r);
+  CK(cudaGetLastError());
+  return LA_OK;
+}
+
 // all decoder layers on the rows of e->d_plan; leaves h = final-norm(x)
 static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
   LlamaPath* p = e->llama;
-  la_rmsnorm_kernel<<<LA_MAX_ROWS, 256, 0, st>>>(e->d_plan, p->x, p->lw[0].attn_norm, p->h, p->d,
-                                                 p->eps, p->embed);
-  CK(cudaGetLastError());
+  __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc);
+  __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc);
+  const size_t lstride = (size_t)e->slots * p->KVH * 128;
+  RET_IF(resid_norm(e, nullptr, p->lw[0].attn_norm, true, st));
   int n = 1;
   for (int l = 0; l < p->L; ++l) {
     RET_IF(la_gemm_launch(p->qkv[l], st));
+    LaQkvEpi q{e->d_plan, p->ws, split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride,
+               p->rope_cos, p->rope_sin, p->H, p->KVH};
+    la_qkv_epi_kernel<<<p->H + 2 * p->KVH, 256, 0, st>>>(q);
     RET_IF(launch_attn(e, l, st));
     RET_IF(la_gemm_launch(p->o[l], st));
-    la_rmsnorm_kernel<<<LA_MAX_ROWS, 256, 0, st>>>(e->d_plan, p->x, p->lw[l].mlp_norm, p->h, p->d,
-                                                   p->eps, nullptr);
+    RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st));
     RET_IF(la_gemm_launch(p->gu[l], st));
+    LaSwigluEpi sw{e->d_plan, p->ws, split_of(p->gu[l]), p->act, p->ffn};
+    la_swiglu_epi_kernel<<<p->ffn / 64, 256, 0, st>>>(sw);
     RET_IF(la_gemm_launch(p->down[l], st));
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
-    la_rmsnorm_kernel<<<LA_MAX_ROWS, 256, 0, st>>>(e->d_plan, p->x, next, p->h, p->d, p->eps, nullptr);
+    RET_IF(resid_norm(e, &p->down[l], next, false, st));
     CK(cudaGetLastError());
-    n += 8;
+    n += 10;
   }
   *nk += n;
   return LA_OK;
@@ -336,12 +288,13 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
 
 static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
   LlamaPath* p = e->llama;
-  p->head.args.logits = p->logits;
   RET_IF(la_gemm_launch(p->head, st));
+  LaLogitsEpi lg{e->d_plan, p->ws, split_of(p->head), p->pmax, p->logits, p->V};
+  la_logits_epi_kernel<<<p->head_tiles, 128, 0, st>>>(lg);
   la_argmax_reduce_kernel<<<1, 128, 0, st>>>(e->d_plan, p->pmax, p->head_tiles, p->row_amax,
                                             scatter ? e->d_dec : nullptr);
   CK(cudaGetLastError());
-  *nk += 2;
+  *nk += 3;
   return LA_OK;
 }
 
@@ -363,7 +316,6 @@ int llama_forward_plan(la_engine* e, float* d_logits, cudaStream_t st) {
   int rc = forward_layers(e, st, &nk);
   if (rc == LA_OK) rc = forward_head(e, st, false, &nk);
   p->logits = nullptr;
-  p->head.args.logits = nullptr;
   return rc;
 }
 
@@ -414,8 +366,28 @@ static int build_loop_graph(la_engine* e) {
   return LA_OK;
 }
 
+// LA_LAUNCH_MODE=eager: host loop of plain launches (profilers cannot see
+// kernel nodes inside conditional graphs); default: one WHILE-graph launch.
+static int eager_loop(la_engine* e, cudaStream_t st, int* launches) {
+  static thread_local int* pinned = nullptr;
+  if (!pinned) CK(cudaMallocHost(&pinned, sizeof(int)));
+  int nk = 0;
+  for (int step = 0; step < e->h_dec.max_steps; ++step) {
+    RET_IF(record_step(e, st, true, &nk));
+    if ((step + 1) % 4 == 0) {
+      CK(cudaMemcpyAsync(pinned, &e->d_dec->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (*pinned) break;
+    }
+  }
+  *launches = nk;
+  return LA_OK;
+}
+
 int llama_decode_loop(la_engine* e, cudaStream_t st, int* launches) {
   LlamaPath* p = e->llama;
+  const char* mode = getenv("LA_LAUNCH_MODE");
+  if (mode && !strcmp(mode, "eager")) return eager_loop(e, st, launches);
   if (!p->loop_exec) RET_IF(build_loop_graph(e));
   CK(cudaGraphLaunch(p->loop_exec, st));
   // kernels launched = per-step kernels x steps; the host learns the step
@@ -439,6 +411,13 @@ int llama_step_forward(la_engine* e, cudaStream_t st) {
     p->fwd_graph = g;
   }
   CK(cudaGraphLaunch(p->fwd_exec, st));
+  return LA_OK;
+}
+
+// debug: per-CTA trace of the last launch of each GEMM kind (LA_GEMM_TRACE=1)
+int llama_read_trace(la_engine* e, void* host, size_t bytes) {
+  if (!e->llama || !e->llama->trace) { la_set_error("trace disabled (set LA_GEMM_TRACE=1)"); return LA_ERR_INVALID_CONFIG; }
+  CK(cudaMemcpy(host, e->llama->trace, std::min<size_t>(bytes, 4 * 256 * 4 * 8), cudaMemcpyDeviceToHost));
   return LA_OK;
 }
 

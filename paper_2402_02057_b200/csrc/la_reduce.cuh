@@ -1,0 +1,54 @@
+// Parameter blocks of the split-K reduce / epilogue kernels (la_reduce.cu).
+#pragma once
+#include <cuda_bf16.h>
+
+#include "la_common.cuh"
+
+// stream-K geometry of the producing GEMM
+struct LaSplit {
+  int n_tiles, kb, grid, max_segs;
+};
+
+struct LaQkvEpi {
+  const FwdPlan* plan;
+  const float* ws;
+  LaSplit sp;
+  __nv_bfloat16* q_out;          // [128][H][128]
+  __nv_bfloat16 *kc, *vc;        // layer base [slots][KVH][128]
+  const float *rope_cos, *rope_sin;
+  int H, KVH;
+};
+
+struct LaResidNorm {
+  const FwdPlan* plan;
+  const float* ws;               // null: no partials to add
+  LaSplit sp;
+  const __nv_bfloat16* embed;    // non-null: x := embedding row (start of the step)
+  float* x;                      // [128][d] fp32 residual stream
+  const float* g;                // RMSNorm gain
+  __nv_bfloat16* h;              // [128][d]
+  int d;
+  float eps;
+};
+
+struct LaSwigluEpi {
+  const FwdPlan* plan;
+  const float* ws;
+  LaSplit sp;
+  __nv_bfloat16* act;
+  int act_ld;
+};
+
+struct LaLogitsEpi {
+  const FwdPlan* plan;
+  const float* ws;
+  LaSplit sp;
+  float2* pmax;                  // [tiles][128]
+  float* logits;                 // [128][V] or null
+  int V;
+};
+
+__global__ void la_qkv_epi_kernel(LaQkvEpi e);
+__global__ void la_resid_norm_kernel(LaResidNorm e);
+__global__ void la_swiglu_epi_kernel(LaSwigluEpi e);
+__global__ void la_logits_epi_kernel(LaLogitsEpi e);

@@ -210,11 +210,16 @@ def llama_weight_shapes(cfg: LlamaConfig) -> dict:
 class LlamaModel(B200Model):
     """Llama-2-shaped decoder (RMSNorm, rotate-half RoPE, SwiGLU, GQA).
 
-    ``dtype="bf16"``: the tcgen05 multi-kernel path (configs 2-5).
+    ``dtype="bf16"``: the tcgen05 multi-kernel path (configs 2-5).  Projection
+    matrices live in the packed LA-tile layout (``la_pack_weight``): q/k/v
+    stacked, gate/up interleaved per 64 rows, each 128x64 block one
+    contiguous 16 KB swizzled image so the GEMM streams HBM sequentially.
     ``dtype="f32"``: the fp32 SIMT single-CTA path (small parity models).
-    ``weights``: optional name -> array/tensor dict (HF layout, [out][in]);
-    otherwise random-init N(0, 0.02^2) matrices and unit norm gains from a
-    seeded CUDA generator (BASELINE: synthetic weights of the named shape)."""
+    ``weights``: optional name -> array/tensor dict in HF layout ([out][in]:
+    ``embed, lm_head, final_norm, i.wq, i.wk, i.wv, i.wo, i.w_gate, i.w_up,
+    i.w_down, i.attn_norm, i.mlp_norm``), converted on the device; otherwise
+    random-init N(0, 0.02^2) matrices and unit norm gains from a seeded CUDA
+    generator (BASELINE: synthetic weights of the named shape)."""
 
     def __init__(self, cfg: LlamaConfig, *, dtype: str = "bf16", weights: dict | None = None,
                  seed: int = 0, max_context: int = 2048, device: int = 0, init_std: float = 0.02):
@@ -225,23 +230,98 @@ class LlamaModel(B200Model):
         self.dtype = dtype
         self.arch = _lib.ARCH_LLAMA_BF16 if dtype == "bf16" else _lib.ARCH_LLAMA_F32
         dev = torch.device("cuda", device)
-        mat_dtype = torch.bfloat16 if dtype == "bf16" else torch.float32
-        named = {}
-        shapes = llama_weight_shapes(cfg)
-        gen = None
-        for name, shape in shapes.items():
-            is_norm = len(shape) == 1
-            want = torch.float32 if is_norm else mat_dtype
-            if weights is not None:
-                src = weights[name]
-                t = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.asarray(src))
-                t = t.to(device=dev, dtype=want).contiguous()
-            elif is_norm:
-                t = torch.ones(shape, dtype=want, device=dev)
-            else:
-                if gen is None:
-                    gen = torch.Generator(device=dev)
-                    gen.manual_seed(seed)
-                t = torch.empty(shape, dtype=want, device=dev).normal_(0.0, init_std, generator=gen)
-            named[name] = t
+        self._gen = None
+        self._seed = seed
+        self._std = init_std
+        self._dev = dev
+        if dtype == "f32":
+            named = {}
+            for name, shape in llama_weight_shapes(cfg).items():
+                named[name] = self._tensor(weights, name, shape, torch.float32)
+        else:
+            named = self._packed_bf16(cfg, weights)
         super().__init__(cfg.as_desc(max_context), named, device)
+
+    # ---------------------------------------------------------- weights
+    def _rand(self, shape, dtype):
+        torch = _torch()
+        if self._gen is None:
+            self._gen = torch.Generator(device=self._dev)
+            self._gen.manual_seed(self._seed)
+        return torch.empty(shape, dtype=dtype, device=self._dev).normal_(0.0, self._std,
+                                                                        generator=self._gen)
+
+    def _tensor(self, weights, name, shape, dtype):
+        torch = _torch()
+        if weights is not None:
+            src = weights[name]
+            t = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.asarray(src))
+            return t.to(device=self._dev, dtype=dtype).contiguous()
+        if len(shape) == 1:
+            return torch.ones(shape, dtype=torch.float32, device=self._dev)
+        return self._rand(shape, dtype)
+
+    def _packed_bf16(self, cfg: LlamaConfig, weights: dict | None) -> dict:
+        torch = _torch()
+        lib = _lib.load()
+        bf = torch.bfloat16
+        d, hd, H, KVH, F, V = cfg.dim, cfg.head_dim, cfg.heads, cfg.kv_heads, cfg.ffn, cfg.vocab
+        stream = C.c_void_p(torch.cuda.current_stream(self._dev).cuda_stream)
+
+        def packed(rows, K):
+            n = lib.la_packed_bytes(rows, K)
+            if n < 0:
+                raise ValueError(f"cannot pack a [{rows}][{K}] matrix (K % 64 != 0)")
+            return torch.zeros(n // 2, dtype=bf, device=self._dev)
+
+        def pack_into(dst, name, rows, K, mode=0, off=0):
+            src = self._tensor(weights, name, (rows, K), bf)
+            _lib.check(lib.la_pack_weight(C.c_void_p(src.data_ptr()), rows, K,
+                                          C.c_void_p(dst.data_ptr()), mode, off, stream))
+            del src
+
+        named = {"embed": self._tensor(weights, "embed", (V, d), bf),
+                 "final_norm": self._tensor(weights, "final_norm", (d,), torch.float32)}
+        if weights is None:
+            # synthetic: draw the packed tiles directly (same distribution)
+            def fill(rows, K):
+                t = packed(rows, K)
+                t.normal_(0.0, self._std, generator=self._gen_or_new())
+                return t
+            named["lm_head_tiles"] = fill(V, d)
+            for i in range(cfg.layers):
+                named[f"{i}.wqkv_tiles"] = fill((H + 2 * KVH) * hd, d)
+                named[f"{i}.wo_tiles"] = fill(d, H * hd)
+                named[f"{i}.wgu_tiles"] = fill(2 * F, d)
+                named[f"{i}.wd_tiles"] = fill(d, F)
+                named[f"{i}.attn_norm"] = torch.ones(d, dtype=torch.float32, device=self._dev)
+                named[f"{i}.mlp_norm"] = torch.ones(d, dtype=torch.float32, device=self._dev)
+            return named
+        lm = packed(V, d)
+        pack_into(lm, "lm_head", V, d)
+        named["lm_head_tiles"] = lm
+        for i in range(cfg.layers):
+            qkv = packed((H + 2 * KVH) * hd, d)
+            pack_into(qkv, f"{i}.wq", H * hd, d, 0, 0)
+            pack_into(qkv, f"{i}.wk", KVH * hd, d, 0, H * hd)
+            pack_into(qkv, f"{i}.wv", KVH * hd, d, 0, (H + KVH) * hd)
+            wo = packed(d, H * hd)
+            pack_into(wo, f"{i}.wo", d, H * hd)
+            gu = packed(2 * F, d)
+            pack_into(gu, f"{i}.w_gate", F, d, 1)
+            pack_into(gu, f"{i}.w_up", F, d, 2)
+            wd = packed(d, F)
+            pack_into(wd, f"{i}.w_down", d, F)
+            named.update({f"{i}.wqkv_tiles": qkv, f"{i}.wo_tiles": wo, f"{i}.wgu_tiles": gu,
+                          f"{i}.wd_tiles": wd,
+                          f"{i}.attn_norm": self._tensor(weights, f"{i}.attn_norm", (d,), torch.float32),
+                          f"{i}.mlp_norm": self._tensor(weights, f"{i}.mlp_norm", (d,), torch.float32)})
+        torch.cuda.synchronize(self._dev)
+        return named
+
+    def _gen_or_new(self):
+        torch = _torch()
+        if self._gen is None:
+            self._gen = torch.Generator(device=self._dev)
+            self._gen.manual_seed(self._seed)
+        return self._gen

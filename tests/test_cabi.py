@@ -39,11 +39,15 @@ def test_weight_names_and_abi(lib):
     assert lib.la_abi_version() == 1
     d = _lib.la_model_desc(_lib.ARCH_LLAMA_BF16, 32000, 4096, 32, 32, 32, 128, 11008, 1e4, 1e-5, 2048)
     n = lib.la_weight_count(C.byref(d))
-    assert n == 3 + 9 * 32
+    assert n == 3 + 6 * 32
     names = [lib.la_weight_name(C.byref(d), i).decode() for i in range(n)]
-    assert names[:3] == ["embed", "lm_head", "final_norm"]
-    assert names[3:12] == ["0.wq", "0.wk", "0.wv", "0.wo", "0.w_gate", "0.w_up", "0.w_down",
-                           "0.attn_norm", "0.mlp_norm"]
+    assert names[:3] == ["embed", "lm_head_tiles", "final_norm"]
+    assert names[3:9] == ["0.wqkv_tiles", "0.wo_tiles", "0.wgu_tiles", "0.wd_tiles",
+                          "0.attn_norm", "0.mlp_norm"]
+    f = _lib.la_model_desc(_lib.ARCH_LLAMA_F32, 64, 64, 2, 4, 2, 16, 96, 1e4, 1e-5, 256)
+    assert lib.la_weight_count(C.byref(f)) == 3 + 9 * 2
+    assert lib.la_packed_bytes(32000, 4096) == 250 * 64 * 16384
+    assert lib.la_packed_bytes(32016, 4096) == 251 * 64 * 16384
     g = _lib.la_model_desc(_lib.ARCH_GPT_F32, 256, 16, 2, 2, 2, 8, 64, 1e4, 1e-5, 256)
     assert lib.la_weight_count(C.byref(g)) == 4 + 12 * 2
 
