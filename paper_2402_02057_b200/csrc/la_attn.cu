@@ -18,6 +18,7 @@
 
 #include "la_attn.cuh"
 #include "la_common.cuh"
+#include "la_gemm.cuh"
 
 namespace {
 
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(512) la_attn_chain_kernel(LaAttnArgs a) {
     }
     __syncwarp();
     const float inv = 1.0f / l;
-    __nv_bfloat16* dst = a.out + (size_t)r * a.H * 128 + h * 128 + lane * 4;
+    __nv_bfloat16* dst = a.out + la_act_off(r, h * 128 + lane * 4);   // packed LA rows
     *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(o[0] * inv, o[1] * inv),
                                                 pack_bf16(o[2] * inv, o[3] * inv));
   }

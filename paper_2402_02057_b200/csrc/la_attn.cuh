@@ -10,7 +10,7 @@ struct LaAttnArgs {
   const __nv_bfloat16 *kc, *vc;  // layer base, [slots][KVH][128]
   float* part_o;                 // [NC][LA_MAX_ROWS][H][128]
   float2* part_ml;               // [NC][LA_MAX_ROWS][H]  (max, sum) in log2 units
-  __nv_bfloat16* out;            // [LA_MAX_ROWS][H*128]
+  __nv_bfloat16* out;            // packed LA rows [H*128/64][128][64] (la_act_off)
   int H, KVH, NC;
   float scale;                   // 1/sqrt(head_dim)
 };

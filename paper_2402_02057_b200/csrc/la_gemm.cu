@@ -19,11 +19,12 @@ void la_set_error(const char* fmt, ...);
 
 namespace {
 
-constexpr int kStages = 6;
-constexpr int kABytes = 128 * 128;   // 128 rows x 64 bf16
-constexpr int kBBytes = 128 * 128;   // <= 128 rows x 64 bf16
+constexpr int kStages = 4;
+constexpr int kTileBytes = 128 * 128;          // 128 rows x 64 bf16
+constexpr int kABytes = LA_TPC * kTileBytes;   // weight tiles per unit
+constexpr int kBBytes = 128 * 128;             // <= 128 rows x 64 bf16
 constexpr int kThreads = 192;
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = 512;                 // 2 buffers x LA_TPC tiles x 128 columns
 constexpr size_t kSmemBytes = 1024 + kStages * (kABytes + kBBytes) + 2 * kStages * 8 + 4 * 8 + 16;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -33,7 +34,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    la_gemm_kernel(const __grid_constant__ CUtensorMap mB, const LaGemmArgs args) {
+    la_gemm_kernel(const LaGemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   const FwdPlan* P = args.plan;
   const int n_rows = P->n_rows;
@@ -57,7 +58,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
     ptx::fence_barrier_init();
-    ptx::tma_prefetch_desc(&mB);
   }
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
 
   const int kb = args.kb;
-  const long U = (long)args.n_tiles * kb;
+  const int n_units_t = args.n_tiles / LA_TPC;   // tile pairs
+  const long U = (long)n_units_t * kb;
   const long Pn = gridDim.x;
   const long u_begin = (long)blockIdx.x * U / Pn;
   const long u_end = (long)(blockIdx.x + 1) * U / Pn;
@@ -84,11 +85,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = (int)(it % kStages);
         const uint32_t r = (uint32_t)(it / kStages);
         if (r > 0) ptx::mbar_wait(&empty[s], (r - 1) & 1);
-        ptx::mbar_expect_tx(&full[s], kABytes + bbytes);
+        const bool load_b = !(args.debug & 1);
+        ptx::mbar_expect_tx(&full[s], kABytes + (load_b ? bbytes : 0));
         ptx::bulk_load(sA + s * kABytes, args.a + (size_t)u * (kABytes / 2), kABytes, &full[s], pol_w);
-        uint8_t* b = sB + s * kBBytes;
-        for (int jb = 0; jb < n_pad / 16; ++jb)
-          ptx::tma_load_2d(b + jb * 2048, &mB, &full[s], k * 64, jb * 16, pol_x);
+        if (load_b)
+          ptx::bulk_load(sB + s * kBBytes, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
       }
     }
   } else if (warp == 1) {
@@ -104,18 +105,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&tempty[buf], (use[buf] - 1) & 1);
           ptx::tc_fence_after();
         }
-        const uint32_t d_tmem = tmem + buf * 128;
+        const uint32_t d_tmem = tmem + buf * (LA_TPC * 128);
         for (; u < seg_end; ++u, ++it) {
           const int s = (int)(it % kStages);
           ptx::mbar_wait(&full[s], (uint32_t)(it / kStages) & 1);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sA + s * kABytes);
           const uint32_t b_addr = ptx::smem_u32(sB + s * kBBytes);
+          if (args.debug & 2) {
+            ptx::mbar_arrive(&empty[s]);
+            continue;
+          }
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            ptx::umma_bf16(d_tmem, ptx::umma_desc_sw128(a_addr + kk * 32),
-                           ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
-                           (u > seg_start || kk > 0) ? 1u : 0u);
+          for (int tt = 0; tt < LA_TPC; ++tt)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kTileBytes + kk * 32),
+                             ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
+                             (u > seg_start || kk > 0) ? 1u : 0u);
           ptx::umma_commit(&empty[s]);
         }
         ptx::umma_commit(&tfull[buf]);
@@ -136,15 +143,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg = (int)(blockIdx.x - la_cta_of((long)tile * kb, U, Pn));
       ptx::mbar_wait(&tfull[buf], use[buf] & 1);
       ptx::tc_fence_after();
-      const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * 128;
-      float* wsp = args.ws + ((size_t)tile * args.max_segs + seg) * 128 * 128 + f;
-      for (int c0 = 0; c0 < n_pad; c0 += 32) {
-        float v[32];
-        ptx::tmem_ld32(t_base + c0, v);
-        const int nj = min(32, n_rows - c0);
+      for (int tt = 0; tt < LA_TPC; ++tt) {
+        const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
+        const int ftile = tile * LA_TPC + tt;
+        float* wsp = args.ws + ((size_t)ftile * args.max_segs + seg) * 128 * 128 + f;
+        for (int c0 = 0; c0 < n_pad; c0 += 32) {
+          float v[32];
+          ptx::tmem_ld32(t_base + c0, v);
+          const int nj = min(32, n_rows - c0);
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj)
-          if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
+          for (int jj = 0; jj < 32; ++jj)
+            if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
+        }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[buf]);
@@ -186,7 +196,8 @@ int la_sm_count() {
 }
 
 size_t la_packed_elems(int rows, int K) {
-  return (size_t)((rows + 127) / 128) * (K / 64) * 128 * 64;
+  const int tiles = ((rows + 127) / 128 + LA_TPC - 1) / LA_TPC * LA_TPC;
+  return (size_t)tiles * (K / 64) * 128 * 64;
 }
 
 int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_rows) {
@@ -217,11 +228,11 @@ int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_ro
 }
 
 int la_gemm_workspace_segs(int n_tiles, int kb, int grid) {
-  long U = (long)n_tiles * kb, mx = 1;
+  long mx = 1;
   for (int t = 0; t < n_tiles; ++t) {
     long c0;
     int n;
-    la_tile_segs(t, kb, U, grid, c0, n);
+    la_tile_segs(t, kb, n_tiles, grid, c0, n);
     mx = std::max<long>(mx, n);
   }
   return (int)mx;
@@ -235,15 +246,17 @@ int la_gemm_launch(const LaGemm& g, cudaStream_t st) {
     if (e != cudaSuccess) { la_set_error("gemm smem attr: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }
     attr = true;
   }
-  la_gemm_kernel<<<g.grid, kThreads, kSmemBytes, st>>>(g.b, g.args);
+  la_gemm_kernel<<<g.grid, kThreads, kSmemBytes, st>>>(g.args);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { la_set_error("gemm launch: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }
   return LA_OK;
 }
 
 // ---------------------------------------------------------------- packing
-// Packed "LA tile" layout: matrix rows grouped in 128-row tiles, K in 64-wide
-// blocks; block (t, kb) is 16 KB at ((t * KB) + kb) * 8192 elements, holding
+// Packed "LA tile" layout: matrix rows grouped in 128-row tiles (tile count
+// rounded up to LA_TPC), K in 64-wide blocks; block (t, kb) is 16 KB at
+// (((t / LA_TPC) * KB + kb) * LA_TPC + t % LA_TPC) * 8192 elements -- the
+// LA_TPC tiles of one stream-K unit are adjacent -- holding
 // rows r = 0..127 as 128-byte lines with 16-byte chunk c stored at chunk
 // position c ^ (r & 7) -- exactly the SWIZZLE_128B shared-memory image the
 // UMMA descriptor expects, so a 1-D bulk copy lands it ready to multiply.
@@ -262,7 +275,8 @@ __global__ void la_pack_kernel(const __nv_bfloat16* __restrict__ src, int rows, 
     else if (mode == 1) vr = (r / 64) * 128 + (r % 64);
     else vr = (r / 64) * 128 + 64 + (r % 64);
     const int t = vr / 128, rr = vr % 128, kb = c / 8, cc = c % 8;
-    const size_t off = ((size_t)t * KB + kb) * 8192 + (size_t)rr * 64 + ((cc ^ (rr & 7)) * 8);
+    const size_t blk = ((size_t)(t / LA_TPC) * KB + kb) * LA_TPC + (t % LA_TPC);
+    const size_t off = blk * 8192 + (size_t)rr * 64 + ((cc ^ (rr & 7)) * 8);
     *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(src + (size_t)r * K + c * 8);
   }
 }
@@ -274,7 +288,7 @@ extern "C" int64_t la_packed_bytes(int32_t rows, int32_t K) {
 
 extern "C" int32_t la_pack_weight(const void* src, int32_t rows, int32_t K, void* dst, int32_t mode,
                                   int32_t row_offset, void* stream) {
-  if (!src || !dst || rows < 1 || K < 64 || K % 64 || mode < 0 || mode > 2 ||
+  if (!src || !dst || rows < 1 || K < 64 || K % 64 || mode < 0 || mode > 2 || row_offset < 0 ||
       (mode && rows % 64)) {
     la_set_error("la_pack_weight: bad arguments (K %% 64 == 0; gate/up rows %% 64 == 0)");
     return LA_ERR_INVALID_CONFIG;

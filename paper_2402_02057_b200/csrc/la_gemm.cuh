@@ -21,9 +21,21 @@
 
 #include "la_common.cuh"
 
+// Tiles processed per stream-K unit: one step-row (B) load feeds two 128-row
+// weight tiles, halving the L2->SM traffic of the activations.
+#define LA_TPC 2
+
+// Packed activation layout ("LA rows"): [K/64 blocks][128 rows][64] bf16,
+// every 16 KB block the SWIZZLE_128B image of a 128 x 64 tile, so the first
+// n_pad rows of a k-block are ONE contiguous n_pad*128-byte bulk copy.
+__host__ __device__ __forceinline__ size_t la_act_off(int r, int k) {
+  return (size_t)(k >> 6) * 8192 + (size_t)r * 64 + ((((k >> 3) & 7) ^ (r & 7)) << 3) + (k & 7);
+}
+
 struct LaGemmArgs {
-  const __nv_bfloat16* a;   // packed weight tiles [n_tiles][kb][128*64]
-  int n_tiles;              // 128-row feature tiles
+  const __nv_bfloat16* a;   // packed weight tiles [n_tiles/2][kb][2][128*64]
+  const __nv_bfloat16* b;   // packed step rows [kb][128][64]
+  int n_tiles;              // 128-row feature tiles (even)
   int kb;                   // K / 64
   int max_segs;             // workspace segments per tile
   const FwdPlan* plan;
@@ -33,10 +45,10 @@ struct LaGemmArgs {
   unsigned long long* timing;
   // optional per-CTA trace [gridDim][4]: start, prologue done, MMA done, end
   unsigned long long* trace;
+  int debug;   // experiments: bit0 skip step-row loads, bit1 skip MMAs
 };
 
 struct LaGemm {
-  CUtensorMap b;     // step rows [128][K], box 64 x 16
   LaGemmArgs args;
   int grid;
 };
@@ -50,10 +62,12 @@ size_t la_packed_elems(int rows, int K);   // bf16 elements of a packed matrix
 __host__ __device__ __forceinline__ long la_cta_of(long u, long U, long P) {
   return ((u + 1) * P + U - 1) / U - 1;
 }
-// contributing CTAs [c0, c0 + n) of feature tile t
-__host__ __device__ __forceinline__ void la_tile_segs(int t, int kb, long U, long P, long& c0,
+// contributing CTAs [c0, c0 + n) of feature tile t (n_tiles tiles, LA_TPC per unit)
+__host__ __device__ __forceinline__ void la_tile_segs(int t, int kb, int n_tiles, long P, long& c0,
                                                       int& n) {
-  c0 = la_cta_of((long)t * kb, U, P);
-  long c1 = la_cta_of((long)(t + 1) * kb - 1, U, P);
+  const long U = (long)(n_tiles / LA_TPC) * kb;
+  const long pair = t / LA_TPC;
+  c0 = la_cta_of(pair * kb, U, P);
+  long c1 = la_cta_of((pair + 1) * kb - 1, U, P);
   n = (int)(c1 - c0 + 1);
 }

@@ -104,11 +104,12 @@ __global__ void la_set_cond_kernel(cudaGraphConditionalHandle h, const DevDecode
 // ------------------------------------------------------------ host setup
 static int build_gemm(LaGemm& g, const void* a_packed, int n_tiles, const void* b, int K) {
   memset(&g, 0, sizeof(g));
-  RET_IF(la_make_tmap(&g.b, b, LA_MAX_ROWS, K, 16));
+  n_tiles = (n_tiles + LA_TPC - 1) / LA_TPC * LA_TPC;   // packed buffers carry zero tiles
   g.args.a = reinterpret_cast<const __nv_bfloat16*>(a_packed);
+  g.args.b = reinterpret_cast<const __nv_bfloat16*>(b);
   g.args.n_tiles = n_tiles;
   g.args.kb = K / 64;
-  long U = (long)n_tiles * g.args.kb;
+  long U = (long)(n_tiles / LA_TPC) * g.args.kb;
   g.grid = (int)std::min<long>(la_sm_count(), U);
   g.args.max_segs = la_gemm_workspace_segs(n_tiles, g.args.kb, g.grid);
   return LA_OK;
@@ -191,13 +192,14 @@ int llama_create(la_engine* e) {
   p->head_tiles = (D.vocab + 127) / 128;
   RET_IF(build_gemm(p->head, p->lm_head, p->head_tiles, p->h, d));
   track(p->head);
-  RET_IF(lalloc(e, &p->pmax, (size_t)p->head_tiles * 128));
+  RET_IF(lalloc(e, &p->pmax, (size_t)(p->head_tiles + 1) * 128));
   RET_IF(lalloc(e, &p->ws, ws_need));
   RET_IF(lalloc(e, &p->timing, 32));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
   if (trace) RET_IF(lalloc(e, &p->trace, 4 * 256 * 4));
+  const int dbg = getenv("LA_GEMM_DEBUG") ? atoi(getenv("LA_GEMM_DEBUG")) : 0;
   auto fin = [&](LaGemm& gg, int kind) {
-    gg.args.plan = e->d_plan; gg.args.ws = p->ws;
+    gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.debug = dbg;
     gg.args.timing = p->timing + 8 * kind;
     gg.args.trace = trace ? p->trace + 256 * 4 * kind : nullptr;
   };

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) la_qkv_epi_kernel(LaQkvEpi e) {
   const int t = blockIdx.x;
   long c0;
   int nseg;
-  la_tile_segs(t, e.sp.kb, (long)e.sp.n_tiles * e.sp.kb, e.sp.grid, c0, nseg);
+  la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
   const int i = threadIdx.x & 63;
   const bool v_tile = t >= e.H + e.KVH;
   for (int tok = threadIdx.x >> 6; tok < n; tok += blockDim.x >> 6) {
@@ -76,7 +76,6 @@ __global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
   if (r >= P->n_rows) return;
   __shared__ float red[8];
   float* xr = e.x + (size_t)r * e.d;
-  const long U = (long)e.sp.n_tiles * e.sp.kb;
   float ss = 0.f;
   for (int f = threadIdx.x; f < e.d; f += blockDim.x) {
     float v;
@@ -88,7 +87,7 @@ __global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
         const int t = f >> 7;
         long c0;
         int nseg;
-        la_tile_segs(t, e.sp.kb, U, e.sp.grid, c0, nseg);
+        la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
         v += seg_sum(e.ws, t, e.sp.max_segs, nseg, r, f & 127);
       }
     }
@@ -96,8 +95,8 @@ __global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
     ss += v * v;
   }
   const float inv = rsqrtf(block_sum(ss, red) / e.d + e.eps);
-  __nv_bfloat16* hr = e.h + (size_t)r * e.d;
-  for (int f = threadIdx.x; f < e.d; f += blockDim.x) hr[f] = __float2bfloat16_rn(xr[f] * inv * e.g[f]);
+  for (int f = threadIdx.x; f < e.d; f += blockDim.x)
+    e.h[la_act_off(r, f)] = __float2bfloat16_rn(xr[f] * inv * e.g[f]);
 }
 
 // grid = ffn/64 tiles (64 gate + 64 up rows each), block = 256
@@ -108,12 +107,12 @@ __global__ void __launch_bounds__(256) la_swiglu_epi_kernel(LaSwigluEpi e) {
   const int t = blockIdx.x;
   long c0;
   int nseg;
-  la_tile_segs(t, e.sp.kb, (long)e.sp.n_tiles * e.sp.kb, e.sp.grid, c0, nseg);
+  la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
   const int i = threadIdx.x & 63;
   for (int tok = threadIdx.x >> 6; tok < n; tok += blockDim.x >> 6) {
     const float g = seg_sum(e.ws, t, e.sp.max_segs, nseg, tok, i);
     const float u = seg_sum(e.ws, t, e.sp.max_segs, nseg, tok, i + 64);
-    e.act[(size_t)tok * e.act_ld + t * 64 + i] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+    e.act[la_act_off(tok, t * 64 + i)] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
   }
 }
 
@@ -126,7 +125,7 @@ __global__ void __launch_bounds__(128) la_logits_epi_kernel(LaLogitsEpi e) {
   const int t = blockIdx.x;
   long c0;
   int nseg;
-  la_tile_segs(t, e.sp.kb, (long)e.sp.n_tiles * e.sp.kb, e.sp.grid, c0, nseg);
+  la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
   float best = -INFINITY;
   int bi = 0x7fffffff;
   const float* base = e.ws + ((size_t)t * e.sp.max_segs * 128 + tok) * 128;

@@ -26,7 +26,7 @@ struct LaResidNorm {
   const __nv_bfloat16* embed;    // non-null: x := embedding row (start of the step)
   float* x;                      // [128][d] fp32 residual stream
   const float* g;                // RMSNorm gain
-  __nv_bfloat16* h;              // [128][d]
+  __nv_bfloat16* h;              // packed LA rows (la_act_off)
   int d;
   float eps;
 };
@@ -35,7 +35,7 @@ struct LaSwigluEpi {
   const FwdPlan* plan;
   const float* ws;
   LaSplit sp;
-  __nv_bfloat16* act;
+  __nv_bfloat16* act;            // packed LA rows (la_act_off)
   int act_ld;
 };
 
