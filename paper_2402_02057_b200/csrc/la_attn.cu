@@ -1,19 +1,21 @@
 // Attention of the step rows (reference models.py:250-260 with the visibility
-// sets of layout.py:139-170), in two kernels:
+// sets of layout.py:139-170), as two kernels:
 //
-//  1. la_attn_prefix_kernel -- every step row sees the whole confirmed prefix
-//     (cache slots [0, ctx)), so that part is plain dense attention:
-//     flash-decoding split over NC key chunks x KV heads x 64-query-row
-//     blocks (GQA groups share the K/V tile), mma.sync bf16 tensor-core QK^T
-//     and PV with an online softmax; emits unnormalised partial O + (m, l).
-//  2. la_attn_chain_kernel -- merges the chunk partials in fixed order, then
-//     walks the row's chain of visible step keys in relative-position order
-//     (the paper's structured mask, generated per row from the plan -- never
-//     materialised) and finally the row itself.
+//  1. la_attn_chunks_kernel -- flash-decoding over NC+1 key chunks x KV heads
+//     x 64-query-row blocks (GQA groups share the K/V tile), mma.sync bf16
+//     QK^T and PV with an online softmax, unnormalised partial O + (m, l):
+//       chunks 0..NC-1: the confirmed prefix (cache slots [0, ctx)), which
+//         every step row sees -- dense, no mask;
+//       chunk NC: the step block (slots ctx + global row), masked by the
+//         paper's structured mask GENERATED in-kernel from the plan's per-row
+//         chains (a 128-bit visibility set per query row, never an M x M
+//         matrix in memory).
+//  2. la_attn_merge_kernel -- merges the chunk partials in chunk order and
+//     writes the normalised output (packed LA rows, the O-projection input).
 //
-// Both are layout-independent per row: a row's result depends only on ctx
-// and its own token chain, so lookahead-parallel shards reproduce the
-// single-device outputs bit for bit.
+// Layout independence: prefix chunking depends only on ctx, and step keys
+// sit at their GLOBAL row position with masked entries exactly zero, so a
+// row's result is bit-identical in every lookahead-parallel shard.
 #include <cuda_bf16.h>
 
 #include "la_attn.cuh"
@@ -74,26 +76,36 @@ __device__ __forceinline__ int chunk_keys(int ctx, int NC) {
 
 }  // namespace
 
-size_t la_attn_prefix_smem() { return 64 * 256 + 4 * kKeyTile * 256; }
+size_t la_attn_prefix_smem() { return 64 * 256 + 4 * kKeyTile * 256 + 64 * 4 * 4; }
 
-// grid = (KVH, NC, row blocks of 64 flattened (row, head-in-group) queries)
-__global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
+// grid = (KVH, NC + 1, row blocks of 64 flattened (row, head-in-group) queries)
+__global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
+  LA_PDL_ENTRY();
   const FwdPlan* P = a.plan;
   const int n_rows = P->n_rows, ctx = P->n_prefix;
-  if (n_rows == 0 || ctx == 0) return;
+  if (n_rows == 0) return;
   const int g = a.H / a.KVH;
   const int kvh = blockIdx.x, c = blockIdx.y, rb = blockIdx.z;
   const int nq = n_rows * g;
   if (rb * 64 >= nq) return;
-  const int CH = chunk_keys(ctx, a.NC);
-  const int k_begin = c * CH;
-  if (k_begin >= ctx) return;
-  const int k_end = min(ctx, k_begin + CH);
+  const bool step_chunk = c == a.NC;
+  int k_begin, k_end;
+  if (step_chunk) {
+    k_begin = ctx;
+    k_end = ctx + P->n_global;
+  } else {
+    if (ctx == 0) return;
+    const int CH = chunk_keys(ctx, a.NC);
+    k_begin = c * CH;
+    if (k_begin >= ctx) return;
+    k_end = min(ctx, k_begin + CH);
+  }
 
   extern __shared__ __align__(128) uint8_t attn_smem[];
   uint8_t* sQ = attn_smem;
   uint8_t* sK[2] = {sQ + 64 * 256, sQ + 64 * 256 + kKeyTile * 256};
   uint8_t* sV[2] = {sQ + 64 * 256 + 2 * kKeyTile * 256, sQ + 64 * 256 + 3 * kKeyTile * 256};
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(sQ + 64 * 256 + 4 * kKeyTile * 256);  // [64][4]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t kv_ld = (size_t)a.KVH * 128;
 
@@ -107,6 +119,21 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
       src = a.q + ((size_t)r * a.H + h) * 128 + ch * 8;
     }
     cp_async16(smem_u32(sQ) + swz(row, ch), src, ok);
+  }
+  if (step_chunk) {
+    // structured mask: a query row sees its chain's step keys and itself
+    for (int i = tid; i < 64 * 4; i += 128) sMask[i] = 0u;
+    __syncthreads();
+    for (int row = warp; row < 64; row += 4) {
+      const int qr = rb * 64 + row;
+      if (qr >= nq) continue;
+      const int r = qr / g;
+      const int n = P->chain_n[r];
+      for (int j = lane; j <= n; j += 32) {
+        const int key = (j < n ? P->chain[r][j] : P->slot[r]) - ctx;
+        atomicOr(&sMask[row * 4 + (key >> 5)], 1u << (key & 31));
+      }
+    }
   }
   auto load_kv = [&](int buf, int t0) {
     for (int i = tid; i < kKeyTile * 16; i += 128) {
@@ -127,6 +154,7 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const float sl2 = a.scale * kLog2e;
   const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+  const int qrow0 = warp * 16 + (lane >> 2);   // this thread's two query rows in the tile
 
   for (int t = 0; t < n_tiles; ++t) {
     const int buf = t & 1;
@@ -158,16 +186,20 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
         mma16816(s[2 * np + 1], qf[kk], b2, b3);
       }
     }
-    // mask keys past the chunk end, scale into log2 units
+    // mask (chunk end, structured step mask), scale into log2 units
     const int kbase = k_begin + t * kKeyTile;
     float mx0 = m0, mx1 = m1;
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        int key = kbase + n * 8 + (lane & 3) * 2 + (e & 1);
-        float v = key < k_end ? s[n][e] * sl2 : -INFINITY;
-        s[n][e] = v;
+        const int key = kbase + n * 8 + (lane & 3) * 2 + (e & 1);
+        bool vis = key < k_end;
+        if (step_chunk && vis) {
+          const int kg = key - ctx, row = qrow0 + (e >> 1) * 8;
+          vis = (sMask[row * 4 + (kg >> 5)] >> (kg & 31)) & 1u;
+        }
+        s[n][e] = vis ? s[n][e] * sl2 : -INFINITY;
       }
       mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
       mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
@@ -177,16 +209,18 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
     }
-    const float al0 = exp2f(m0 - mx0), al1 = exp2f(m1 - mx1);
+    // rows with nothing visible yet keep (m, l, o) = (-inf, 0, 0)
+    const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
+    const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
     m0 = mx0;
     m1 = mx1;
     float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
-      s[n][0] = exp2f(s[n][0] - m0);
-      s[n][1] = exp2f(s[n][1] - m0);
-      s[n][2] = exp2f(s[n][2] - m1);
-      s[n][3] = exp2f(s[n][3] - m1);
+      s[n][0] = exp2f(s[n][0] - b0);
+      s[n][1] = exp2f(s[n][1] - b0);
+      s[n][2] = exp2f(s[n][2] - b1);
+      s[n][3] = exp2f(s[n][3] - b1);
       rs0 += s[n][0] + s[n][1];
       rs1 += s[n][2] + s[n][3];
     }
@@ -206,10 +240,10 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
       for (int dp = 0; dp < 8; ++dp) {
         int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         int ch = dp * 2 + (lane >> 4);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(smem_u32(sV[buf]) + swz(key, ch), b0, b1, b2, b3);
-        mma16816(o[2 * dp], pa, b0, b1);
-        mma16816(o[2 * dp + 1], pa, b2, b3);
+        uint32_t v0, v1, v2, v3;
+        ldsm_x4_t(smem_u32(sV[buf]) + swz(key, ch), v0, v1, v2, v3);
+        mma16816(o[2 * dp], pa, v0, v1);
+        mma16816(o[2 * dp + 1], pa, v2, v3);
       }
     }
     __syncthreads();
@@ -223,7 +257,7 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
   // write unnormalised partial O and (m, l) in log2 units
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    int qr = rb * 64 + warp * 16 + (lane >> 2) + half * 8;
+    int qr = rb * 64 + qrow0 + half * 8;
     if (qr >= nq) continue;
     int r = qr / g, h = kvh * g + qr % g;
     size_t base = ((size_t)c * LA_MAX_ROWS + r) * a.H + h;
@@ -238,101 +272,45 @@ __global__ void __launch_bounds__(128) la_attn_prefix_kernel(LaAttnArgs a) {
   }
 }
 
-// grid = n rows (LA_MAX_ROWS), block = 512 (16 warps loop over heads).
-// Chain keys are processed 32 at a time, one key per lane (scores in one
-// round of loads), then P.V with lanes over head dims; the merge order --
-// prefix chunks, then chain keys in relative-position order, then the row
-// itself -- depends only on the row's chain, never on the step layout.
-__global__ void __launch_bounds__(512) la_attn_chain_kernel(LaAttnArgs a) {
+// grid = rows, block = 32 x min(H, 32): warp per (row, head); merges the
+// active prefix chunks in chunk order, then the step chunk, and writes the
+// normalised bf16 output into the packed O-projection input.
+__global__ void __launch_bounds__(1024) la_attn_merge_kernel(LaAttnArgs a) {
+  LA_PDL_ENTRY();
   const FwdPlan* P = a.plan;
   const int r = blockIdx.x;
   if (r >= P->n_rows) return;
-  __shared__ float sq[16][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int ctx = P->n_prefix, g = a.H / a.KVH;
+  const int ctx = P->n_prefix;
   const int n_chunks = ctx == 0 ? 0 : (ctx + chunk_keys(ctx, a.NC) - 1) / chunk_keys(ctx, a.NC);
-  const float sl2 = a.scale * kLog2e;
-  const size_t kv_ld = (size_t)a.KVH * 128;
-  const int nch = P->chain_n[r];
-  const int nkeys = nch + 1;                       // chain + the row itself
-  const int my_slot_self = P->slot[r];
   for (int h = warp; h < a.H; h += nw) {
-    const int kvh = h / g;
-    float m = -INFINITY, l = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int c = 0; c < n_chunks; ++c) {
-      size_t base = ((size_t)c * LA_MAX_ROWS + r) * a.H + h;
-      float2 ml = a.part_ml[base];
-      float4 po = reinterpret_cast<const float4*>(a.part_o + base * 128)[lane];
-      float mn = fmaxf(m, ml.x);
-      float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
-      o[0] = o[0] * s0 + po.x * s1;
-      o[1] = o[1] * s0 + po.y * s1;
-      o[2] = o[2] * s0 + po.z * s1;
-      o[3] = o[3] * s0 + po.w * s1;
-      l = l * s0 + ml.y * s1;
-      m = mn;
-    }
-    {
-      const __nv_bfloat16* qp = a.q + ((size_t)r * a.H + h) * 128 + lane * 4;
-      float2 q01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp));
-      float2 q23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp + 2));
-      sq[warp][lane * 4 + 0] = q01.x;
-      sq[warp][lane * 4 + 1] = q01.y;
-      sq[warp][lane * 4 + 2] = q23.x;
-      sq[warp][lane * 4 + 3] = q23.y;
-      __syncwarp();
-    }
-    for (int j0 = 0; j0 < nkeys; j0 += 32) {
-      const int j = j0 + lane;
-      const bool valid = j < nkeys;
-      const int slot = !valid ? my_slot_self : (j < nch ? P->chain[r][j] : my_slot_self);
-      float sc = -INFINITY;
-      if (valid) {
-        const uint4* kp = reinterpret_cast<const uint4*>(a.kc + (size_t)slot * kv_ld + kvh * 128);
-        float dot = 0.f;
+    float2 ml[9];
+    float4 po[9];
 #pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          uint4 u = kp[v];
-          const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            float2 f = __bfloat1622float2(b[k]);
-            dot = fmaf(sq[warp][v * 8 + 2 * k], f.x, dot);
-            dot = fmaf(sq[warp][v * 8 + 2 * k + 1], f.y, dot);
-          }
-        }
-        sc = dot * sl2;
-      }
-      float pmax = sc;
-#pragma unroll
-      for (int sh = 16; sh > 0; sh >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, sh));
-      const float mn = fmaxf(m, pmax);
-      const float s0 = exp2f(m - mn);
-      const float pj = valid ? exp2f(sc - mn) : 0.f;
-      float psum = pj;
-#pragma unroll
-      for (int sh = 16; sh > 0; sh >>= 1) psum += __shfl_xor_sync(0xffffffffu, psum, sh);
-      o[0] *= s0; o[1] *= s0; o[2] *= s0; o[3] *= s0;
-      l = l * s0 + psum;
-      m = mn;
-      const int cnt = min(32, nkeys - j0);
-#pragma unroll 4
-      for (int t = 0; t < cnt; ++t) {
-        const float pt = __shfl_sync(0xffffffffu, pj, t);
-        const int st = __shfl_sync(0xffffffffu, slot, t);
-        const __nv_bfloat16* vp = a.vc + (size_t)st * kv_ld + kvh * 128 + lane * 4;
-        float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vp));
-        float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vp + 2));
-        o[0] = fmaf(pt, v01.x, o[0]);
-        o[1] = fmaf(pt, v01.y, o[1]);
-        o[2] = fmaf(pt, v23.x, o[2]);
-        o[3] = fmaf(pt, v23.y, o[3]);
+    for (int i = 0; i < 9; ++i) {
+      const int c = i < n_chunks ? i : a.NC;
+      if (i <= n_chunks) {
+        const size_t base = ((size_t)c * LA_MAX_ROWS + r) * a.H + h;
+        ml[i] = a.part_ml[base];
+        po[i] = reinterpret_cast<const float4*>(a.part_o + base * 128)[lane];
       }
     }
-    __syncwarp();
+    float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      if (i <= n_chunks) {
+        const float mn = fmaxf(m, ml[i].x);
+        const float s0 = exp2f(m - mn), s1 = exp2f(ml[i].x - mn);
+        o0 = o0 * s0 + po[i].x * s1;
+        o1 = o1 * s0 + po[i].y * s1;
+        o2 = o2 * s0 + po[i].z * s1;
+        o3 = o3 * s0 + po[i].w * s1;
+        l = l * s0 + ml[i].y * s1;
+        m = mn;
+      }
     const float inv = 1.0f / l;
     __nv_bfloat16* dst = a.out + la_act_off(r, h * 128 + lane * 4);   // packed LA rows
-    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(o[0] * inv, o[1] * inv),
-                                                pack_bf16(o[2] * inv, o[3] * inv));
+    *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(o0 * inv, o1 * inv),
+                                                pack_bf16(o2 * inv, o3 * inv));
   }
 }

@@ -8,13 +8,13 @@ struct LaAttnArgs {
   const FwdPlan* plan;
   const __nv_bfloat16* q;        // [LA_MAX_ROWS][H][128] (RoPE applied)
   const __nv_bfloat16 *kc, *vc;  // layer base, [slots][KVH][128]
-  float* part_o;                 // [NC][LA_MAX_ROWS][H][128]
-  float2* part_ml;               // [NC][LA_MAX_ROWS][H]  (max, sum) in log2 units
+  float* part_o;                 // [NC+1][LA_MAX_ROWS][H][128] (chunk NC = step block)
+  float2* part_ml;               // [NC+1][LA_MAX_ROWS][H]  (max, sum) in log2 units
   __nv_bfloat16* out;            // packed LA rows [H*128/64][128][64] (la_act_off)
   int H, KVH, NC;
   float scale;                   // 1/sqrt(head_dim)
 };
 
-__global__ void la_attn_prefix_kernel(LaAttnArgs a);
-__global__ void la_attn_chain_kernel(LaAttnArgs a);
+__global__ void la_attn_chunks_kernel(LaAttnArgs a);
+__global__ void la_attn_merge_kernel(LaAttnArgs a);
 size_t la_attn_prefix_smem();

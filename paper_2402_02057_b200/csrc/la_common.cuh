@@ -52,6 +52,8 @@ struct FwdPlan {
   int n_rows;      // 0 -> every forward kernel exits immediately
   int n_pad;       // n_rows rounded up to 16 (MMA N)
   int n_prefix;    // ctx
+  int n_global;    // rows of the whole step layout (all LP shards); step keys
+                   // sit at slots n_prefix + global row
   int want_logits; // dump fp32 logits (parity hook)
   int ids[LA_MAX_ROWS];
   int pos[LA_MAX_ROWS];
@@ -111,3 +113,39 @@ __device__ __forceinline__ int la_round16(int x) { return (x + 15) & ~15; }
       return LA_ERR_CUDA;                                                     \
     }                                                                         \
   } while (0)
+
+// ------------------------------------------------ programmatic dependent launch
+// Every kernel of the step graph is launched with programmatic stream
+// serialisation: it lets its dependent start (launch_dependents) and then waits
+// for its own prerequisites (wait) before touching their outputs.  Without the
+// launch attribute both instructions are no-ops.
+__device__ __forceinline__ void la_pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void la_pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#define LA_PDL_ENTRY() \
+  do {                 \
+    la_pdl_trigger();  \
+    la_pdl_wait();     \
+  } while (0)
+
+#ifdef __CUDACC__
+// cudaLaunchKernelEx with the PDL attribute (pdl = false: plain launch)
+template <typename... KArgs, typename... Args>
+static inline cudaError_t la_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+#endif

@@ -494,7 +494,8 @@ extern "C" int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_
   if (rel[0] != 0) { la_set_error("query 0 must sit at relative position 0"); return LA_ERR_LAYOUT; }
   FwdPlan* P = new FwdPlan();
   memset(P, 0, sizeof(FwdPlan));
-  P->n_rows = n_rows; P->n_pad = (n_rows + 15) & ~15; P->n_prefix = n_prefix; P->want_logits = 1;
+  P->n_rows = n_rows; P->n_pad = (n_rows + 15) & ~15; P->n_prefix = n_prefix; P->n_global = n_rows;
+  P->want_logits = 1;
   for (int i = 0; i < n_rows; ++i) {
     if (rel[i] < 0 || rel[i] >= LA_MAX_CHAIN) { delete P; la_set_error("rel_pos out of range"); return LA_ERR_LAYOUT; }
     P->ids[i] = ids[i];

@@ -37,9 +37,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     la_gemm_kernel(const LaGemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   const FwdPlan* P = args.plan;
-  const int n_rows = P->n_rows;
-  if (n_rows == 0) return;                       // decode finished: nothing to do
-  const int n_pad = P->n_pad;
   uint8_t* sm = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = sm;
   uint8_t* sB = sA + kStages * kABytes;
@@ -50,10 +47,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (args.timing && threadIdx.x == 0) {
-    if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();
-  }
-  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 0] = globaltimer();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
@@ -64,7 +57,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
 
   const int kb = args.kb;
   const int n_units_t = args.n_tiles / LA_TPC;   // tile pairs
@@ -72,11 +64,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long Pn = gridDim.x;
   const long u_begin = (long)blockIdx.x * U / Pn;
   const long u_end = (long)(blockIdx.x + 1) * U / Pn;
+  const int n_pre = (int)min((long)kStages, u_end - u_begin);
 
-  if (warp == 0) {
+  // PDL: the weights do not depend on the previous kernel, so the first
+  // stages' weight tiles stream in while the previous kernel drains.
+  la_pdl_trigger();
+  uint64_t pol_w = 0;
+  if (warp == 0 && lane == 0) {
+    pol_w = ptx::policy_evict_first();   // weights: streamed once
+    for (int i = 0; i < n_pre; ++i) {
+      ptx::mbar_expect_tx_noarrive(&full[i], kABytes);
+      ptx::bulk_load(sA + i * kABytes, args.a + (size_t)(u_begin + i) * (kABytes / 2), kABytes,
+                     &full[i], pol_w);
+    }
+  }
+  la_pdl_wait();
+  if (args.timing && threadIdx.x == 0) {
+    if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();
+  }
+  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 0] = globaltimer();
+  const int n_rows = P->n_rows;
+  const int n_pad = P->n_pad;
+  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
+
+  if (n_rows == 0) {
+    // decode finished: drain the prefetched weight tiles before exiting
+    if (warp == 0 && lane == 0)
+      for (int i = 0; i < n_pre; ++i) {
+        ptx::mbar_arrive(&full[i]);
+        ptx::mbar_wait(&full[i], 0);
+      }
+  } else if (warp == 0) {
     // --------------------------------------------------------- producer
     if (lane == 0) {
-      const uint64_t pol_w = ptx::policy_evict_first();   // weights: streamed once
       const uint64_t pol_x = ptx::policy_evict_last();    // step rows: re-read by every CTA
       const uint32_t bbytes = (uint32_t)n_pad * 128;
       long it = 0;
@@ -84,10 +104,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k = (int)(u % kb);
         const int s = (int)(it % kStages);
         const uint32_t r = (uint32_t)(it / kStages);
-        if (r > 0) ptx::mbar_wait(&empty[s], (r - 1) & 1);
         const bool load_b = !(args.debug & 1);
-        ptx::mbar_expect_tx(&full[s], kABytes + (load_b ? bbytes : 0));
-        ptx::bulk_load(sA + s * kABytes, args.a + (size_t)u * (kABytes / 2), kABytes, &full[s], pol_w);
+        if (it < n_pre) {
+          ptx::mbar_expect_tx(&full[s], load_b ? bbytes : 0);   // weights already in flight
+        } else {
+          ptx::mbar_wait(&empty[s], (r - 1) & 1);
+          ptx::mbar_expect_tx(&full[s], kABytes + (load_b ? bbytes : 0));
+          ptx::bulk_load(sA + s * kABytes, args.a + (size_t)u * (kABytes / 2), kABytes, &full[s], pol_w);
+        }
         if (load_b)
           ptx::bulk_load(sB + s * kBBytes, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
       }
@@ -238,7 +262,7 @@ int la_gemm_workspace_segs(int n_tiles, int kb, int grid) {
   return (int)mx;
 }
 
-int la_gemm_launch(const LaGemm& g, cudaStream_t st) {
+int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(la_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -246,8 +270,8 @@ int la_gemm_launch(const LaGemm& g, cudaStream_t st) {
     if (e != cudaSuccess) { la_set_error("gemm smem attr: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }
     attr = true;
   }
-  la_gemm_kernel<<<g.grid, kThreads, kSmemBytes, st>>>(g.args);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = la_launch(la_gemm_kernel, dim3(g.grid), dim3(kThreads), kSmemBytes, st, pdl, g.args);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { la_set_error("gemm launch: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }
   return LA_OK;
 }

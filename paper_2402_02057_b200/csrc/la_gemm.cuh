@@ -54,7 +54,7 @@ struct LaGemm {
 };
 
 int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_rows);
-int la_gemm_launch(const LaGemm& g, cudaStream_t st);
+int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl = false);
 int la_gemm_workspace_segs(int n_tiles, int kb, int grid);
 int la_sm_count();
 size_t la_packed_elems(int rows, int K);   // bf16 elements of a packed matrix

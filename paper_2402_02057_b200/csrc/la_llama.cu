@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 
@@ -41,7 +42,7 @@ struct LlamaPath {
   float* x = nullptr;
   __nv_bfloat16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
   float* ws = nullptr;
-  float2* pmax = nullptr;
+  unsigned long long* keys = nullptr;     // [128] argmax keys
   float* part_o = nullptr;
   float2* part_ml = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
@@ -53,6 +54,7 @@ struct LlamaPath {
   LaGemm head{};
   int head_tiles = 0;
   int kernels_per_step = 0;
+  bool pdl = true;                        // programmatic dependent launch (LA_PDL=0: off)
   cudaStream_t cap = nullptr;
   cudaGraphExec_t loop_exec = nullptr;   // while(!done) { step }
   cudaGraphExec_t fwd_exec = nullptr;    // K1 + forward + owned argmax (LP)
@@ -62,27 +64,12 @@ struct LlamaPath {
 // ------------------------------------------------------------- kernels
 namespace {
 
-// per-row argmax over the LM-head tiles (lowest index on ties), then the
-// owned rows go to the decode state's global-row table
-__global__ void la_argmax_reduce_kernel(const FwdPlan* P, const float2* pmax, int n_tiles,
-                                        int* row_amax, DevDecode* dp) {
-  const int r = threadIdx.x;
-  if (r >= P->n_rows) return;
-  float best = -INFINITY;
-  int bi = 0x7fffffff;
-  for (int t = 0; t < n_tiles; ++t) {
-    float2 v = pmax[(size_t)t * 128 + r];
-    int idx = __float_as_int(v.y);
-    if (v.x > best || (v.x == best && idx < bi)) { best = v.x; bi = idx; }
-  }
-  row_amax[r] = bi;
-  if (dp && P->own[r]) dp->amax[P->grow[r]] = bi;
-}
-
 // prefill plan: causal chain over tokens[start, start+R)
 __global__ void la_plan_chain_kernel(FwdPlan* P, const int* tokens, int start, int R) {
+  LA_PDL_ENTRY();
   if (threadIdx.x == 0) {
-    P->n_rows = R; P->n_pad = (R + 15) & ~15; P->n_prefix = start; P->want_logits = 0;
+    P->n_rows = R; P->n_pad = (R + 15) & ~15; P->n_prefix = start; P->n_global = R;
+    P->want_logits = 0;
   }
   for (int r = threadIdx.x; r < R; r += blockDim.x) {
     P->ids[r] = tokens[start + r];
@@ -96,6 +83,7 @@ __global__ void la_plan_chain_kernel(FwdPlan* P, const int* tokens, int start, i
 }
 
 __global__ void la_set_cond_kernel(cudaGraphConditionalHandle h, const DevDecode* d) {
+  LA_PDL_ENTRY();
   cudaGraphSetConditional(h, d->done ? 0u : 1u);
 }
 
@@ -154,9 +142,9 @@ int llama_create(la_engine* e) {
   // prefix-attention split: ~2 CTAs per SM at full rows
   const int g = D.heads / D.kv_heads;
   const int rblocks = (R * g + 63) / 64;
-  p->NC = std::max(1, std::min(16, (2 * la_sm_count() + D.kv_heads * rblocks - 1) / (D.kv_heads * rblocks)));
-  RET_IF(lalloc(e, &p->part_o, (size_t)p->NC * R * D.heads * 128));
-  RET_IF(lalloc(e, &p->part_ml, (size_t)p->NC * R * D.heads));
+  p->NC = std::max(1, std::min(8, (2 * la_sm_count() + D.kv_heads * rblocks - 1) / (D.kv_heads * rblocks)));
+  RET_IF(lalloc(e, &p->part_o, (size_t)(p->NC + 1) * R * D.heads * 128));
+  RET_IF(lalloc(e, &p->part_ml, (size_t)(p->NC + 1) * R * D.heads));
   // RoPE tables (float64 on the host, stored fp32)
   {
     std::vector<float> c((size_t)e->slots * 64), s((size_t)e->slots * 64);
@@ -192,7 +180,7 @@ int llama_create(la_engine* e) {
   p->head_tiles = (D.vocab + 127) / 128;
   RET_IF(build_gemm(p->head, p->lm_head, p->head_tiles, p->h, d));
   track(p->head);
-  RET_IF(lalloc(e, &p->pmax, (size_t)(p->head_tiles + 1) * 128));
+  RET_IF(lalloc(e, &p->keys, LA_MAX_ROWS));
   RET_IF(lalloc(e, &p->ws, ws_need));
   RET_IF(lalloc(e, &p->timing, 32));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
@@ -206,7 +194,8 @@ int llama_create(la_engine* e) {
   for (int l = 0; l < D.layers; ++l) { fin(p->qkv[l], 0); fin(p->o[l], 1); fin(p->gu[l], 2); fin(p->down[l], 1); }
   fin(p->head, 3);
   CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
-  cudaError_t ce = cudaFuncSetAttribute(la_attn_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  p->pdl = !(getenv("LA_PDL") && !strcmp(getenv("LA_PDL"), "0"));
+  cudaError_t ce = cudaFuncSetAttribute(la_attn_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)la_attn_prefix_smem());
   if (ce != cudaSuccess) { la_set_error("attn smem attr: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
   return LA_OK;
@@ -224,6 +213,60 @@ void llama_destroy(la_engine* e) {
   e->llama = nullptr;
 }
 
+// ------------------------------------------------- per-kernel event timing
+// LA_KTIME=1 (eager mode only): CUDA events around every launch, summed per
+// kernel kind and printed to stderr after each decode -- a warm-cache
+// breakdown of the real step (ncu serialises and flushes caches).
+struct KTimer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  void begin(cudaStream_t s) { st = s; }
+  void mark(const char* name, cudaEvent_t a, cudaEvent_t b) { marks.push_back({name, {a, b}}); }
+};
+static KTimer g_kt;
+static cudaEvent_t kt_event() {
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+#define KT_BEGIN(st)                       \
+  cudaEvent_t _kt_a = nullptr;             \
+  if (g_kt.on) {                           \
+    _kt_a = kt_event();                    \
+    cudaEventRecord(_kt_a, st);            \
+  }
+#define KT_END(st, name)                   \
+  if (g_kt.on) {                           \
+    cudaEvent_t _kt_b = kt_event();        \
+    cudaEventRecord(_kt_b, st);            \
+    g_kt.mark(name, _kt_a, _kt_b);         \
+  }
+
+static void kt_report() {
+  if (!g_kt.on || g_kt.marks.empty()) return;
+  cudaDeviceSynchronize();
+  std::vector<std::pair<std::string, std::pair<double, int>>> acc;
+  for (auto& m : g_kt.marks) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, m.second.first, m.second.second);
+    bool found = false;
+    for (auto& a : acc)
+      if (a.first == m.first) { a.second.first += ms; a.second.second++; found = true; }
+    if (!found) acc.push_back({m.first, {ms, 1}});
+    cudaEventDestroy(m.second.first);
+    cudaEventDestroy(m.second.second);
+  }
+  double tot = 0;
+  for (auto& a : acc) tot += a.second.first;
+  fprintf(stderr, "[la ktime] %-18s %8s %10s %8s\n", "kernel", "count", "mean_us", "share");
+  for (auto& a : acc)
+    fprintf(stderr, "[la ktime] %-18s %8d %10.2f %7.1f%%\n", a.first.c_str(), a.second.second,
+            a.second.first * 1e3 / a.second.second, 100.0 * a.second.first / tot);
+  fprintf(stderr, "[la ktime] total %.3f ms\n", tot);
+  g_kt.marks.clear();
+}
+
 // ------------------------------------------------------------- forward
 static int launch_attn(la_engine* e, int l, cudaStream_t st) {
   LlamaPath* p = e->llama;
@@ -239,9 +282,18 @@ static int launch_attn(la_engine* e, int l, cudaStream_t st) {
   a.H = p->H; a.KVH = p->KVH; a.NC = p->NC;
   a.scale = 1.0f / sqrtf(128.0f);
   const int g = p->H / p->KVH;
-  dim3 grid(p->KVH, p->NC, (LA_MAX_ROWS * g + 63) / 64);
-  la_attn_prefix_kernel<<<grid, 128, la_attn_prefix_smem(), st>>>(a);
-  la_attn_chain_kernel<<<LA_MAX_ROWS, 512, 0, st>>>(a);
+  dim3 grid(p->KVH, p->NC + 1, (LA_MAX_ROWS * g + 63) / 64);
+  {
+    KT_BEGIN(st);
+    CK(la_launch(la_attn_chunks_kernel, grid, dim3(128), la_attn_prefix_smem(), st, p->pdl, a));
+    KT_END(st, "attn_chunks");
+  }
+  {
+    KT_BEGIN(st);
+    CK(la_launch(la_attn_merge_kernel, dim3(LA_MAX_ROWS), dim3(32 * std::min(p->H, 32)), 0, st,
+                 p->pdl, a));
+    KT_END(st, "attn_merge");
+  }
   CK(cudaGetLastError());
   return LA_OK;
 }
@@ -254,7 +306,9 @@ static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool emb
   r.sp = from ? split_of(*from) : LaSplit{1, 1, 1, 1};
   r.embed = embed ? p->embed : nullptr;
   r.x = p->x; r.g = g; r.h = p->h; r.d = p->d; r.eps = p->eps;
-  la_resid_norm_kernel<<<LA_MAX_ROWS, 256, 0, st>>>(r);
+  KT_BEGIN(st);
+  CK(la_launch(la_resid_norm_kernel, dim3(LA_MAX_ROWS), dim3(512), 0, st, p->pdl, r));
+  KT_END(st, from ? "resid_norm" : "embed_norm");
   CK(cudaGetLastError());
   return LA_OK;
 }
@@ -268,17 +322,41 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
   RET_IF(resid_norm(e, nullptr, p->lw[0].attn_norm, true, st));
   int n = 1;
   for (int l = 0; l < p->L; ++l) {
-    RET_IF(la_gemm_launch(p->qkv[l], st));
-    LaQkvEpi q{e->d_plan, p->ws, split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride,
-               p->rope_cos, p->rope_sin, p->H, p->KVH};
-    la_qkv_epi_kernel<<<p->H + 2 * p->KVH, 256, 0, st>>>(q);
+    {
+      KT_BEGIN(st);
+      RET_IF(la_gemm_launch(p->qkv[l], st, p->pdl));
+      KT_END(st, "gemm_qkv");
+    }
+    {
+      LaQkvEpi q{e->d_plan, p->ws, split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride,
+                 p->rope_cos, p->rope_sin, p->H, p->KVH};
+      KT_BEGIN(st);
+      CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
+      KT_END(st, "qkv_epi");
+    }
     RET_IF(launch_attn(e, l, st));
-    RET_IF(la_gemm_launch(p->o[l], st));
+    {
+      KT_BEGIN(st);
+      RET_IF(la_gemm_launch(p->o[l], st, p->pdl));
+      KT_END(st, "gemm_o");
+    }
     RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st));
-    RET_IF(la_gemm_launch(p->gu[l], st));
-    LaSwigluEpi sw{e->d_plan, p->ws, split_of(p->gu[l]), p->act, p->ffn};
-    la_swiglu_epi_kernel<<<p->ffn / 64, 256, 0, st>>>(sw);
-    RET_IF(la_gemm_launch(p->down[l], st));
+    {
+      KT_BEGIN(st);
+      RET_IF(la_gemm_launch(p->gu[l], st, p->pdl));
+      KT_END(st, "gemm_gu");
+    }
+    {
+      LaSwigluEpi sw{e->d_plan, p->ws, split_of(p->gu[l]), p->act, p->ffn};
+      KT_BEGIN(st);
+      CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, sw));
+      KT_END(st, "swiglu_epi");
+    }
+    {
+      KT_BEGIN(st);
+      RET_IF(la_gemm_launch(p->down[l], st, p->pdl));
+      KT_END(st, "gemm_down");
+    }
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
     RET_IF(resid_norm(e, &p->down[l], next, false, st));
     CK(cudaGetLastError());
@@ -290,11 +368,17 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
 
 static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
   LlamaPath* p = e->llama;
-  RET_IF(la_gemm_launch(p->head, st));
-  LaLogitsEpi lg{e->d_plan, p->ws, split_of(p->head), p->pmax, p->logits, p->V};
-  la_logits_epi_kernel<<<p->head_tiles, 128, 0, st>>>(lg);
-  la_argmax_reduce_kernel<<<1, 128, 0, st>>>(e->d_plan, p->pmax, p->head_tiles, p->row_amax,
-                                            scatter ? e->d_dec : nullptr);
+  {
+    KT_BEGIN(st);
+    RET_IF(la_gemm_launch(p->head, st, p->pdl));
+    KT_END(st, "gemm_head");
+  }
+  KT_BEGIN(st);
+  LaLogitsEpi lg{e->d_plan, p->ws, split_of(p->head), p->keys, p->logits, p->V};
+  CK(la_launch(la_logits_epi_kernel, dim3(p->head_tiles, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, lg));
+  CK(la_launch(la_argmax_finish_kernel, dim3(1), dim3(LA_MAX_ROWS), 0, st, p->pdl, e->d_plan,
+               p->keys, p->row_amax, scatter ? e->d_dec : nullptr));
+  KT_END(st, "logits_argmax");
   CK(cudaGetLastError());
   *nk += 3;
   return LA_OK;
@@ -324,15 +408,22 @@ int llama_forward_plan(la_engine* e, float* d_logits, cudaStream_t st) {
 // one step's kernels: K1 -> forward -> argmax (-> K10 -> commit)
 static int record_step(la_engine* e, cudaStream_t st, bool finish, int* nk) {
   LlamaPath* p = e->llama;
-  la_step_build_kernel<<<1, 256, 0, st>>>(e->d_dec, e->d_plan);
+  {
+    KT_BEGIN(st);
+    CK(la_launch(la_step_build_kernel, dim3(1), dim3(256), 0, st, p->pdl, e->d_dec, e->d_plan));
+    KT_END(st, "step_build");
+  }
   CK(cudaGetLastError());
   *nk += 1;
   RET_IF(forward_layers(e, st, nk));
   RET_IF(forward_head(e, st, true, nk));
   if (finish) {
-    la_step_finish_kernel<<<1, 256, 0, st>>>(e->d_dec);
-    la_kv_commit_kernel<<<std::max(1, std::min(148, p->L * e->row_bytes / 16 / 256)), 256, 0, st>>>(
-        e->d_dec, (uint8_t*)e->kc, (uint8_t*)e->vc, p->L, e->slots, e->row_bytes);
+    KT_BEGIN(st);
+    CK(la_launch(la_step_finish_kernel, dim3(1), dim3(256), 0, st, p->pdl, e->d_dec));
+    KT_END(st, "step_finish+commit");
+    CK(la_launch(la_kv_commit_kernel, dim3(std::max(1, std::min(148, p->L * e->row_bytes / 16 / 256))),
+                 dim3(256), 0, st, p->pdl, (const DevDecode*)e->d_dec, (uint8_t*)e->kc,
+                 (uint8_t*)e->vc, p->L, e->slots, e->row_bytes));
     CK(cudaGetLastError());
     *nk += 2;
   }
@@ -356,7 +447,8 @@ static int build_loop_graph(la_engine* e) {
   CK(cudaStreamBeginCaptureToGraph(p->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   int nk = 0;
   int rc = record_step(e, p->cap, true, &nk);
-  la_set_cond_kernel<<<1, 1, 0, p->cap>>>(handle, e->d_dec);
+  cudaError_t lce = la_launch(la_set_cond_kernel, dim3(1), dim3(1), 0, p->cap, p->pdl, handle, (const DevDecode*)e->d_dec);
+  if (lce != cudaSuccess && rc == LA_OK) { la_set_error("set_cond launch: %s", cudaGetErrorString(lce)); rc = LA_ERR_CUDA; }
   cudaGraph_t captured;
   cudaError_t ce = cudaStreamEndCapture(p->cap, &captured);
   if (rc != LA_OK) { cudaGraphDestroy(g); return rc; }
@@ -371,6 +463,9 @@ static int build_loop_graph(la_engine* e) {
 // LA_LAUNCH_MODE=eager: host loop of plain launches (profilers cannot see
 // kernel nodes inside conditional graphs); default: one WHILE-graph launch.
 static int eager_loop(la_engine* e, cudaStream_t st, int* launches) {
+  g_kt.on = getenv("LA_KTIME") != nullptr;
+  const bool saved_pdl = e->llama->pdl;
+  if (g_kt.on) e->llama->pdl = false;   // events between kernels would serialise anyway
   static thread_local int* pinned = nullptr;
   if (!pinned) CK(cudaMallocHost(&pinned, sizeof(int)));
   int nk = 0;
@@ -383,6 +478,9 @@ static int eager_loop(la_engine* e, cudaStream_t st, int* launches) {
     }
   }
   *launches = nk;
+  kt_report();
+  g_kt.on = false;
+  e->llama->pdl = saved_pdl;
   return LA_OK;
 }
 

@@ -8,7 +8,10 @@
 //   QKV     -> rotate-half RoPE on q, k; q to the Q buffer, k/v to the cache slot
 //   O, down -> residual add + the next RMSNorm (one CTA per row)
 //   gate/up -> SwiGLU
-//   LM head -> per-tile (max, argmax) (+ optional fp32 logits dump)
+//   LM head -> per-row (max, argmax) via one 64-bit atomicMax per (tile, row)
+// Every thread handles 4 consecutive features and issues the loads of all
+// segments before summing (latency-bound otherwise: ~10 segments per element
+// for the narrow O / down projections).
 #include <cuda_bf16.h>
 
 #include "la_gemm.cuh"
@@ -16,11 +19,38 @@
 
 namespace {
 
-__device__ __forceinline__ float seg_sum(const float* ws, int t, int max_segs, int nseg, int tok, int f) {
-  const float* p = ws + ((size_t)t * max_segs * 128 + tok) * 128 + f;
-  float acc = 0.f;
-  for (int s = 0; s < nseg; ++s) acc += __ldcg(p + (size_t)s * 128 * 128);
+constexpr int kMaxSegUnroll = 16;
+
+// sum over segments of 4 consecutive features (f4 = f/4) of token tok, tile t
+__device__ __forceinline__ float4 seg_sum4(const float* ws, int t, int max_segs, int nseg, int tok,
+                                           int f) {
+  const float4* p = reinterpret_cast<const float4*>(ws + ((size_t)t * max_segs * 128 + tok) * 128 + f);
+  constexpr size_t stride = 128 * 128 / 4;
+  float4 v[kMaxSegUnroll];
+#pragma unroll
+  for (int s = 0; s < kMaxSegUnroll; ++s)
+    if (s < nseg) v[s] = __ldcg(p + s * stride);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < kMaxSegUnroll; ++s)
+    if (s < nseg) { acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w; }
+  for (int s = kMaxSegUnroll; s < nseg; ++s) {   // rare: very narrow GEMMs
+    float4 w = __ldcg(p + s * stride);
+    acc.x += w.x; acc.y += w.y; acc.z += w.z; acc.w += w.w;
+  }
   return acc;
+}
+
+__device__ __forceinline__ int tile_nseg(const LaSplit& sp, int t) {
+  long c0;
+  int n;
+  la_tile_segs(t, sp.kb, sp.n_tiles, sp.grid, c0, n);
+  return n;
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
 }
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -35,115 +65,145 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-}  // namespace
-
-// grid = H + 2*KVH tiles (one attention head each), block = 256
-__global__ void __launch_bounds__(256) la_qkv_epi_kernel(LaQkvEpi e) {
-  const FwdPlan* P = e.plan;
-  const int n = P->n_rows;
-  if (n == 0) return;
-  const int t = blockIdx.x;
-  long c0;
-  int nseg;
-  la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
-  const int i = threadIdx.x & 63;
-  const bool v_tile = t >= e.H + e.KVH;
-  for (int tok = threadIdx.x >> 6; tok < n; tok += blockDim.x >> 6) {
-    float a = seg_sum(e.ws, t, e.sp.max_segs, nseg, tok, i);
-    float b = seg_sum(e.ws, t, e.sp.max_segs, nseg, tok, i + 64);
-    __nv_bfloat16* dst;
-    if (t < e.H) dst = e.q_out + ((size_t)tok * e.H + t) * 128;
-    else if (!v_tile) dst = e.kc + ((size_t)P->slot[tok] * e.KVH + (t - e.H)) * 128;
-    else dst = e.vc + ((size_t)P->slot[tok] * e.KVH + (t - e.H - e.KVH)) * 128;
-    if (!v_tile) {
-      // rotate-half RoPE at the row's absolute position
-      const float c = e.rope_cos[(size_t)P->pos[tok] * 64 + i];
-      const float s = e.rope_sin[(size_t)P->pos[tok] * 64 + i];
-      const float a2 = a * c - b * s, b2 = b * c + a * s;
-      a = a2;
-      b = b2;
-    }
-    dst[i] = __float2bfloat16_rn(a);
-    dst[i + 64] = __float2bfloat16_rn(b);
-  }
+// order-preserving key: larger value wins, then the LOWER index
+__device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+  uint32_t u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)u << 32) | (uint32_t)(0x7fffffff - idx);
 }
 
-// grid = rows, block = 256: x (+)= sum of segment partials (or := embedding
-// row), then RMSNorm -> bf16 GEMM input
-__global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
+}  // namespace
+
+// grid = (H + 2*KVH tiles, rows/8), block = 128: thread = (token, 4 rotary pairs)
+__global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
+  LA_PDL_ENTRY();
+  const FwdPlan* P = e.plan;
+  const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
+  if (tok >= P->n_rows) return;
+  const int t = blockIdx.x;
+  const int nseg = tile_nseg(e.sp, t);
+  const int i0 = (threadIdx.x & 15) * 4;
+  float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
+  float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
+  const bool v_tile = t >= e.H + e.KVH;
+  __nv_bfloat16* dst;
+  if (t < e.H) dst = e.q_out + ((size_t)tok * e.H + t) * 128;
+  else if (!v_tile) dst = e.kc + ((size_t)P->slot[tok] * e.KVH + (t - e.H)) * 128;
+  else dst = e.vc + ((size_t)P->slot[tok] * e.KVH + (t - e.H - e.KVH)) * 128;
+  if (!v_tile) {
+    // rotate-half RoPE at the row's absolute position
+    const float4 c = *reinterpret_cast<const float4*>(e.rope_cos + (size_t)P->pos[tok] * 64 + i0);
+    const float4 s = *reinterpret_cast<const float4*>(e.rope_sin + (size_t)P->pos[tok] * 64 + i0);
+    const float4 a2 = make_float4(a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y,
+                                  a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
+    const float4 b2 = make_float4(b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y,
+                                  b.z * c.z + a.z * s.z, b.w * c.w + a.w * s.w);
+    a = a2;
+    b = b2;
+  }
+  *reinterpret_cast<uint2*>(dst + i0) = make_uint2(pack2(a.x, a.y), pack2(a.z, a.w));
+  *reinterpret_cast<uint2*>(dst + i0 + 64) = make_uint2(pack2(b.x, b.y), pack2(b.z, b.w));
+}
+
+// grid = rows, block = 512: x (+)= sum of segment partials (or := embedding
+// row), then RMSNorm -> bf16 GEMM input (packed LA rows)
+__global__ void __launch_bounds__(512) la_resid_norm_kernel(LaResidNorm e) {
+  LA_PDL_ENTRY();
   const FwdPlan* P = e.plan;
   const int r = blockIdx.x;
   if (r >= P->n_rows) return;
-  __shared__ float red[8];
+  __shared__ float red[16];
   float* xr = e.x + (size_t)r * e.d;
   float ss = 0.f;
-  for (int f = threadIdx.x; f < e.d; f += blockDim.x) {
-    float v;
+  for (int f = threadIdx.x * 4; f < e.d; f += blockDim.x * 4) {
+    float4 v;
     if (e.embed) {
-      v = __bfloat162float(e.embed[(size_t)P->ids[r] * e.d + f]);
+      const __nv_bfloat16* er = e.embed + (size_t)P->ids[r] * e.d + f;
+      float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(er));
+      float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(er + 2));
+      v = make_float4(lo.x, lo.y, hi.x, hi.y);
     } else {
-      v = xr[f];
+      v = *reinterpret_cast<const float4*>(xr + f);
       if (e.ws) {
         const int t = f >> 7;
-        long c0;
-        int nseg;
-        la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
-        v += seg_sum(e.ws, t, e.sp.max_segs, nseg, r, f & 127);
+        const float4 p = seg_sum4(e.ws, t, e.sp.max_segs, tile_nseg(e.sp, t), r, f & 127);
+        v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
       }
     }
-    xr[f] = v;
-    ss += v * v;
+    *reinterpret_cast<float4*>(xr + f) = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   const float inv = rsqrtf(block_sum(ss, red) / e.d + e.eps);
-  for (int f = threadIdx.x; f < e.d; f += blockDim.x)
-    e.h[la_act_off(r, f)] = __float2bfloat16_rn(xr[f] * inv * e.g[f]);
-}
-
-// grid = ffn/64 tiles (64 gate + 64 up rows each), block = 256
-__global__ void __launch_bounds__(256) la_swiglu_epi_kernel(LaSwigluEpi e) {
-  const FwdPlan* P = e.plan;
-  const int n = P->n_rows;
-  if (n == 0) return;
-  const int t = blockIdx.x;
-  long c0;
-  int nseg;
-  la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
-  const int i = threadIdx.x & 63;
-  for (int tok = threadIdx.x >> 6; tok < n; tok += blockDim.x >> 6) {
-    const float g = seg_sum(e.ws, t, e.sp.max_segs, nseg, tok, i);
-    const float u = seg_sum(e.ws, t, e.sp.max_segs, nseg, tok, i + 64);
-    e.act[la_act_off(tok, t * 64 + i)] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+  for (int f = threadIdx.x * 4; f < e.d; f += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + f);
+    const float4 g = *reinterpret_cast<const float4*>(e.g + f);
+    *reinterpret_cast<uint2*>(e.h + la_act_off(r, f)) =
+        make_uint2(pack2(v.x * inv * g.x, v.y * inv * g.y), pack2(v.z * inv * g.z, v.w * inv * g.w));
   }
 }
 
-// grid = LM-head tiles, block = 128 (thread = token): per-tile (max, argmax)
-// over the tile's 128 vocabulary rows, ties -> lowest id (sampling.py:17-19)
-__global__ void __launch_bounds__(128) la_logits_epi_kernel(LaLogitsEpi e) {
+// grid = (ffn/64 tiles, rows/8), block = 128: thread = (token, 4 outputs)
+__global__ void __launch_bounds__(128) la_swiglu_epi_kernel(LaSwigluEpi e) {
+  LA_PDL_ENTRY();
   const FwdPlan* P = e.plan;
-  const int tok = threadIdx.x;
+  const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
   if (tok >= P->n_rows) return;
   const int t = blockIdx.x;
-  long c0;
-  int nseg;
-  la_tile_segs(t, e.sp.kb, e.sp.n_tiles, e.sp.grid, c0, nseg);
-  float best = -INFINITY;
-  int bi = 0x7fffffff;
-  const float* base = e.ws + ((size_t)t * e.sp.max_segs * 128 + tok) * 128;
-  for (int f4 = 0; f4 < 32; ++f4) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < nseg; ++s) {
-      float4 v = __ldcg(reinterpret_cast<const float4*>(base + (size_t)s * 128 * 128) + f4);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-    const float vals[4] = {acc.x, acc.y, acc.z, acc.w};
+  const int nseg = tile_nseg(e.sp, t);
+  const int i0 = (threadIdx.x & 15) * 4;
+  const float4 g = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
+  const float4 u = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
+  auto sw = [](float gg, float uu) { return gg / (1.0f + __expf(-gg)) * uu; };
+  *reinterpret_cast<uint2*>(e.act + la_act_off(tok, t * 64 + i0)) =
+      make_uint2(pack2(sw(g.x, u.x), sw(g.y, u.y)), pack2(sw(g.z, u.z), sw(g.w, u.w)));
+}
+
+// grid = (LM-head tiles, rows/8), block = 128: thread = (token, 8 vocabulary
+// rows); the row's argmax is folded with one 64-bit atomicMax per (tile, row)
+// whose key orders by value then by LOWER index (sampling.py:17-19), so the
+// result does not depend on arrival order.
+__global__ void __launch_bounds__(128) la_logits_epi_kernel(LaLogitsEpi e) {
+  LA_PDL_ENTRY();
+  const FwdPlan* P = e.plan;
+  const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
+  const bool valid = tok < P->n_rows;
+  const int t = blockIdx.x;
+  const int nseg = tile_nseg(e.sp, t);
+  const int f0 = (threadIdx.x & 15) * 8;
+  unsigned long long best = 0ull;
+  if (valid) {
+    const float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0);
+    const float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0 + 4);
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int fg = t * 128 + f4 * 4 + q;
+    for (int q = 0; q < 8; ++q) {
+      const int fg = t * 128 + f0 + q;
       if (fg < e.V) {
-        if (e.logits) e.logits[(size_t)tok * e.V + fg] = vals[q];
-        if (vals[q] > best) { best = vals[q]; bi = fg; }
+        if (e.logits) e.logits[(size_t)tok * e.V + fg] = v[q];
+        unsigned long long k = argmax_key(v[q], fg);
+        best = k > best ? k : best;
       }
     }
   }
-  e.pmax[(size_t)t * 128 + tok] = make_float2(best, __int_as_float(bi));
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    unsigned long long k = __shfl_xor_sync(0xffffffffu, best, o);
+    best = k > best ? k : best;
+  }
+  if (valid && (threadIdx.x & 15) == 0 && best) atomicMax(e.keys + tok, best);
+}
+
+// per-row winner of the atomicMax keys -> row argmax; owned rows go to the
+// decode state's global-row table; keys are reset for the next forward
+__global__ void la_argmax_finish_kernel(const FwdPlan* P, unsigned long long* keys, int* row_amax,
+                                        DevDecode* dp) {
+  LA_PDL_ENTRY();
+  const int r = threadIdx.x;
+  if (r >= LA_MAX_ROWS) return;
+  const unsigned long long k = keys[r];
+  keys[r] = 0ull;
+  if (r >= P->n_rows) return;
+  const int idx = 0x7fffffff - (int)(uint32_t)(k & 0xffffffffu);
+  row_amax[r] = idx;
+  if (dp && P->own[r]) dp->amax[P->grow[r]] = idx;
 }

@@ -43,7 +43,7 @@ struct LaLogitsEpi {
   const FwdPlan* plan;
   const float* ws;
   LaSplit sp;
-  float2* pmax;                  // [tiles][128]
+  unsigned long long* keys;      // [128] per-row (value, -index) atomicMax keys
   float* logits;                 // [128][V] or null
   int V;
 };
@@ -52,3 +52,5 @@ __global__ void la_qkv_epi_kernel(LaQkvEpi e);
 __global__ void la_resid_norm_kernel(LaResidNorm e);
 __global__ void la_swiglu_epi_kernel(LaSwigluEpi e);
 __global__ void la_logits_epi_kernel(LaLogitsEpi e);
+__global__ void la_argmax_finish_kernel(const FwdPlan* P, unsigned long long* keys, int* row_amax,
+                                        DevDecode* dp);

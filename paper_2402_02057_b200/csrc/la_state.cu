@@ -19,16 +19,19 @@ __global__ void la_pool_seed_kernel(DevDecode* dp, const int* grams, int n, int 
 
 // K1: prepare_step (decoding.py:152-157) as one CTA.
 __global__ void __launch_bounds__(256) la_step_build_kernel(DevDecode* dp, FwdPlan* P) {
+  LA_PDL_ENTRY();
   la_step_build(*dp, *P);
 }
 
 // K10: finish_step (decoding.py:160-204) as one CTA.
 __global__ void __launch_bounds__(256) la_step_finish_kernel(DevDecode* dp) {
+  LA_PDL_ENTRY();
   la_step_finish(*dp);
 }
 
 // Per-row argmax merge into the global-row array (owned rows only).
 __global__ void la_scatter_amax_kernel(DevDecode* dp, const FwdPlan* P, const int* row_amax) {
+  LA_PDL_ENTRY();
   const int n = P->n_rows;
   for (int r = threadIdx.x; r < n; r += blockDim.x)
     if (P->own[r]) dp->amax[P->grow[r]] = row_amax[r];
@@ -36,6 +39,7 @@ __global__ void la_scatter_amax_kernel(DevDecode* dp, const FwdPlan* P, const in
 
 // Merge an all-gathered [world][LA_MAX_ROWS] argmax table (LP exchange).
 __global__ void la_merge_amax_kernel(DevDecode* dp, const int* gathered, int world) {
+  LA_PDL_ENTRY();
   for (int g = threadIdx.x; g < LA_MAX_ROWS; g += blockDim.x) {
     int v = -1;
     for (int r = 0; r < world; ++r) v = max(v, gathered[r * LA_MAX_ROWS + g]);
@@ -51,6 +55,7 @@ __global__ void la_merge_amax_kernel(DevDecode* dp, const int* gathered, int wor
 // can only alias the source of an i' <= i, already read by this thread.
 __global__ void la_kv_commit_kernel(const DevDecode* dp, uint8_t* kc, uint8_t* vc, int layers,
                                     int slots, int row_bytes) {
+  LA_PDL_ENTRY();
   const int n = dp->commit_n;
   if (dp->mode != LA_MODE_LOOKAHEAD || n <= 0) return;
   const int ctx = dp->commit_ctx, base = dp->commit_base;

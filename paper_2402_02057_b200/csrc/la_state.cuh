@@ -196,7 +196,7 @@ static __device__ void la_step_build(DevDecode& d, FwdPlan& P) {
   const int W = d.W, N = d.N, S = N - 1, c = s_c;
   if (d.mode == LA_MODE_AUTOREGRESSIVE) {
     if (tid == 0) {
-      P.n_rows = 1; P.n_pad = 16; P.n_prefix = d.ctx;
+      P.n_rows = 1; P.n_pad = 16; P.n_prefix = d.ctx; P.n_global = 1;
       P.ids[0] = d.last; P.pos[0] = d.ctx; P.slot[0] = d.ctx; P.grow[0] = 0;
       P.own[0] = 1; P.chain_n[0] = 0;
       d.amax[0] = -1;
@@ -224,6 +224,7 @@ static __device__ void la_step_build(DevDecode& d, FwdPlan& P) {
     P.n_rows = n;
     P.n_pad = la_round16(n);
     P.n_prefix = d.ctx;
+    P.n_global = M;
   }
   for (int g = tid; g < LA_MAX_ROWS; g += nth) d.amax[g] = -1;
   __syncthreads();

@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(1024) la_tiny_prefill(TinyModel m, TinyScratch
   for (int start = 0; start < n; start += LA_MAX_ROWS) {
     int R = min(LA_MAX_ROWS, n - start);
     if (threadIdx.x == 0) {
-      P->n_rows = R; P->n_pad = la_round16(R); P->n_prefix = start; P->want_logits = 0;
+      P->n_rows = R; P->n_pad = la_round16(R); P->n_prefix = start; P->n_global = R;
+      P->want_logits = 0;
     }
     for (int r = threadIdx.x; r < R; r += blockDim.x) {
       P->ids[r] = tokens[start + r];
