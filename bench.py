@@ -44,6 +44,32 @@ W, N, G = 15, 5, 15
 METRIC = "batch-1 decode tokens/s (greedy lookahead, W15 N5 G15)"
 UNIT = "tokens/s"
 
+# BASELINE.json configs[1..4] (configs[0] is the CPU-runnable tiny model, a
+# parity case).  cfg2 is the default single-GPU workload.
+CONFIGS = {
+    "cfg2": dict(preset="llama2-7b", W=15, N=5, G=15, prompt=512, new=512,
+                 name="llama2-7b-shaped W15 N5 G15 prompt512 new512 (cfg2)"),
+    "cfg3": dict(preset="codellama-7b", W=15, N=5, G=15, prompt=512, new=512,
+                 name="codellama-7b-shaped W15 N5 G15 prompt512 new512, LP over the job's GPUs (cfg3)"),
+    "cfg4": dict(preset="llama2-13b", W=10, N=5, G=10, prompt=3584, new=512,
+                 name="llama2-13b-shaped W10 N5 G10 prompt3584 new512, KV to 4096 (cfg4)"),
+    "cfg5": dict(preset="llama2-70b", W=15, N=5, G=15, prompt=512, new=512,
+                 name="llama2-70b-shaped W15 N5 G15 prompt512 new512 (cfg5)"),
+}
+
+
+def _apply_config(name):
+    global PROMPT_LEN, NEW_TOKENS, W, N, G, METRIC, WORKLOAD, PRESET
+    c = CONFIGS[name]
+    PROMPT_LEN, NEW_TOKENS, W, N, G = c["prompt"], c["new"], c["W"], c["N"], c["G"]
+    METRIC = f"batch-1 decode tokens/s (greedy lookahead, W{W} N{N} G{G})"
+    WORKLOAD = c["name"]
+    PRESET = c["preset"]
+
+
+WORKLOAD = CONFIGS["cfg2"]["name"]
+PRESET = "llama2-7b"
+
 
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
@@ -150,7 +176,8 @@ def cpu_reference_sample(cfg, ctx_mean, m_mean, s_mean, budget_s=20.0):
     Wg = rng.standard_normal((d, F), dtype=np.float32) * 0.02
     Wu = rng.standard_normal((d, F), dtype=np.float32) * 0.02
     Wd = rng.standard_normal((F, d), dtype=np.float32) * 0.02
-    T = int(ctx_mean)
+    T_full = int(ctx_mean)
+    T = min(T_full, 768)          # bounded sample; scaled linearly to T_full below
     x = rng.standard_normal((T, d), dtype=np.float32)
 
     def block(x):
@@ -179,12 +206,13 @@ def cpu_reference_sample(cfg, ctx_mean, m_mean, s_mean, budget_s=20.0):
         times.append(time.perf_counter() - t0)
         if time.perf_counter() > t_end or len(times) >= 5:
             break
-    t_chain_layer = min(times)
+    t_chain_layer = min(times) * (T_full / T)
     step_s = t_chain_layer * cfg.layers * m_mean
     return {
         "value": s_mean / step_s, "unit": UNIT, "cores": ncores, "kind": "port",
-        "sample": (f"one chain of {T} tokens through 1 of {cfg.layers} Llama-2-7B-shaped layers, "
-                   f"numpy fp32, {len(times)} reps, best {t_chain_layer:.3f}s; extrapolated to "
+        "sample": (f"one chain of {T} tokens (scaled x{T_full / T:.2f} to the mean context {T_full}) "
+                   f"through 1 of {cfg.layers} {PRESET}-shaped layers, numpy fp32, {len(times)} reps, "
+                   f"{t_chain_layer:.3f}s per chain-layer; extrapolated to "
                    f"{m_mean:.1f} chains x {cfg.layers} layers per step, S={s_mean:.3f} tokens/step"),
         "step_seconds_extrapolated": step_s,
     }
@@ -195,8 +223,8 @@ def run_reference(args):
     rank, world, _ = _dist()
     if rank != 0:
         return
-    from paper_2402_02057_b200.models import LLAMA2_7B
-    cfg = LLAMA2_7B
+    from paper_2402_02057_b200.models import PRESETS
+    cfg = PRESETS[PRESET]
     # mean context / rows of the workload's lookahead steps (prompt + half of
     # the generated tokens; M = (N-1)(W+c) with c = G, the steady state)
     ctx_mean = PROMPT_LEN + NEW_TOKENS // 2
@@ -214,9 +242,8 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": cb["step_seconds_extrapolated"] * 1e3 * NEW_TOKENS / s_mean,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic", "impl": "reference",
-           "config": {"workload": "llama2-7b-shaped W15 N5 G15 prompt512 new512 (cfg2)",
-                      "model": "llama2-7b-shaped", "global_batch": 1, "seq_len": PROMPT_LEN + NEW_TOKENS,
-                      "parallelism": "cpu"},
+           "config": {"workload": WORKLOAD, "model": PRESET + "-shaped", "global_batch": 1,
+                      "seq_len": PROMPT_LEN + NEW_TOKENS, "parallelism": "cpu"},
            "cpu_baseline": cb,
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -227,7 +254,7 @@ def run_ours(args):
     import torch
     import paper_2402_02057_b200 as la
     from paper_2402_02057_b200 import decoding as dec
-    from paper_2402_02057_b200.models import LLAMA2_7B
+    from paper_2402_02057_b200.models import PRESETS
     import ctypes as C
 
     rank, world, local = _dist()
@@ -235,7 +262,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = LLAMA2_7B
+    cfg = PRESETS[PRESET]
     model = la.LlamaModel(cfg, dtype="bf16", seed=0, max_context=PROMPT_LEN + NEW_TOKENS + 64,
                           device=local)
     prompt = _prompt(cfg.vocab)
@@ -310,8 +337,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": e2e_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompt (default_rng(0)), random-init N(0,0.02^2) bf16 weights",
-        "config": {"workload": "llama2-7b-shaped W15 N5 G15 prompt512 new512 (cfg2)",
-                   "model": "llama2-7b-shaped", "global_batch": 1,
+        "config": {"workload": WORKLOAD, "model": PRESET + "-shaped", "global_batch": 1,
                    "seq_len": PROMPT_LEN + NEW_TOKENS,
                    "parallelism": "lp%d" % world if world > 1 else "single",
                    "l2": "weights 13.5 GB >> 126 MB L2 (no flush needed)"},
@@ -345,7 +371,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     args = ap.parse_args()
+    _apply_config(args.config)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -1,17 +1,19 @@
 // Attention of the step rows (reference models.py:250-260 with the visibility
 // sets of layout.py:139-170), as two kernels:
 //
-//  1. la_attn_chunks_kernel -- flash-decoding over NC+1 key chunks x KV heads
-//     x 64-query-row blocks (GQA groups share the K/V tile), mma.sync bf16
-//     QK^T and PV with an online softmax, unnormalised partial O + (m, l):
-//       chunks 0..NC-1: the confirmed prefix (cache slots [0, ctx)), which
-//         every step row sees -- dense, no mask;
-//       chunk NC: the step block (slots ctx + global row), masked by the
-//         paper's structured mask GENERATED in-kernel from the plan's per-row
-//         chains (a 128-bit visibility set per query row, never an M x M
-//         matrix in memory).
-//  2. la_attn_merge_kernel -- merges the chunk partials in chunk order and
-//     writes the normalised output (packed LA rows, the O-projection input).
+//  1. la_attn_chunks_kernel -- flash attention over <= NC key chunks x KV
+//     heads x 128-query-row blocks (GQA groups share the K/V tile), mma.sync
+//     bf16 QK^T and PV with an online softmax and a double-buffered cp.async K/V
+//     pipeline.  The confirmed prefix (cache slots [0, ctx)) is dense -- every
+//     step row sees it; the last chunk continues into the step block (slots
+//     ctx + global row) under the paper's structured mask, GENERATED
+//     in-kernel from the plan's per-row chains (a 128-bit visibility set per
+//     query row, never an M x M matrix in memory).  One chunk per 128 prefix
+//     keys (at most NC): short contexts finish in one pass and write the
+//     output directly.
+//  2. la_attn_merge_kernel -- for multi-chunk contexts, merges the chunk
+//     partials in chunk order and writes the normalised output (packed LA
+//     rows, the O-projection input).
 //
 // Layout independence: prefix chunking depends only on ctx, and step keys
 // sit at their GLOBAL row position with masked entries exactly zero, so a
@@ -68,50 +70,52 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// keys per prefix chunk: ceil(ctx / NC) rounded up to the key tile; depends
-// on ctx only, so every shard of a step chunks the prefix identically
-__device__ __forceinline__ int chunk_keys(int ctx, int NC) {
-  return ((ctx + NC - 1) / NC + kKeyTile - 1) / kKeyTile * kKeyTile;
+// Prefix split: one chunk per >= kMinChunk keys (at most NC).  Depends on
+// ctx only, so every shard of a step chunks the prefix identically.  The
+// last chunk also owns the step block, so short contexts need ONE pass.
+__device__ __forceinline__ int n_chunks_of(int ctx, int NC, int min_chunk) {
+  return max(1, min(NC, (ctx + min_chunk - 1) / min_chunk));
+}
+__device__ __forceinline__ int chunk_keys(int ctx, int nch) {
+  return ((ctx + nch - 1) / nch + kKeyTile - 1) / kKeyTile * kKeyTile;
 }
 
 }  // namespace
 
-size_t la_attn_prefix_smem() { return 64 * 256 + 4 * kKeyTile * 256 + 64 * 4 * 4; }
+constexpr int kStages = 2;    // K/V tile pipeline depth (2 CTAs per SM)
 
-// grid = (KVH, NC + 1, row blocks of 64 flattened (row, head-in-group) queries)
-__global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
-  LA_PDL_ENTRY();
+size_t la_attn_prefix_smem(int qrows) { return qrows * 256 + kStages * 2 * kKeyTile * 256 + qrows * 4 * 4; }
+
+// grid = (KVH, NC, row blocks of kQRows flattened (row, head-in-group)
+// queries); kQRows / 16 warps
+template <int kQRows>
+__global__ void __launch_bounds__(kQRows * 2) la_attn_chunks_kernel(LaAttnArgs a) {
+  LA_PDL_ENTRY_PF(a.pf);
   const FwdPlan* P = a.plan;
   const int n_rows = P->n_rows, ctx = P->n_prefix;
   if (n_rows == 0) return;
   const int g = a.H / a.KVH;
   const int kvh = blockIdx.x, c = blockIdx.y, rb = blockIdx.z;
   const int nq = n_rows * g;
-  if (rb * 64 >= nq) return;
-  const bool step_chunk = c == a.NC;
-  int k_begin, k_end;
-  if (step_chunk) {
-    k_begin = ctx;
-    k_end = ctx + P->n_global;
-  } else {
-    if (ctx == 0) return;
-    const int CH = chunk_keys(ctx, a.NC);
-    k_begin = c * CH;
-    if (k_begin >= ctx) return;
-    k_end = min(ctx, k_begin + CH);
-  }
+  if (rb * kQRows >= nq) return;
+  const int nch = n_chunks_of(ctx, a.NC, a.min_chunk);
+  if (c >= nch) return;
+  const bool last = c == nch - 1;           // also owns the masked step block
+  const int CH = ctx > 0 ? chunk_keys(ctx, nch) : 0;
+  const int k_begin = min(ctx, c * CH);
+  const int k_end = last ? ctx + P->n_global : min(ctx, (c + 1) * CH);
 
   extern __shared__ __align__(128) uint8_t attn_smem[];
   uint8_t* sQ = attn_smem;
-  uint8_t* sK[2] = {sQ + 64 * 256, sQ + 64 * 256 + kKeyTile * 256};
-  uint8_t* sV[2] = {sQ + 64 * 256 + 2 * kKeyTile * 256, sQ + 64 * 256 + 3 * kKeyTile * 256};
-  uint32_t* sMask = reinterpret_cast<uint32_t*>(sQ + 64 * 256 + 4 * kKeyTile * 256);  // [64][4]
+  uint8_t* sKV = sQ + kQRows * 256;                              // [kStages][K, V]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(sKV + kStages * 2 * kKeyTile * 256);  // [kQRows][4]
+  const int nthr = blockDim.x, nwarp = nthr >> 5;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t kv_ld = (size_t)a.KVH * 128;
 
-  // ---- Q tile (64 query rows x 128 dims)
-  for (int i = tid; i < 64 * 16; i += 128) {
-    int row = i >> 4, ch = i & 15, qr = rb * 64 + row;
+  // ---- Q tile (128 query rows x 128 dims)
+  for (int i = tid; i < kQRows * 16; i += nthr) {
+    int row = i >> 4, ch = i & 15, qr = rb * kQRows + row;
     const __nv_bfloat16* src = a.q;
     bool ok = qr < nq;
     if (ok) {
@@ -120,12 +124,12 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
     }
     cp_async16(smem_u32(sQ) + swz(row, ch), src, ok);
   }
-  if (step_chunk) {
+  if (last) {
     // structured mask: a query row sees its chain's step keys and itself
-    for (int i = tid; i < 64 * 4; i += 128) sMask[i] = 0u;
+    for (int i = tid; i < kQRows * 4; i += nthr) sMask[i] = 0u;
     __syncthreads();
-    for (int row = warp; row < 64; row += 4) {
-      const int qr = rb * 64 + row;
+    for (int row = warp; row < kQRows; row += nwarp) {
+      const int qr = rb * kQRows + row;
       if (qr >= nq) continue;
       const int r = qr / g;
       const int n = P->chain_n[r];
@@ -135,17 +139,25 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
       }
     }
   }
-  auto load_kv = [&](int buf, int t0) {
-    for (int i = tid; i < kKeyTile * 16; i += 128) {
+  // keys [k_begin, k_end) are cache slots [k_begin, k_end): the prefix slots
+  // and, for the last chunk, the step slots ctx + global row right after them
+  const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+  auto load_kv = [&](int t) {
+    uint8_t* kb = sKV + (t % kStages) * 2 * kKeyTile * 256;
+    const int t0 = k_begin + t * kKeyTile;
+    for (int i = tid; i < kKeyTile * 16; i += nthr) {
       int row = i >> 4, ch = i & 15, key = t0 + row;
       bool ok = key < k_end;
       size_t off = ((size_t)(ok ? key : k_begin) * kv_ld) + kvh * 128 + ch * 8;
-      cp_async16(smem_u32(sK[buf]) + swz(row, ch), a.kc + off, ok);
-      cp_async16(smem_u32(sV[buf]) + swz(row, ch), a.vc + off, ok);
+      cp_async16(smem_u32(kb) + swz(row, ch), a.kc + off, ok);
+      cp_async16(smem_u32(kb + kKeyTile * 256) + swz(row, ch), a.vc + off, ok);
     }
   };
-  load_kv(0, k_begin);
-  cp_commit();
+#pragma unroll
+  for (int t = 0; t < kStages - 1; ++t) {
+    if (t < n_tiles) load_kv(t);
+    cp_commit();
+  }
 
   uint32_t qf[8][4];
   float o[16][4];
@@ -153,15 +165,15 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const float sl2 = a.scale * kLog2e;
-  const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
   const int qrow0 = warp * 16 + (lane >> 2);   // this thread's two query rows in the tile
 
   for (int t = 0; t < n_tiles; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < n_tiles) load_kv(buf ^ 1, k_begin + (t + 1) * kKeyTile);
+    if (t + kStages - 1 < n_tiles) load_kv(t + kStages - 1);
     cp_commit();
-    cp_wait<1>();
+    cp_wait<kStages - 1>();
     __syncthreads();
+    const uint8_t* sK = sKV + (t % kStages) * 2 * kKeyTile * 256;
+    const uint8_t* sV = sK + kKeyTile * 256;
     if (t == 0) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
@@ -181,12 +193,12 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
         int key = np * 16 + (lane & 7) + (lane >> 4) * 8;
         int ch = kk * 2 + ((lane >> 3) & 1);
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(smem_u32(sK[buf]) + swz(key, ch), b0, b1, b2, b3);
+        ldsm_x4(smem_u32(sK) + swz(key, ch), b0, b1, b2, b3);
         mma16816(s[2 * np], qf[kk], b0, b1);
         mma16816(s[2 * np + 1], qf[kk], b2, b3);
       }
     }
-    // mask (chunk end, structured step mask), scale into log2 units
+    // mask (range end; structured mask on step keys), scale into log2 units
     const int kbase = k_begin + t * kKeyTile;
     float mx0 = m0, mx1 = m1;
 #pragma unroll
@@ -195,7 +207,7 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
       for (int e = 0; e < 4; ++e) {
         const int key = kbase + n * 8 + (lane & 3) * 2 + (e & 1);
         bool vis = key < k_end;
-        if (step_chunk && vis) {
+        if (vis && key >= ctx) {
           const int kg = key - ctx, row = qrow0 + (e >> 1) * 8;
           vis = (sMask[row * 4 + (kg >> 5)] >> (kg & 31)) & 1u;
         }
@@ -241,7 +253,7 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
         int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         int ch = dp * 2 + (lane >> 4);
         uint32_t v0, v1, v2, v3;
-        ldsm_x4_t(smem_u32(sV[buf]) + swz(key, ch), v0, v1, v2, v3);
+        ldsm_x4_t(smem_u32(sV) + swz(key, ch), v0, v1, v2, v3);
         mma16816(o[2 * dp], pa, v0, v1);
         mma16816(o[2 * dp + 1], pa, v2, v3);
       }
@@ -254,12 +266,23 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
     l0 += __shfl_xor_sync(0xffffffffu, l0, off);
     l1 += __shfl_xor_sync(0xffffffffu, l1, off);
   }
-  // write unnormalised partial O and (m, l) in log2 units
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    int qr = rb * 64 + qrow0 + half * 8;
+    int qr = rb * kQRows + qrow0 + half * 8;
     if (qr >= nq) continue;
     int r = qr / g, h = kvh * g + qr % g;
+    if (nch == 1) {
+      // single pass: normalise and write the O-projection input directly
+      const float inv = 1.0f / (half ? l1 : l0);
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        int col = d * 8 + (lane & 3) * 2;
+        *reinterpret_cast<uint32_t*>(a.out + la_act_off(r, h * 128 + col)) =
+            pack_bf16(o[d][half * 2] * inv, o[d][half * 2 + 1] * inv);
+      }
+      continue;
+    }
+    // unnormalised partial O and (m, l) in log2 units
     size_t base = ((size_t)c * LA_MAX_ROWS + r) * a.H + h;
     float* dst = a.part_o + base * 128;
 #pragma unroll
@@ -272,33 +295,32 @@ __global__ void __launch_bounds__(128) la_attn_chunks_kernel(LaAttnArgs a) {
   }
 }
 
-// grid = rows, block = 32 x min(H, 32): warp per (row, head); merges the
+// grid = rows, block = 32 x min(H, 16): warp per (row, head); merges the
 // active prefix chunks in chunk order, then the step chunk, and writes the
 // normalised bf16 output into the packed O-projection input.
-__global__ void __launch_bounds__(1024) la_attn_merge_kernel(LaAttnArgs a) {
+__global__ void __launch_bounds__(512) la_attn_merge_kernel(LaAttnArgs a) {
   LA_PDL_ENTRY();
   const FwdPlan* P = a.plan;
   const int r = blockIdx.x;
   if (r >= P->n_rows) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int ctx = P->n_prefix;
-  const int n_chunks = ctx == 0 ? 0 : (ctx + chunk_keys(ctx, a.NC) - 1) / chunk_keys(ctx, a.NC);
+  const int n_chunks = n_chunks_of(P->n_prefix, a.NC, a.min_chunk);
+  if (n_chunks == 1) return;   // the chunk kernel already wrote the output
   for (int h = warp; h < a.H; h += nw) {
-    float2 ml[9];
-    float4 po[9];
+    float2 ml[8];
+    float4 po[8];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      const int c = i < n_chunks ? i : a.NC;
-      if (i <= n_chunks) {
-        const size_t base = ((size_t)c * LA_MAX_ROWS + r) * a.H + h;
+    for (int i = 0; i < 8; ++i) {
+      if (i < n_chunks) {
+        const size_t base = ((size_t)i * LA_MAX_ROWS + r) * a.H + h;
         ml[i] = a.part_ml[base];
         po[i] = reinterpret_cast<const float4*>(a.part_o + base * 128)[lane];
       }
     }
     float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
 #pragma unroll
-    for (int i = 0; i < 9; ++i)
-      if (i <= n_chunks) {
+    for (int i = 0; i < 8; ++i)
+      if (i < n_chunks) {
         const float mn = fmaxf(m, ml[i].x);
         const float s0 = exp2f(m - mn), s1 = exp2f(ml[i].x - mn);
         o0 = o0 * s0 + po[i].x * s1;
@@ -314,3 +336,6 @@ __global__ void __launch_bounds__(1024) la_attn_merge_kernel(LaAttnArgs a) {
                                                 pack_bf16(o2 * inv, o3 * inv));
   }
 }
+
+template __global__ void la_attn_chunks_kernel<64>(LaAttnArgs a);
+template __global__ void la_attn_chunks_kernel<128>(LaAttnArgs a);

@@ -5,6 +5,7 @@
 #include "la_common.cuh"
 
 struct LaAttnArgs {
+  LaPrefetch pf;                 // next GEMM's weights -> L2 (optional)
   const FwdPlan* plan;
   const __nv_bfloat16* q;        // [LA_MAX_ROWS][H][128] (RoPE applied)
   const __nv_bfloat16 *kc, *vc;  // layer base, [slots][KVH][128]
@@ -12,9 +13,11 @@ struct LaAttnArgs {
   float2* part_ml;               // [NC+1][LA_MAX_ROWS][H]  (max, sum) in log2 units
   __nv_bfloat16* out;            // packed LA rows [H*128/64][128][64] (la_act_off)
   int H, KVH, NC;
+  int min_chunk;                 // prefix keys per chunk at least (chunks = min(NC, ctx/min))
   float scale;                   // 1/sqrt(head_dim)
 };
 
+template <int kQRows>
 __global__ void la_attn_chunks_kernel(LaAttnArgs a);
 __global__ void la_attn_merge_kernel(LaAttnArgs a);
-size_t la_attn_prefix_smem();
+size_t la_attn_prefix_smem(int qrows);

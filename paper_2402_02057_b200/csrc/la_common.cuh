@@ -149,3 +149,49 @@ static inline cudaError_t la_launch(void (*kernel)(KArgs...), dim3 grid, dim3 bl
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 #endif
+
+// ------------------------------------------------------ L2 weight prefetch
+// The latency-bound kernels between two GEMMs (epilogues, attention, norms)
+// leave HBM idle.  They pull the NEXT GEMM's first weight units into L2
+// (cp.async.bulk.prefetch.L2) so HBM keeps streaming while they run: for
+// each GEMM CTA c, the first `frac` of its stream-K unit range.
+struct LaPrefetch {
+  const void* a;   // packed weights of the next GEMM (null: none)
+  int n_tiles, kb, tpc, grid;
+  float frac;
+};
+
+__device__ __forceinline__ void la_l2_prefetch_gemm(const LaPrefetch& pf) {
+  if (!pf.a || pf.frac <= 0.f) return;
+  // GEMM CTA c is prefetched by block (c mod nblk), thread c / nblk: the bulk
+  // prefetches spread over every SM's copy engine instead of one CTA's
+  const long nblk = (long)gridDim.x * gridDim.y * gridDim.z;
+  const long bid = (long)blockIdx.x + (long)gridDim.x * (blockIdx.y + (long)gridDim.y * blockIdx.z);
+  const long U = (long)(pf.n_tiles / pf.tpc) * pf.kb, P = pf.grid;
+  const char* base = reinterpret_cast<const char*>(pf.a);
+  for (long c = bid + (long)threadIdx.x * nblk; c < P; c += (long)blockDim.x * nblk) {
+    const long u0 = c * U / P, u1 = (c + 1) * U / P;
+    const long n = (long)((u1 - u0) * pf.frac + 0.999f);
+    for (long u = u0; u < u0 + n && u < u1; ++u) {
+      size_t off;
+      uint32_t bytes;
+      if (pf.tpc == 2) {
+        off = (size_t)u * 32768;
+        bytes = 32768;
+      } else {   // single-tile unit inside the pair-interleaved packing
+        const long t = u / pf.kb, k = u % pf.kb;
+        off = ((size_t)((t / 2) * pf.kb + k) * 2 + (t % 2)) * 16384;
+        bytes = 16384;
+      }
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(bytes)
+                   : "memory");
+    }
+  }
+}
+
+#define LA_PDL_ENTRY_PF(pf)   \
+  do {                        \
+    la_pdl_trigger();         \
+    la_l2_prefetch_gemm(pf);  \
+    la_pdl_wait();            \
+  } while (0)

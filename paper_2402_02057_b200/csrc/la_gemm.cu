@@ -25,7 +25,109 @@ constexpr int kABytes = LA_TPC * kTileBytes;   // weight tiles per unit
 constexpr int kBBytes = 128 * 128;             // <= 128 rows x 64 bf16
 constexpr int kThreads = 192;
 constexpr int kTmemCols = 512;                 // 2 buffers x LA_TPC tiles x 128 columns
-constexpr size_t kSmemBytes = 1024 + kStages * (kABytes + kBBytes) + 2 * kStages * 8 + 4 * 8 + 16;
+constexpr int kEpiLd = 33;                     // fused-epilogue staging [128 f][33]
+constexpr size_t kSmemBytes =
+    1024 + kStages * (kABytes + kBBytes) + 128 * kEpiLd * 4 + 2 * kStages * 8 + 4 * 8 + 16;
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// order-preserving argmax key: larger value wins, then the LOWER index
+__device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+  uint32_t u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)u << 32) | (uint32_t)(0x7fffffff - idx);
+}
+
+// Fused epilogue of one 32-token chunk of feature tile `ftile` held in
+// sEpi[f][j]; thread et (0..127) owns token j = et/4, quarter p = et%4.
+template <int EPI>
+__device__ __forceinline__ void epi_apply(const LaGemmArgs& a, const FwdPlan* P, int ftile, int c0,
+                                          int n_rows, const float* sEpi, int et) {
+  const int j = et >> 2, p = et & 3;
+  const int tok = c0 + j;
+  const bool valid = tok < n_rows;
+  if constexpr (EPI == LA_EPI_QKV) {
+    if (!valid) return;
+    __nv_bfloat16* dst;
+    bool rope = true;
+    if (ftile < a.H) {
+      dst = a.q_out + ((size_t)tok * a.H + ftile) * 128;
+    } else if (ftile < a.H + a.KVH) {
+      dst = a.kc + ((size_t)P->slot[tok] * a.KVH + (ftile - a.H)) * 128;
+    } else if (ftile < a.H + 2 * a.KVH) {
+      dst = a.vc + ((size_t)P->slot[tok] * a.KVH + (ftile - a.H - a.KVH)) * 128;
+      rope = false;
+    } else {
+      return;   // zero padding tile
+    }
+    if (rope) {
+      // rotate-half RoPE: (x_i, x_{i+64}) -> (x_i c - x_{i+64} s, x_{i+64} c + x_i s)
+      const float* cs = a.rope_cos + (size_t)P->pos[tok] * 64;
+      const float* sn = a.rope_sin + (size_t)P->pos[tok] * 64;
+      uint32_t lo[8], hi[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i0 = p * 16 + 2 * q, i1 = i0 + 1;
+        const float x0 = sEpi[i0 * kEpiLd + j], x1 = sEpi[i1 * kEpiLd + j];
+        const float y0 = sEpi[(i0 + 64) * kEpiLd + j], y1 = sEpi[(i1 + 64) * kEpiLd + j];
+        lo[q] = pack_bf16(x0 * cs[i0] - y0 * sn[i0], x1 * cs[i1] - y1 * sn[i1]);
+        hi[q] = pack_bf16(y0 * cs[i0] + x0 * sn[i0], y1 * cs[i1] + x1 * sn[i1]);
+      }
+      uint4* d0 = reinterpret_cast<uint4*>(dst + p * 16);
+      uint4* d1 = reinterpret_cast<uint4*>(dst + 64 + p * 16);
+      d0[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      d0[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+      d1[0] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      d1[1] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+    } else {
+      uint32_t w[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        w[q] = pack_bf16(sEpi[(p * 32 + 2 * q) * kEpiLd + j], sEpi[(p * 32 + 2 * q + 1) * kEpiLd + j]);
+      uint4* d = reinterpret_cast<uint4*>(dst + p * 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    }
+  } else if constexpr (EPI == LA_EPI_SWIGLU) {
+    if (!valid) return;
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i0 = p * 16 + 2 * q;
+      const float g0 = sEpi[i0 * kEpiLd + j], g1 = sEpi[(i0 + 1) * kEpiLd + j];
+      const float u0 = sEpi[(64 + i0) * kEpiLd + j], u1 = sEpi[(64 + i0 + 1) * kEpiLd + j];
+      w[q] = pack_bf16(g0 / (1.0f + __expf(-g0)) * u0, g1 / (1.0f + __expf(-g1)) * u1);
+    }
+    // 16 outputs = 2 swizzled 16-byte chunks of the packed LA-row layout
+    __nv_bfloat16* base = a.act;
+    const int k0 = ftile * 64 + p * 16;
+    *reinterpret_cast<uint4*>(base + la_act_off(tok, k0)) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(base + la_act_off(tok, k0 + 8)) = make_uint4(w[4], w[5], w[6], w[7]);
+  } else if constexpr (EPI == LA_EPI_LOGITS) {
+    unsigned long long best = 0ull;
+    if (valid) {
+#pragma unroll 8
+      for (int q = 0; q < 32; ++q) {
+        const int f = p * 32 + q, fg = ftile * 128 + f;
+        if (fg < a.V) {
+          const float v = sEpi[f * kEpiLd + j];
+          if (a.logits) a.logits[(size_t)tok * a.V + fg] = v;
+          const unsigned long long k = argmax_key(v, fg);
+          best = k > best ? k : best;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const unsigned long long k = __shfl_xor_sync(0xffffffffu, best, o);
+      best = k > best ? k : best;
+    }
+    if (valid && p == 0 && best) atomicMax(a.keys + tok, best);
+  }
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -33,6 +135,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     la_gemm_kernel(const LaGemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -45,6 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* sflag = reinterpret_cast<int*>(tmem_slot + 1);
+  float* sEpi = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -59,7 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   const int kb = args.kb;
-  const int n_units_t = args.n_tiles / LA_TPC;   // tile pairs
+  const int tpc = args.tpc;
+  const int n_units_t = args.n_tiles / tpc;      // unit tiles (pairs when tpc == 2)
   const long U = (long)n_units_t * kb;
   const long Pn = gridDim.x;
   const long u_begin = (long)blockIdx.x * U / Pn;
@@ -69,13 +175,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   // PDL: the weights do not depend on the previous kernel, so the first
   // stages' weight tiles stream in while the previous kernel drains.
   la_pdl_trigger();
+  // weight block of unit u: packed tiles are pair-interleaved per k-block, so
+  // a 2-tile unit is one 32 KB copy and a 1-tile unit one 16 KB copy
+  const uint32_t a_bytes = (uint32_t)tpc * kTileBytes;
+  auto a_src = [&](long u) -> const __nv_bfloat16* {
+    if (tpc == LA_TPC) return args.a + (size_t)u * (kABytes / 2);
+    const long t = u / kb, k = u % kb;
+    return args.a + ((size_t)((t / LA_TPC) * kb + k) * LA_TPC + (t % LA_TPC)) * (kTileBytes / 2);
+  };
   uint64_t pol_w = 0;
   if (warp == 0 && lane == 0) {
     pol_w = ptx::policy_evict_first();   // weights: streamed once
     for (int i = 0; i < n_pre; ++i) {
-      ptx::mbar_expect_tx_noarrive(&full[i], kABytes);
-      ptx::bulk_load(sA + i * kABytes, args.a + (size_t)(u_begin + i) * (kABytes / 2), kABytes,
-                     &full[i], pol_w);
+      ptx::mbar_expect_tx_noarrive(&full[i], a_bytes);
+      ptx::bulk_load(sA + i * kABytes, a_src(u_begin + i), a_bytes, &full[i], pol_w);
     }
   }
   la_pdl_wait();
@@ -109,8 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_expect_tx(&full[s], load_b ? bbytes : 0);   // weights already in flight
         } else {
           ptx::mbar_wait(&empty[s], (r - 1) & 1);
-          ptx::mbar_expect_tx(&full[s], kABytes + (load_b ? bbytes : 0));
-          ptx::bulk_load(sA + s * kABytes, args.a + (size_t)u * (kABytes / 2), kABytes, &full[s], pol_w);
+          ptx::mbar_expect_tx(&full[s], a_bytes + (load_b ? bbytes : 0));
+          ptx::bulk_load(sA + s * kABytes, a_src(u), a_bytes, &full[s], pol_w);
         }
         if (load_b)
           ptx::bulk_load(sB + s * kBBytes, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
@@ -129,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&tempty[buf], (use[buf] - 1) & 1);
           ptx::tc_fence_after();
         }
-        const uint32_t d_tmem = tmem + buf * (LA_TPC * 128);
+        const uint32_t d_tmem = tmem + buf * (LA_TPC * 128);   // TMEM sized for LA_TPC
         for (; u < seg_end; ++u, ++it) {
           const int s = (int)(it % kStages);
           ptx::mbar_wait(&full[s], (uint32_t)(it / kStages) & 1);
@@ -140,8 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_arrive(&empty[s]);
             continue;
           }
-#pragma unroll
-          for (int tt = 0; tt < LA_TPC; ++tt)
+          for (int tt = 0; tt < tpc; ++tt)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kTileBytes + kk * 32),
@@ -156,32 +268,77 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (args.trace) args.trace[blockIdx.x * 4 + 2] = globaltimer();
     }
   } else {
-    // ---------------------------------- drain TMEM -> fp32 partial tiles
+    // ------------------------------------------- drain TMEM / epilogue
+    const int et = threadIdx.x - 64;              // 0..127
     const int row_base = 32 * (warp & 3);
     const int f = row_base + lane;                // accumulator lane = feature in tile
     int use[2] = {0, 0}, buf = 0;
     long u = u_begin;
     while (u < u_end) {
-      const int tile = (int)(u / kb);
+      const int tile = (int)(u / kb);             // unit tile
       const long seg_end = std::min(u_end, (long)(tile + 1) * kb);
-      const int seg = (int)(blockIdx.x - la_cta_of((long)tile * kb, U, Pn));
+      const long c_first = la_cta_of((long)tile * kb, U, Pn);
+      const int seg = (int)(blockIdx.x - c_first);
       ptx::mbar_wait(&tfull[buf], use[buf] & 1);
       ptx::tc_fence_after();
-      for (int tt = 0; tt < LA_TPC; ++tt) {
-        const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
-        const int ftile = tile * LA_TPC + tt;
-        float* wsp = args.ws + ((size_t)ftile * args.max_segs + seg) * 128 * 128 + f;
-        for (int c0 = 0; c0 < n_pad; c0 += 32) {
-          float v[32];
-          ptx::tmem_ld32(t_base + c0, v);
-          const int nj = min(32, n_rows - c0);
+      if (EPI == LA_EPI_PARTIAL || seg != 0) {
+        // write this piece's fp32 partial
+        for (int tt = 0; tt < tpc; ++tt) {
+          const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
+          const int ftile = tile * tpc + tt;
+          float* wsp = args.ws + ((size_t)ftile * args.max_segs + seg) * 128 * 128 + f;
+          for (int c0 = 0; c0 < n_pad; c0 += 32) {
+            float v[32];
+            ptx::tmem_ld32(t_base + c0, v);
+            const int nj = min(32, n_rows - c0);
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
+          }
         }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[buf]);
+        if (EPI != LA_EPI_PARTIAL) {
+          __threadfence();
+          ptx::named_bar_sync(1, 128);
+          if (et == 0) atomicAdd(args.counters + tile, 1);
+        }
+      } else if constexpr (EPI != LA_EPI_PARTIAL) {
+        // owner of the tile's k = 0 piece: wait for the other pieces, sum them
+        // in piece order onto the accumulator, apply the fused epilogue
+        const int nseg = (int)(la_cta_of((long)(tile + 1) * kb - 1, U, Pn) - c_first + 1);
+        if (nseg > 1) {
+          if (et == 0) {
+            while (atomicAdd(args.counters + tile, 0) < nseg - 1) __nanosleep(64);
+            args.counters[tile] = 0;
+          }
+          ptx::named_bar_sync(1, 128);
+          __threadfence();
+        }
+        for (int tt = 0; tt < tpc; ++tt) {
+          const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
+          const int ftile = tile * tpc + tt;
+          const float* wsp = args.ws + (size_t)ftile * args.max_segs * 128 * 128 + f;
+          for (int c0 = 0; c0 < n_pad; c0 += 32) {
+            float v[32];
+            ptx::tmem_ld32(t_base + c0, v);
+            const int nj = min(32, n_rows - c0);
+            for (int sg = 1; sg < nseg; ++sg) {
+              const float* pp = wsp + ((size_t)sg * 128 + c0) * 128;
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj)
+                if (jj < nj) v[jj] += __ldcg(pp + (size_t)jj * 128);
+            }
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) sEpi[f * kEpiLd + jj] = v[jj];
+            ptx::named_bar_sync(1, 128);
+            epi_apply<EPI>(args, P, ftile, c0, n_rows, sEpi, et);
+            ptx::named_bar_sync(1, 128);
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[buf]);
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[buf]);
       use[buf]++;
       buf ^= 1;
       u = seg_end;
@@ -251,26 +408,37 @@ int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_ro
   return LA_OK;
 }
 
-int la_gemm_workspace_segs(int n_tiles, int kb, int grid) {
+int la_gemm_workspace_segs(int n_tiles, int kb, int grid, int tpc) {
   long mx = 1;
   for (int t = 0; t < n_tiles; ++t) {
     long c0;
     int n;
-    la_tile_segs(t, kb, n_tiles, grid, c0, n);
+    la_tile_segs(t, kb, n_tiles, grid, c0, n, tpc);
     mx = std::max<long>(mx, n);
   }
   return (int)mx;
 }
 
-int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {
+template <int EPI>
+static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(la_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kSmemBytes);
-    if (e != cudaSuccess) { la_set_error("gemm smem attr: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }
+    cudaError_t e = cudaFuncSetAttribute(la_gemm_kernel<EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
-  cudaError_t e = la_launch(la_gemm_kernel, dim3(g.grid), dim3(kThreads), kSmemBytes, st, pdl, g.args);
+  return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), kSmemBytes, st, pdl, g.args);
+}
+
+int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {
+  cudaError_t e;
+  switch (g.epi) {
+    case LA_EPI_QKV: e = launch_epi<LA_EPI_QKV>(g, st, pdl); break;
+    case LA_EPI_SWIGLU: e = launch_epi<LA_EPI_SWIGLU>(g, st, pdl); break;
+    case LA_EPI_LOGITS: e = launch_epi<LA_EPI_LOGITS>(g, st, pdl); break;
+    default: e = launch_epi<LA_EPI_PARTIAL>(g, st, pdl); break;
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { la_set_error("gemm launch: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }
   return LA_OK;

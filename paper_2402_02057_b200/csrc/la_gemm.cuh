@@ -36,6 +36,7 @@ struct LaGemmArgs {
   const __nv_bfloat16* a;   // packed weight tiles [n_tiles/2][kb][2][128*64]
   const __nv_bfloat16* b;   // packed step rows [kb][128][64]
   int n_tiles;              // 128-row feature tiles (even)
+  int tpc;                  // tiles per stream-K unit (1 or LA_TPC)
   int kb;                   // K / 64
   int max_segs;             // workspace segments per tile
   const FwdPlan* plan;
@@ -46,27 +47,42 @@ struct LaGemmArgs {
   // optional per-CTA trace [gridDim][4]: start, prologue done, MMA done, end
   unsigned long long* trace;
   int debug;   // experiments: bit0 skip step-row loads, bit1 skip MMAs
+  // ---- fused epilogue (LA_EPI_QKV / SWIGLU / LOGITS): stream-K fix-up in
+  // the GEMM -- the CTA owning a tile's k = 0 piece adds the other pieces'
+  // partials (in piece order) and applies the epilogue
+  int* counters;                     // [unit tiles] pieces arrived (reset by the owner)
+  __nv_bfloat16* q_out;              // QKV: [128][H][128]
+  __nv_bfloat16 *kc, *vc;            // QKV: layer base [slots][KVH][128]
+  const float *rope_cos, *rope_sin;  // QKV: [slots][64]
+  int H, KVH;
+  __nv_bfloat16* act;                // SWIGLU: packed LA rows
+  unsigned long long* keys;          // LOGITS: [128] (value, -index) atomicMax keys
+  float* logits;                     // LOGITS: [128][V] dump or null
+  int V;
 };
+
+enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_LOGITS = 3 };
 
 struct LaGemm {
   LaGemmArgs args;
   int grid;
+  int epi;    // LaGemmEpi
 };
 
 int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_rows);
 int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl = false);
-int la_gemm_workspace_segs(int n_tiles, int kb, int grid);
+int la_gemm_workspace_segs(int n_tiles, int kb, int grid, int tpc);
 int la_sm_count();
 size_t la_packed_elems(int rows, int K);   // bf16 elements of a packed matrix
 
 __host__ __device__ __forceinline__ long la_cta_of(long u, long U, long P) {
   return ((u + 1) * P + U - 1) / U - 1;
 }
-// contributing CTAs [c0, c0 + n) of feature tile t (n_tiles tiles, LA_TPC per unit)
+// contributing CTAs [c0, c0 + n) of feature tile t (n_tiles tiles, tpc per unit)
 __host__ __device__ __forceinline__ void la_tile_segs(int t, int kb, int n_tiles, long P, long& c0,
-                                                      int& n) {
-  const long U = (long)(n_tiles / LA_TPC) * kb;
-  const long pair = t / LA_TPC;
+                                                      int& n, int tpc = LA_TPC) {
+  const long U = (long)(n_tiles / tpc) * kb;
+  const long pair = t / tpc;
   c0 = la_cta_of(pair * kb, U, P);
   long c1 = la_cta_of((pair + 1) * kb - 1, U, P);
   n = (int)(c1 - c0 + 1);

@@ -44,7 +44,7 @@ __device__ __forceinline__ float4 seg_sum4(const float* ws, int t, int max_segs,
 __device__ __forceinline__ int tile_nseg(const LaSplit& sp, int t) {
   long c0;
   int n;
-  la_tile_segs(t, sp.kb, sp.n_tiles, sp.grid, c0, n);
+  la_tile_segs(t, sp.kb, sp.n_tiles, sp.grid, c0, n, sp.tpc);
   return n;
 }
 
@@ -76,7 +76,7 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
 
 // grid = (H + 2*KVH tiles, rows/8), block = 128: thread = (token, 4 rotary pairs)
 __global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
-  LA_PDL_ENTRY();
+  LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
   const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
   if (tok >= P->n_rows) return;
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
 // grid = rows, block = 512: x (+)= sum of segment partials (or := embedding
 // row), then RMSNorm -> bf16 GEMM input (packed LA rows)
 __global__ void __launch_bounds__(512) la_resid_norm_kernel(LaResidNorm e) {
-  LA_PDL_ENTRY();
+  LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
   const int r = blockIdx.x;
   if (r >= P->n_rows) return;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(512) la_resid_norm_kernel(LaResidNorm e) {
 
 // grid = (ffn/64 tiles, rows/8), block = 128: thread = (token, 4 outputs)
 __global__ void __launch_bounds__(128) la_swiglu_epi_kernel(LaSwigluEpi e) {
-  LA_PDL_ENTRY();
+  LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
   const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
   if (tok >= P->n_rows) return;

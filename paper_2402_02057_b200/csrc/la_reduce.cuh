@@ -6,10 +6,11 @@
 
 // stream-K geometry of the producing GEMM
 struct LaSplit {
-  int n_tiles, kb, grid, max_segs;
+  int n_tiles, kb, grid, max_segs, tpc;
 };
 
 struct LaQkvEpi {
+  LaPrefetch pf;                 // next GEMM's weights -> L2 (optional)
   const FwdPlan* plan;
   const float* ws;
   LaSplit sp;
@@ -20,6 +21,7 @@ struct LaQkvEpi {
 };
 
 struct LaResidNorm {
+  LaPrefetch pf;                 // next GEMM's weights -> L2 (optional)
   const FwdPlan* plan;
   const float* ws;               // null: no partials to add
   LaSplit sp;
@@ -32,6 +34,7 @@ struct LaResidNorm {
 };
 
 struct LaSwigluEpi {
+  LaPrefetch pf;                 // next GEMM's weights -> L2 (optional)
   const FwdPlan* plan;
   const float* ws;
   LaSplit sp;
