@@ -58,6 +58,7 @@ struct LlamaPath {
   bool fused = false;                     // GEMM-fused epilogues (LA_FUSED_EPI=1)
   int attn_rows = 64;                     // query rows per attention CTA (LA_ATTN_ROWS)
   int attn_min_chunk = 128;               // LA_ATTN_MIN_CHUNK
+  int skip = 0;                           // LA_SKIP: debug mask of per-layer launches to omit (timing only)
   cudaStream_t cap = nullptr;
   cudaGraphExec_t loop_exec = nullptr;   // while(!done) { step }
   cudaGraphExec_t fwd_exec = nullptr;    // K1 + forward + owned argmax (LP)
@@ -241,6 +242,7 @@ int llama_create(la_engine* e) {
   fin(p->head, 3);
   CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
   p->pdl = !(getenv("LA_PDL") && !strcmp(getenv("LA_PDL"), "0"));
+  p->skip = getenv("LA_SKIP") ? atoi(getenv("LA_SKIP")) : 0;
   cudaError_t ce = cudaFuncSetAttribute(la_attn_chunks_kernel<128>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)la_attn_prefix_smem(128));
   if (ce == cudaSuccess)
@@ -381,7 +383,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
   for (int l = 0; l < p->L; ++l) {
     {
       KT_BEGIN(st);
-      RET_IF(la_gemm_launch(p->qkv[l], st, p->pdl));
+      if (!(p->skip & 64)) RET_IF(la_gemm_launch(p->qkv[l], st, p->pdl));
       KT_END(st, "gemm_qkv");
     }
     if (!p->fused) {
@@ -389,37 +391,37 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
                  split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride, p->rope_cos,
                  p->rope_sin, p->H, p->KVH};
       KT_BEGIN(st);
-      CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
+      if (!(p->skip & 1)) CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
       KT_END(st, "qkv_epi");
       ++n;
     }
-    RET_IF(launch_attn(e, l, st));
+      if (!(p->skip & 2)) RET_IF(launch_attn(e, l, st));
     {
       KT_BEGIN(st);
-      RET_IF(la_gemm_launch(p->o[l], st, p->pdl));
+      if (!(p->skip & 128)) RET_IF(la_gemm_launch(p->o[l], st, p->pdl));
       KT_END(st, "gemm_o");
     }
-    RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st, &p->gu[l]));
+      if (!(p->skip & 8)) RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st, &p->gu[l]));
     {
       KT_BEGIN(st);
-      RET_IF(la_gemm_launch(p->gu[l], st, p->pdl));
+      if (!(p->skip & 256)) RET_IF(la_gemm_launch(p->gu[l], st, p->pdl));
       KT_END(st, "gemm_gu");
     }
     if (!p->fused) {
       LaSwigluEpi sw{prefetch_of(p->down[l], pf_frac(p->down[l], 40e6)), e->d_plan, p->ws,
                      split_of(p->gu[l]), p->act, p->ffn};
       KT_BEGIN(st);
-      CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, sw));
+      if (!(p->skip & 16)) CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, sw));
       KT_END(st, "swiglu_epi");
       ++n;
     }
     {
       KT_BEGIN(st);
-      RET_IF(la_gemm_launch(p->down[l], st, p->pdl));
+      if (!(p->skip & 512)) RET_IF(la_gemm_launch(p->down[l], st, p->pdl));
       KT_END(st, "gemm_down");
     }
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
-    RET_IF(resid_norm(e, &p->down[l], next, false, st, l + 1 < p->L ? &p->qkv[l + 1] : &p->head));
+      if (!(p->skip & 32)) RET_IF(resid_norm(e, &p->down[l], next, false, st, l + 1 < p->L ? &p->qkv[l + 1] : &p->head));
     CK(cudaGetLastError());
     n += 8;
   }
