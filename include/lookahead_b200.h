@@ -153,6 +153,10 @@ int32_t la_decode_lookahead_group(la_engine* const* engines, int32_t n, const la
  * 3 LM head. */
 int32_t la_gemm_timing_reset(la_engine* e);
 int32_t la_gemm_timing_read(la_engine* e, double* out16);
+/* Device time of the persistent forward kernel (bf16 path): out2 = {summed ns,
+ * launches} since la_gemm_timing_reset.  Profiling only; no reference
+ * counterpart (the reference has no device). */
+int32_t la_forward_timing_read(la_engine* e, double* out2);
 
 /* ------------------------------------------------------------ debugging */
 /* Copy an engine buffer to host (tests only): what = 0 argmax table

@@ -143,6 +143,17 @@ class LlamaOracle:
         ms = (x.astype(np.float64) ** 2).mean(axis=-1, keepdims=True)
         return (x / np.sqrt(ms + self.cfg["eps"]).astype(np.float32)) * g
 
+    def _norm_in(self, x, g):
+        """(GEMM input, row scale) of a normalised projection.  The device
+        applies RMSNorm deferred (la_mega.cuh): the projection consumes
+        bf16(x * g) and its fp32 accumulator is scaled by the row's
+        rsqrt(mean(x^2) + eps) -- mathematically rms(x) * g @ W^T."""
+        if not self.emul:
+            return self._rms(x, g), np.float32(1.0)
+        ms = (x.astype(np.float64) ** 2).mean(axis=-1, keepdims=True)
+        rstd = (1.0 / np.sqrt(ms + self.cfg["eps"])).astype(np.float32)
+        return bf16_round(x * g), rstd
+
     def _rope(self, x, pos):
         # x: (T, heads, hd); rotate-half convention
         hd = x.shape[-1]
@@ -156,11 +167,11 @@ class LlamaOracle:
         c = self.cfg
         w = self.w
         T = x.shape[0]
-        h = self._r(self._rms(x, w[f"{i}.attn_norm"]))
+        h, rs = self._norm_in(x, w[f"{i}.attn_norm"])
         # the device applies RoPE to the fp32 accumulator and stores bf16 once
-        q = (h @ w[f"{i}.wq"].T).reshape(T, c["heads"], c["head_dim"])
-        k = (h @ w[f"{i}.wk"].T).reshape(T, c["kv_heads"], c["head_dim"])
-        v = self._r(h @ w[f"{i}.wv"].T).reshape(T, c["kv_heads"], c["head_dim"])
+        q = ((h @ w[f"{i}.wq"].T) * rs).reshape(T, c["heads"], c["head_dim"])
+        k = ((h @ w[f"{i}.wk"].T) * rs).reshape(T, c["kv_heads"], c["head_dim"])
+        v = self._r((h @ w[f"{i}.wv"].T) * rs).reshape(T, c["kv_heads"], c["head_dim"])
         q = self._r(self._rope(q, pos))
         k = self._r(self._rope(k, pos))
         return q, k, v
@@ -189,9 +200,9 @@ class LlamaOracle:
         T0 = K.shape[0] - x.shape[0]
         o = self._r(self._attend(q, K, V, T0))
         x = x + o @ w[f"{i}.wo"].T
-        h = self._r(self._rms(x, w[f"{i}.mlp_norm"]))
-        g = h @ w[f"{i}.w_gate"].T
-        u = h @ w[f"{i}.w_up"].T
+        h, rs = self._norm_in(x, w[f"{i}.mlp_norm"])
+        g = (h @ w[f"{i}.w_gate"].T) * rs
+        u = (h @ w[f"{i}.w_up"].T) * rs
         a = self._r(g / (1.0 + np.exp(-g)) * u)
         x = x + a @ w[f"{i}.w_down"].T
         return x, K, V
@@ -210,8 +221,8 @@ class LlamaOracle:
 
     def final_logits(self, x_rows):
         w = self.w
-        h = self._r(self._rms(x_rows, w["final_norm"]))
-        return (h @ w["lm_head"].T).astype(np.float32)
+        h, rs = self._norm_in(x_rows, w["final_norm"])
+        return ((h @ w["lm_head"].T) * rs).astype(np.float32)
 
     def logits_rows(self, prefix, rows) -> list[np.ndarray]:
         prefix = [int(t) for t in prefix]

@@ -404,6 +404,10 @@ static int readback(la_engine* e, la_decode_io* io, cudaStream_t st) {
   CK(cudaMemcpyAsync(counters, e->p_counters, sizeof(counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (d.overflow) { la_set_error("device capacity exceeded (pool table, log or RNG stream)"); return LA_ERR_CAPACITY; }
+  if (!e->is_tiny() && llama_mega_error(e)) {
+    la_set_error("persistent forward kernel: dependency wait timed out (engine state is invalid)");
+    return LA_ERR_CUDA;
+  }
   io->n_out = d.n_out;
   io->n_steps = d.n_steps;
   io->pool_log_n = counters[1];
@@ -591,6 +595,7 @@ extern "C" int32_t la_decode_lookahead_group(la_engine* const* es, int32_t n,
 }
 
 int llama_read_trace(la_engine* e, void* host, size_t bytes);
+bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes);
 
 // ------------------------------------------------------------ debug copy
 extern "C" int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t bytes) {
@@ -607,7 +612,8 @@ extern "C" int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t
     case 3: src = e->d_dec; avail = sizeof(DevDecode); break;
     case 4: src = e->d_plan; avail = sizeof(FwdPlan); break;
     case 5: return llama_read_trace(e, host, (size_t)bytes);
-    default: la_set_error("unknown debug buffer %d", what); return LA_ERR_INVALID_CONFIG;
+    default:
+      if (what >= 6 && !e->is_tiny() && llama_debug_buffer(e, what, &src, &avail)) break; la_set_error("unknown debug buffer %d", what); return LA_ERR_INVALID_CONFIG;
   }
   CK(cudaMemcpy(host, src, std::min<size_t>(avail, (size_t)bytes), cudaMemcpyDeviceToHost));
   return LA_OK;

@@ -68,3 +68,4 @@ int llama_prefill(la_engine* e, const int* d_tokens, int n, cudaStream_t st);
 int llama_decode_loop(la_engine* e, cudaStream_t st, int* launches);
 int llama_forward_plan(la_engine* e, float* d_logits, cudaStream_t st);
 int llama_step_forward(la_engine* e, cudaStream_t st);   // K1 + forward + owned argmax
+int llama_mega_error(la_engine* e);                      // persistent-kernel dependency timeout flag

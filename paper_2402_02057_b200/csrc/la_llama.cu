@@ -18,6 +18,7 @@
 #include "la_attn.cuh"
 #include "la_engine.h"
 #include "la_gemm.cuh"
+#include "la_mega.cuh"
 #include "la_kernels.h"
 #include "la_reduce.cuh"
 
@@ -59,6 +60,8 @@ struct LlamaPath {
   int attn_rows = 64;                     // query rows per attention CTA (LA_ATTN_ROWS)
   int attn_min_chunk = 128;               // LA_ATTN_MIN_CHUNK
   int skip = 0;                           // LA_SKIP: debug mask of per-layer launches to omit (timing only)
+  bool mega = false;                      // persistent whole-forward kernel (LA_MEGA=1; experimental)
+  LaMegaArgs ma{};
   cudaStream_t cap = nullptr;
   cudaGraphExec_t loop_exec = nullptr;   // while(!done) { step }
   cudaGraphExec_t fwd_exec = nullptr;    // K1 + forward + owned argmax (LP)
@@ -137,6 +140,94 @@ static int lalloc(la_engine* e, T** p, size_t n) {
   CK(cudaMemset(q, 0, std::max<size_t>(n * sizeof(T), 16)));
   e->owned.push_back(q);
   *p = reinterpret_cast<T*>(q);
+  return LA_OK;
+}
+
+// ------------------------------------------------ persistent forward kernel
+static int mega_create(la_engine* e) {
+  LlamaPath* p = e->llama;
+  LaMegaArgs& a = p->ma;
+  memset(&a, 0, sizeof(a));
+  const int P = la_sm_count();
+  a.L = p->L; a.d = p->d; a.H = p->H; a.KVH = p->KVH; a.ffn = p->ffn; a.V = p->V;
+  a.slots = e->slots; a.eps = p->eps;
+  a.embed = p->embed; a.lm_head = p->lm_head; a.final_norm = p->final_norm;
+  // decomposition per projection: the step-row operand is cheap to re-read
+  // (L2), split-K partials are not, so one tile per unit everywhere; wide
+  // projections (gate/up, LM head: >= one tile per SM) give every CTA one
+  // whole tile (epilogue straight from TMEM) and split only the remainder
+  const bool use_dp = !(getenv("LA_MEGA_DP") && atoi(getenv("LA_MEGA_DP")) == 0);
+  auto geo = [&](int real, int tpc, int K, bool dp) {
+    LaMegaGeo g;
+    g.real = real; g.tpc = tpc;
+    g.n_tiles = (real + tpc - 1) / tpc * tpc;
+    g.kb = K / 64;
+    g.dp = (dp && tpc == 1 && real >= P) ? P : 0;
+    g.max_segs = g.n_tiles > g.dp ? la_gemm_workspace_segs(g.n_tiles - g.dp, g.kb, P, tpc) : 1;
+    return g;
+  };
+  a.geo[LA_MK_QKV] = geo(p->H + 2 * p->KVH, 1, p->d, false);
+  a.geo[LA_MK_O] = geo(p->d / 128, 1, p->H * 128, false);
+  a.geo[LA_MK_GU] = geo(p->ffn / 64, 1, p->d, use_dp);
+  a.geo[LA_MK_DOWN] = geo(p->d / 128, 1, p->ffn, false);
+  a.geo[LA_MK_HEAD] = geo(p->head_tiles, 1, p->d, use_dp);
+  for (int k = 0; k < 5; ++k)
+    RET_IF(lalloc(e, &a.ws[k], (size_t)a.geo[k].n_tiles * a.geo[k].max_segs * 128 * 128));
+  a.x = p->x; a.h_attn = p->h; a.attn_out = p->attn; a.act = p->act; a.q = p->q;
+  RET_IF(lalloc(e, &a.h_mlp, (size_t)LA_MAX_ROWS * p->d));
+  RET_IF(lalloc(e, &a.ss_attn, (size_t)p->d));
+  RET_IF(lalloc(e, &a.ss_mlp, (size_t)p->d));
+  a.kc = reinterpret_cast<__nv_bfloat16*>(e->kc);
+  a.vc = reinterpret_cast<__nv_bfloat16*>(e->vc);
+  a.rope_cos = p->rope_cos; a.rope_sin = p->rope_sin;
+  // attention units: (KV head, 128-query-row block, key chunk); the prefix
+  // split count depends on the model only (LP shards chunk identically)
+  const int g = p->H / p->KVH;
+  a.nrb_max = (LA_MAX_ROWS * g + 127) / 128;
+  int units = std::max(2, std::min(9, P / (p->KVH * a.nrb_max)));
+  if (getenv("LA_MEGA_SPLITS")) units = std::max(2, std::min(16, atoi(getenv("LA_MEGA_SPLITS")) + 1));
+  a.attn_S = units - 1;
+  const size_t n_units = (size_t)p->KVH * a.nrb_max * units;
+  RET_IF(lalloc(e, &a.attn_ws, n_units * 128 * 128));
+  RET_IF(lalloc(e, &a.attn_ml, n_units * 128));
+  a.keys = p->keys; a.row_amax = p->row_amax;
+  // sync area
+  LaMegaSyncMap& m = a.sm;
+  int off = 0;
+  for (int k = 0; k < 4; ++k) { m.cnt[k] = off; off += a.geo[k].n_tiles; }
+  m.rdy_qkv = off; off += a.geo[LA_MK_QKV].n_tiles;
+  m.attn_cnt = off; off += p->KVH * a.nrb_max;
+  m.rdy_attn = off; off += p->KVH;
+  m.rdy_m = off; off += p->d / 128;
+  m.rdy_act = off; off += a.geo[LA_MK_GU].n_tiles;
+  m.rdy_h = off; off += p->d / 128;
+  m.layer_stride = (off + 31) & ~31;
+  off = m.layer_stride * p->L;
+  m.h0 = off; off += p->d / 128;
+  m.head_cnt = off; off += a.geo[LA_MK_HEAD].n_tiles;
+  m.head_done = off++;
+  m.head_gen = off++;
+  m.cta_done = off++;
+  m.gen = off++;
+  m.err = off++;
+  m.total = off;
+  RET_IF(lalloc(e, &a.sync, (size_t)m.total));
+  CK(cudaMemset(a.sync, 0, (size_t)m.total * sizeof(unsigned)));
+  std::vector<LaMegaLayer> lw(p->L);
+  for (int l = 0; l < p->L; ++l)
+    lw[l] = LaMegaLayer{p->lw[l].wqkv, p->lw[l].wo, p->lw[l].wgu, p->lw[l].wd, p->lw[l].attn_norm,
+                        p->lw[l].mlp_norm};
+  LaMegaLayer* dl = nullptr;
+  RET_IF(lalloc(e, &dl, (size_t)p->L));
+  CK(cudaMemcpy(dl, lw.data(), lw.size() * sizeof(LaMegaLayer), cudaMemcpyHostToDevice));
+  a.layers = dl;
+  a.timing = p->timing + 32;
+  a.debug = getenv("LA_MEGA_DEBUG") ? atoi(getenv("LA_MEGA_DEBUG")) : 0;
+  a.pf_units = getenv("LA_MEGA_PF") ? std::max(0, atoi(getenv("LA_MEGA_PF"))) : 8;
+  if (getenv("LA_MEGA_TRACE")) {
+    a.trace_slots = 4 * p->L + 1 + p->L;
+    RET_IF(lalloc(e, &a.trace, (size_t)P * a.trace_slots * 8));
+  }
   return LA_OK;
 }
 
@@ -229,7 +320,7 @@ int llama_create(la_engine* e) {
   int* counters = nullptr;
   RET_IF(lalloc(e, &counters, 4096));
   RET_IF(lalloc(e, &p->ws, ws_need));
-  RET_IF(lalloc(e, &p->timing, 32));
+  RET_IF(lalloc(e, &p->timing, 48));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
   if (trace) RET_IF(lalloc(e, &p->trace, 4 * 256 * 4));
   const int dbg = getenv("LA_GEMM_DEBUG") ? atoi(getenv("LA_GEMM_DEBUG")) : 0;
@@ -249,6 +340,8 @@ int llama_create(la_engine* e) {
     ce = cudaFuncSetAttribute(la_attn_chunks_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)la_attn_prefix_smem(64));
   if (ce != cudaSuccess) { la_set_error("attn smem attr: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
+  p->mega = getenv("LA_MEGA") && atoi(getenv("LA_MEGA")) == 1;
+  if (p->mega) RET_IF(mega_create(e));
   return LA_OK;
 }
 
@@ -451,13 +544,29 @@ static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
   return LA_OK;
 }
 
+// the whole forward (+ LM head / argmax) as ONE persistent launch
+static int mega_forward(la_engine* e, cudaStream_t st, bool head, bool scatter, int* nk) {
+  LlamaPath* p = e->llama;
+  LaMegaArgs a = p->ma;
+  a.plan = e->d_plan;
+  a.dec = scatter ? e->d_dec : nullptr;
+  a.do_head = head ? 1 : 0;
+  a.logits = p->logits;
+  KT_BEGIN(st);
+  CK(la_mega_launch(a, la_sm_count(), st, p->pdl));
+  KT_END(st, "mega_forward");
+  *nk += 1;
+  return LA_OK;
+}
+
 int llama_prefill(la_engine* e, const int* d_tokens, int n, cudaStream_t st) {
   for (int start = 0; start < n; start += LA_MAX_ROWS) {
     int R = std::min(LA_MAX_ROWS, n - start);
     la_plan_chain_kernel<<<1, 128, 0, st>>>(e->d_plan, d_tokens, start, R);
     CK(cudaGetLastError());
     int nk = 0;
-    RET_IF(forward_layers(e, st, &nk));
+    if (e->llama->mega) RET_IF(mega_forward(e, st, false, false, &nk));
+    else RET_IF(forward_layers(e, st, &nk));
   }
   return LA_OK;
 }
@@ -466,8 +575,13 @@ int llama_forward_plan(la_engine* e, float* d_logits, cudaStream_t st) {
   LlamaPath* p = e->llama;
   p->logits = d_logits;
   int nk = 0;
-  int rc = forward_layers(e, st, &nk);
-  if (rc == LA_OK) rc = forward_head(e, st, false, &nk);
+  int rc;
+  if (p->mega) {
+    rc = mega_forward(e, st, true, false, &nk);
+  } else {
+    rc = forward_layers(e, st, &nk);
+    if (rc == LA_OK) rc = forward_head(e, st, false, &nk);
+  }
   p->logits = nullptr;
   return rc;
 }
@@ -482,8 +596,12 @@ static int record_step(la_engine* e, cudaStream_t st, bool finish, int* nk) {
   }
   CK(cudaGetLastError());
   *nk += 1;
-  RET_IF(forward_layers(e, st, nk));
-  RET_IF(forward_head(e, st, true, nk));
+  if (p->mega) {
+    RET_IF(mega_forward(e, st, true, true, nk));
+  } else {
+    RET_IF(forward_layers(e, st, nk));
+    RET_IF(forward_head(e, st, true, nk));
+  }
   if (finish) {
     KT_BEGIN(st);
     CK(la_launch(la_step_finish_kernel, dim3(1), dim3(256), 0, st, p->pdl, e->d_dec));
@@ -581,6 +699,30 @@ int llama_step_forward(la_engine* e, cudaStream_t st) {
   return LA_OK;
 }
 
+// debug: internal buffers of the persistent forward kernel (la_debug_read
+// what >= 6): 6 sync counters, 7 x, 8 h_attn, 9 ss_attn, 10 q, 11 attn_out,
+// 12 h_mlp, 13 ss_mlp, 14 act, 15 row_amax
+bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes) {
+  LlamaPath* p = e->llama;
+  if (!p) return false;
+  const LaMegaArgs& a = p->ma;
+  const size_t R = LA_MAX_ROWS;
+  switch (what) {
+    case 6: *src = a.sync; *bytes = (size_t)a.sm.total * 4; return a.sync != nullptr;
+    case 7: *src = p->x; *bytes = R * p->d * 4; return true;
+    case 8: *src = p->h; *bytes = R * p->d * 2; return true;
+    case 9: *src = a.ss_attn; *bytes = (size_t)p->d * 4; return a.ss_attn != nullptr;
+    case 10: *src = p->q; *bytes = R * p->H * 128 * 2; return true;
+    case 11: *src = p->attn; *bytes = R * p->H * 128 * 2; return true;
+    case 12: *src = a.h_mlp; *bytes = R * p->d * 2; return a.h_mlp != nullptr;
+    case 13: *src = a.ss_mlp; *bytes = (size_t)p->d * 4; return a.ss_mlp != nullptr;
+    case 14: *src = p->act; *bytes = R * p->ffn * 2; return true;
+    case 15: *src = p->row_amax; *bytes = R * 4; return true;
+    case 16: *src = a.trace; *bytes = (size_t)la_sm_count() * a.trace_slots * 64; return a.trace != nullptr;
+    default: return false;
+  }
+}
+
 // debug: per-CTA trace of the last launch of each GEMM kind (LA_GEMM_TRACE=1)
 int llama_read_trace(la_engine* e, void* host, size_t bytes) {
   if (!e->llama || !e->llama->trace) { la_set_error("trace disabled (set LA_GEMM_TRACE=1)"); return LA_ERR_INVALID_CONFIG; }
@@ -592,8 +734,29 @@ int llama_read_trace(la_engine* e, void* host, size_t bytes) {
 extern "C" int32_t la_gemm_timing_reset(la_engine* e) {
   if (!e || !e->llama) { la_set_error("no bf16 path on this engine"); return LA_ERR_INVALID_CONFIG; }
   CK(cudaSetDevice(e->device));
-  CK(cudaMemset(e->llama->timing, 0, 32 * sizeof(unsigned long long)));
+  CK(cudaMemset(e->llama->timing, 0, 48 * sizeof(unsigned long long)));
   return LA_OK;
+}
+
+// device time of the persistent forward kernel: [summed ns, launches] since
+// the last la_gemm_timing_reset; 0 launches when the multi-kernel path ran
+extern "C" int32_t la_forward_timing_read(la_engine* e, double* out2) {
+  if (!e || !e->llama || !out2) { la_set_error("no bf16 path on this engine"); return LA_ERR_INVALID_CONFIG; }
+  CK(cudaSetDevice(e->device));
+  unsigned long long t[8];
+  CK(cudaMemcpy(t, e->llama->timing + 32, sizeof(t), cudaMemcpyDeviceToHost));
+  out2[0] = (double)t[1];
+  out2[1] = (double)t[2];
+  return LA_OK;
+}
+
+// spin-timeout flag of the persistent kernel (a dependency never satisfied)
+int llama_mega_error(la_engine* e) {
+  LlamaPath* p = e->llama;
+  if (!p || !p->mega) return 0;
+  unsigned v = 0;
+  if (cudaMemcpy(&v, p->ma.sync + p->ma.sm.err, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return (int)v;
 }
 
 extern "C" int32_t la_gemm_timing_read(la_engine* e, double* out16) {
