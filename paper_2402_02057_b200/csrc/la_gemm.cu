@@ -329,8 +329,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int jj = 0; jj < 32; ++jj)
                 if (jj < nj) v[jj] += __ldcg(pp + (size_t)jj * 128);
             }
+            // deferred RMSNorm of the projection input: scale token columns
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) sEpi[f * kEpiLd + jj] = v[jj];
+            for (int jj = 0; jj < 32; ++jj)
+              sEpi[f * kEpiLd + jj] = jj < nj ? v[jj] * __ldg(args.rstd + c0 + jj) : 0.f;
             ptx::named_bar_sync(1, 128);
             epi_apply<EPI>(args, P, ftile, c0, n_rows, sEpi, et);
             ptx::named_bar_sync(1, 128);

@@ -41,6 +41,7 @@ struct LlamaPath {
   const float* final_norm = nullptr;
   std::vector<LlamaLayerW> lw;
   float* x = nullptr;
+  float* rstd = nullptr;                  // [128] deferred RMSNorm row scale
   __nv_bfloat16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
   float* ws = nullptr;
   unsigned long long* keys = nullptr;     // [128] argmax keys
@@ -248,6 +249,7 @@ int llama_create(la_engine* e) {
   }
   const int R = LA_MAX_ROWS, qd = D.heads * 128;
   RET_IF(lalloc(e, &p->x, (size_t)R * D.dim));
+  RET_IF(lalloc(e, &p->rstd, (size_t)R));
   RET_IF(lalloc(e, &p->h, (size_t)R * D.dim));
   RET_IF(lalloc(e, &p->q, (size_t)R * qd));
   RET_IF(lalloc(e, &p->attn, (size_t)R * qd));
@@ -330,6 +332,8 @@ int llama_create(la_engine* e) {
     gg.args.trace = trace ? p->trace + 256 * 4 * kind : nullptr;
   };
   for (int l = 0; l < D.layers; ++l) { fin(p->qkv[l], 0); fin(p->o[l], 1); fin(p->gu[l], 2); fin(p->down[l], 1); }
+  for (int l = 0; l < D.layers; ++l) { p->qkv[l].args.rstd = p->rstd; p->gu[l].args.rstd = p->rstd; }
+  p->head.args.rstd = p->rstd;
   fin(p->head, 3);
   CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
   p->pdl = !(getenv("LA_PDL") && !strcmp(getenv("LA_PDL"), "0"));
@@ -457,7 +461,7 @@ static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool emb
   r.ws = from ? p->ws : nullptr;
   r.sp = from ? split_of(*from) : LaSplit{2, 1, 1, 1, 1};
   r.embed = embed ? p->embed : nullptr;
-  r.x = p->x; r.g = g; r.h = p->h; r.d = p->d; r.eps = p->eps;
+  r.x = p->x; r.g = g; r.h = p->h; r.d = p->d; r.eps = p->eps; r.rstd = p->rstd;
   KT_BEGIN(st);
   CK(la_launch(la_resid_norm_kernel, dim3(LA_MAX_ROWS), dim3(512), 0, st, p->pdl, r));
   KT_END(st, from ? "resid_norm" : "embed_norm");
@@ -482,7 +486,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
     if (!p->fused) {
       LaQkvEpi q{prefetch_of(p->o[l], pf_frac(p->o[l], 20e6)), e->d_plan, p->ws,
                  split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride, p->rope_cos,
-                 p->rope_sin, p->H, p->KVH};
+                 p->rope_sin, p->H, p->KVH, p->rstd};
       KT_BEGIN(st);
       if (!(p->skip & 1)) CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
       KT_END(st, "qkv_epi");
@@ -502,7 +506,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
     }
     if (!p->fused) {
       LaSwigluEpi sw{prefetch_of(p->down[l], pf_frac(p->down[l], 40e6)), e->d_plan, p->ws,
-                     split_of(p->gu[l]), p->act, p->ffn};
+                     split_of(p->gu[l]), p->act, p->ffn, p->rstd};
       KT_BEGIN(st);
       if (!(p->skip & 16)) CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, sw));
       KT_END(st, "swiglu_epi");
@@ -532,7 +536,7 @@ static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
   }
   KT_BEGIN(st);
   if (!p->fused) {
-    LaLogitsEpi lg{e->d_plan, p->ws, split_of(p->head), p->keys, p->logits, p->V};
+    LaLogitsEpi lg{e->d_plan, p->ws, split_of(p->head), p->keys, p->logits, p->V, p->rstd};
     CK(la_launch(la_logits_epi_kernel, dim3(p->head_tiles, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, lg));
     *nk += 1;
   }

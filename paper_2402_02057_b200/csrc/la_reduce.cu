@@ -85,6 +85,9 @@ __global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
   const int i0 = (threadIdx.x & 15) * 4;
   float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
   float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
+  const float rs = e.rstd[tok];   // deferred RMSNorm of the projection input
+  a.x *= rs; a.y *= rs; a.z *= rs; a.w *= rs;
+  b.x *= rs; b.y *= rs; b.z *= rs; b.w *= rs;
   const bool v_tile = t >= e.H + e.KVH;
   __nv_bfloat16* dst;
   if (t < e.H) dst = e.q_out + ((size_t)tok * e.H + t) * 128;
@@ -133,12 +136,15 @@ __global__ void __launch_bounds__(512) la_resid_norm_kernel(LaResidNorm e) {
     *reinterpret_cast<float4*>(xr + f) = v;
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
+  // deferred RMSNorm: the next projection consumes bf16(x * g); its epilogue
+  // scales the accumulator by the row's rsqrt(mean(x^2) + eps)
   const float inv = rsqrtf(block_sum(ss, red) / e.d + e.eps);
+  if (threadIdx.x == 0) e.rstd[r] = inv;
   for (int f = threadIdx.x * 4; f < e.d; f += blockDim.x * 4) {
     const float4 v = *reinterpret_cast<const float4*>(xr + f);
     const float4 g = *reinterpret_cast<const float4*>(e.g + f);
     *reinterpret_cast<uint2*>(e.h + la_act_off(r, f)) =
-        make_uint2(pack2(v.x * inv * g.x, v.y * inv * g.y), pack2(v.z * inv * g.z, v.w * inv * g.w));
+        make_uint2(pack2(v.x * g.x, v.y * g.y), pack2(v.z * g.z, v.w * g.w));
   }
 }
 
@@ -151,8 +157,11 @@ __global__ void __launch_bounds__(128) la_swiglu_epi_kernel(LaSwigluEpi e) {
   const int t = blockIdx.x;
   const int nseg = tile_nseg(e.sp, t);
   const int i0 = (threadIdx.x & 15) * 4;
-  const float4 g = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
-  const float4 u = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
+  const float rs = e.rstd[tok];
+  float4 g = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
+  float4 u = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
+  g.x *= rs; g.y *= rs; g.z *= rs; g.w *= rs;
+  u.x *= rs; u.y *= rs; u.z *= rs; u.w *= rs;
   auto sw = [](float gg, float uu) { return gg / (1.0f + __expf(-gg)) * uu; };
   *reinterpret_cast<uint2*>(e.act + la_act_off(tok, t * 64 + i0)) =
       make_uint2(pack2(sw(g.x, u.x), sw(g.y, u.y)), pack2(sw(g.z, u.z), sw(g.w, u.w)));
@@ -174,7 +183,8 @@ __global__ void __launch_bounds__(128) la_logits_epi_kernel(LaLogitsEpi e) {
   if (valid) {
     const float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0);
     const float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0 + 4);
-    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const float rs = e.rstd[tok];
+    const float v[8] = {a.x * rs, a.y * rs, a.z * rs, a.w * rs, b.x * rs, b.y * rs, b.z * rs, b.w * rs};
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int fg = t * 128 + f0 + q;

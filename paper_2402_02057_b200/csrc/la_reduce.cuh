@@ -18,6 +18,7 @@ struct LaQkvEpi {
   __nv_bfloat16 *kc, *vc;        // layer base [slots][KVH][128]
   const float *rope_cos, *rope_sin;
   int H, KVH;
+  const float* rstd;             // [128] deferred RMSNorm row scale (la_resid_norm_kernel)
 };
 
 struct LaResidNorm {
@@ -28,9 +29,10 @@ struct LaResidNorm {
   const __nv_bfloat16* embed;    // non-null: x := embedding row (start of the step)
   float* x;                      // [128][d] fp32 residual stream
   const float* g;                // RMSNorm gain
-  __nv_bfloat16* h;              // packed LA rows (la_act_off)
+  __nv_bfloat16* h;              // packed LA rows (la_act_off): bf16(x * g)
   int d;
   float eps;
+  float* rstd;                   // [128] rsqrt(mean(x^2) + eps), applied by the consumer
 };
 
 struct LaSwigluEpi {
@@ -40,6 +42,7 @@ struct LaSwigluEpi {
   LaSplit sp;
   __nv_bfloat16* act;            // packed LA rows (la_act_off)
   int act_ld;
+  const float* rstd;
 };
 
 struct LaLogitsEpi {
@@ -49,6 +52,7 @@ struct LaLogitsEpi {
   unsigned long long* keys;      // [128] per-row (value, -index) atomicMax keys
   float* logits;                 // [128][V] or null
   int V;
+  const float* rstd;
 };
 
 __global__ void la_qkv_epi_kernel(LaQkvEpi e);

@@ -5,6 +5,8 @@ Tolerances (north_star): logits within 1e-2 relative for bf16; token
 divergence from the oracle is tolerated only where the oracle's top-2 logit
 margin is below that tolerance (documented near ties)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -38,10 +40,28 @@ def _make(name, max_context=1024):
     return m, LlamaOracle(cfg, w, emulate_bf16=True)
 
 
-@pytest.fixture(scope="module", params=list(CONFIGS))
+# forward implementations of the bf16 path, selected at engine creation:
+# default multi-kernel graph, GEMM-fused epilogues, persistent megakernel
+PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "mega": {"LA_MEGA": "1"}}
+
+
+@pytest.fixture(scope="module", params=[(c, p) for p in PATHS for c in CONFIGS],
+                ids=lambda cp: f"{cp[0]}-{cp[1]}")
 def pair(request):
-    m, o = _make(request.param)
-    yield request.param, m, o
+    name, path = request.param
+    saved = {k: os.environ.get(k) for k in ("LA_FUSED_EPI", "LA_MEGA")}
+    for k in saved:
+        os.environ.pop(k, None)
+    os.environ.update(PATHS[path])
+    try:
+        m, o = _make(name)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    yield name, m, o
     m.close()
 
 
