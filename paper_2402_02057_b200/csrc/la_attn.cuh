@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 
 #include "la_common.cuh"
+#include "la_reduce.cuh"
 
 struct LaAttnArgs {
   LaPrefetch pf;                 // next GEMM's weights -> L2 (optional)
@@ -21,3 +22,22 @@ template <int kQRows>
 __global__ void la_attn_chunks_kernel(LaAttnArgs a);
 __global__ void la_attn_merge_kernel(LaAttnArgs a);
 size_t la_attn_prefix_smem(int qrows);
+
+// Attention + chunk merge in one launch (la_attn_fused.cu)
+struct LaAttnFusedArgs {
+  LaPrefetch pf;                 // O-projection weights -> L2 while attention runs
+  const FwdPlan* plan;
+  const __nv_bfloat16* q;        // [LA_MAX_ROWS][H][128] (RoPE applied)
+  const __nv_bfloat16 *kc, *vc;  // layer base, [slots][KVH][128]
+  float* part_o;                 // [KVH][nrb_max][S+1][128][128] chunk partials
+  float2* part_ml;               // [KVH][nrb_max][S+1][128] (max, sum) in log2 units
+  unsigned* cnt;                 // [KVH][nrb_max] chunk arrivals (monotonic; +S+1 per launch)
+  __nv_bfloat16* out;            // packed LA rows (la_act_off), the O-projection input
+  int H, KVH, S, nrb_max;
+  float scale;
+  int spread_merge;              // grid <= SMs: every chunk CTA merges a share of the rows
+  unsigned long long* trace;     // optional [grid][8] globaltimer stamps (LA_ATTN_TRACE=1)
+};
+
+__global__ void la_attn_fused_kernel(LaAttnFusedArgs a);
+size_t la_attn_fused_smem();

@@ -1,0 +1,343 @@
+// Step attention of one decoder layer (reference models.py:250-260 with the
+// visibility sets of layout.py:139-170): flash attention + chunk merge in ONE
+// launch (q / K / V come from la_qkv_epi_kernel).
+//
+// Work unit = (KV head, block of 128 query rows, key chunk).  The confirmed
+// prefix (cache slots [0, ctx)) is cut into S chunks whose boundaries depend
+// on ctx only, so every lookahead-parallel shard -- and the plain greedy step
+// -- sums a row's keys in the same order; unit S is the step block (slots
+// ctx .. ctx+n_global) under the paper's structured mask, generated per row
+// from the plan's chains (a 128-bit visibility set, never an M x M matrix).
+//
+//  * one CTA of 8 warps covers 128 query rows (16 per warp, mma.sync bf16,
+//    fp32 online softmax) so each K/V tile is read from HBM once; all tiles
+//    of a chunk are issued up front into a 5-deep cp.async ring.
+//  * the last chunk of (KV head, row block) to finish merges the chunk
+//    partials in chunk order and writes the O-projection input (packed rows).
+#include <cuda_bf16.h>
+
+#include "la_attn.cuh"
+#include "la_common.cuh"
+#include "la_gemm.cuh"
+
+namespace {
+
+constexpr int kKeyTile = 64;
+constexpr int kStages = 5;                           // K/V tiles in flight
+constexpr int kTileBytes = 2 * kKeyTile * 256;       // K + V of 64 keys
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * 256 + ((chunk ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ int chunk_keys(int ctx, int S) {
+  return ((ctx + S - 1) / S + kKeyTile - 1) / kKeyTile * kKeyTile;
+}
+__device__ __forceinline__ void stamp(const LaAttnFusedArgs& a, int k) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[blockIdx.x * 8 + k] = t;
+  }
+}
+
+}  // namespace
+
+size_t la_attn_fused_smem() { return (size_t)kStages * kTileBytes + LA_MAX_ROWS * 4 * 4 + 16; }
+
+// grid = KVH * nrb_max * (S + 1) units, block = 256 (8 warps x 16 query rows)
+__global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a) {
+  stamp(a, 0);
+  LA_PDL_ENTRY_PF(a.pf);
+  stamp(a, 1);
+  const FwdPlan* P = a.plan;
+  const int n_rows = P->n_rows, ctx = P->n_prefix;
+  if (n_rows == 0) return;
+  const int g = a.H / a.KVH;
+  const int nq = n_rows * g;
+  const int n_rb = (nq + 127) >> 7;
+  const int S = a.S;
+  const int e = blockIdx.x;
+  const int kvh = e / (a.nrb_max * (S + 1));
+  const int rb = (e / (S + 1)) % a.nrb_max;
+  const int split = e % (S + 1);
+  if (rb >= n_rb) return;
+  const bool step_unit = split == S;
+  int k_begin, k_end;
+  if (step_unit) {
+    k_begin = ctx;
+    k_end = ctx + P->n_global;
+  } else {
+    const int CH = chunk_keys(ctx, S);
+    k_begin = min(ctx, split * CH);
+    k_end = min(ctx, (split + 1) * CH);
+  }
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* sKV = smem;                                                   // [kStages][K | V]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + kStages * kTileBytes);   // [128][4]
+  int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t kv_ld = (size_t)a.KVH * 128;
+  const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+
+  auto load_kv = [&](int t) {
+    uint8_t* kb = sKV + (t % kStages) * kTileBytes;
+    const int t0 = k_begin + t * kKeyTile;
+    for (int i = tid; i < kKeyTile * 16; i += 256) {
+      const int row = i >> 4, ch = i & 15, key = t0 + row;
+      const bool ok = key < k_end;
+      const size_t off = ((size_t)(ok ? key : k_begin) * kv_ld) + kvh * 128 + ch * 8;
+      cp_async16(smem_u32(kb) + swz(row, ch), a.kc + off, ok);
+      cp_async16(smem_u32(kb + kKeyTile * 256) + swz(row, ch), a.vc + off, ok);
+    }
+  };
+  // ---- q fragments straight from global (m16n8k16 A layout)
+  const int qrow0 = warp * 16 + (lane >> 2);
+  uint32_t qf[8][4];
+  {
+    const int qa = rb * 128 + qrow0, qb = qa + 8;
+    const __nv_bfloat16* pa = qa < nq ? a.q + ((size_t)(qa / g) * a.H + kvh * g + qa % g) * 128 : nullptr;
+    const __nv_bfloat16* pb = qb < nq ? a.q + ((size_t)(qb / g) * a.H + kvh * g + qb % g) * 128 : nullptr;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int col = kk * 16 + (lane & 3) * 2;
+      qf[kk][0] = pa ? __ldg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
+      qf[kk][1] = pb ? __ldg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
+      qf[kk][2] = pa ? __ldg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
+      qf[kk][3] = pb ? __ldg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
+    }
+  }
+
+  // issue the chunk's first kStages-1 K/V tiles (all of it for <= 4 tiles);
+  // the step block's keys are the rows' own K/V at slots ctx + global row
+#pragma unroll 1
+  for (int t = 0; t < kStages - 1; ++t) {
+    if (t < n_tiles) load_kv(t);
+    cp_commit();
+  }
+  if (step_unit) {
+    // structured mask: a query row sees its chain's step keys and itself
+    for (int i = tid; i < LA_MAX_ROWS * 4; i += 256) sMask[i] = 0u;
+    __syncthreads();
+    for (int row = warp; row < LA_MAX_ROWS; row += 8) {
+      const int qr = rb * 128 + row;
+      if (qr >= nq) continue;
+      const int r = qr / g;
+      const int n = P->chain_n[r];
+      for (int jj = lane; jj <= n; jj += 32) {
+        const int key = (jj < n ? P->chain[r][jj] : P->slot[r]) - ctx;
+        atomicOr(&sMask[row * 4 + (key >> 5)], 1u << (key & 31));
+      }
+    }
+  }
+
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float sl2 = a.scale * kLog2e;
+  stamp(a, 2);
+  const bool warp_active = rb * 128 + warp * 16 < nq;
+
+  for (int t = 0; t < n_tiles; ++t) {
+    if (t + kStages - 1 < n_tiles) load_kv(t + kStages - 1);
+    cp_commit();
+    cp_wait<kStages - 1>();
+    __syncthreads();
+    if (t == 0) stamp(a, 3);
+    if (warp_active) {
+      const uint8_t* sK = sKV + (t % kStages) * kTileBytes;
+      const uint8_t* sV = sK + kKeyTile * 256;
+      float s[8][4];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+        for (int np = 0; np < 4; ++np) {
+          const int key = np * 16 + (lane & 7) + (lane >> 4) * 8;
+          const int ch = kk * 2 + ((lane >> 3) & 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(smem_u32(sK) + swz(key, ch), b0, b1, b2, b3);
+          mma16816(s[2 * np], qf[kk], b0, b1);
+          mma16816(s[2 * np + 1], qf[kk], b2, b3);
+        }
+      }
+      const int kbase = k_begin + t * kKeyTile;
+      float mx0 = m0, mx1 = m1;
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const int key = kbase + n * 8 + (lane & 3) * 2 + (e2 & 1);
+          bool vis = key < k_end;
+          if (step_unit && vis) {
+            const int kg = key - ctx, row = qrow0 + (e2 >> 1) * 8;
+            vis = (sMask[row * 4 + (kg >> 5)] >> (kg & 31)) & 1u;
+          }
+          s[n][e2] = vis ? s[n][e2] * sl2 : -INFINITY;
+        }
+        mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
+        mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
+      }
+#pragma unroll
+      for (int off = 1; off <= 2; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
+      const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
+      m0 = mx0;
+      m1 = mx1;
+      float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        s[n][0] = exp2f(s[n][0] - b0);
+        s[n][1] = exp2f(s[n][1] - b0);
+        s[n][2] = exp2f(s[n][2] - b1);
+        s[n][3] = exp2f(s[n][3] - b1);
+        rs0 += s[n][0] + s[n][1];
+        rs1 += s[n][2] + s[n][3];
+      }
+      l0 = l0 * al0 + rs0;
+      l1 = l1 * al1 + rs1;
+#pragma unroll
+      for (int dd = 0; dd < 16; ++dd) {
+        o[dd][0] *= al0; o[dd][1] *= al0; o[dd][2] *= al1; o[dd][3] *= al1;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint32_t pa[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]), pack_bf16(s[2 * kk][2], s[2 * kk][3]),
+                          pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                          pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+        for (int dp = 0; dp < 8; ++dp) {
+          const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+          const int ch = dp * 2 + (lane >> 4);
+          uint32_t v0, v1, v2, v3;
+          ldsm_x4_t(smem_u32(sV) + swz(key, ch), v0, v1, v2, v3);
+          mma16816(o[2 * dp], pa, v0, v1);
+          mma16816(o[2 * dp + 1], pa, v2, v3);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  stamp(a, 4);
+
+  // ---- chunk partial: unnormalised O and (m, l) in log2 units
+#pragma unroll
+  for (int off = 1; off <= 2; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  const size_t grp = (size_t)kvh * a.nrb_max + rb;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int row = qrow0 + half * 8;
+    if (rb * 128 + row >= nq) continue;
+    float* dst = a.part_o + ((grp * (S + 1) + split) * 128 + row) * 128;
+#pragma unroll
+    for (int dd = 0; dd < 16; ++dd) {
+      const int col = dd * 8 + (lane & 3) * 2;
+      __stcg(reinterpret_cast<float2*>(dst + col), make_float2(o[dd][half * 2], o[dd][half * 2 + 1]));
+    }
+    if ((lane & 3) == 0)
+      __stcg(a.part_ml + (grp * (S + 1) + split) * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
+  }
+  __syncthreads();
+  // arrival of this chunk.  Counters only grow: an active group gains exactly
+  // S+1 per launch, so the group's target is the next multiple of S+1.
+  if (tid == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(a.cnt + grp, 1u);
+    const unsigned target = (old / (unsigned)(S + 1) + 1) * (unsigned)(S + 1);
+    if (a.spread_merge) {
+      // every chunk CTA of the group is resident (grid <= SMs, 1 CTA / SM):
+      // wait for the others, then merge this chunk's share of the rows
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.cnt + grp) : "memory");
+        if ((int)(v - target) < 0) __nanosleep(64);
+      } while ((int)(v - target) < 0);
+      *sFlag = 1;
+    } else {
+      *sFlag = old + 1 == target;   // the last chunk merges every row
+      if (*sFlag) __threadfence();
+    }
+  }
+  __syncthreads();
+  stamp(a, 5);
+  if (!*sFlag) return;
+
+  // ---- merge the S+1 chunk partials of this group in chunk order: rows
+  // [r0, r1) of the group, 8 threads per row x 16 dims
+  const int rows_per = a.spread_merge ? (128 + S) / (S + 1) : 128;
+  const int r0 = a.spread_merge ? split * rows_per : 0;
+  const int r1 = min(128, r0 + rows_per);
+  for (int row = r0 + (tid >> 3); row < r1; row += 32) {
+    const int qr = rb * 128 + row;
+    if (qr >= nq) break;
+    const int hd = (tid & 7) * 16;
+    float m = -INFINITY, ll = 0.f;
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    for (int sp = 0; sp <= S; ++sp) {
+      const size_t us = grp * (S + 1) + sp;
+      const float2 ml = __ldcg(a.part_ml + us * 128 + row);
+      const float4* po = reinterpret_cast<const float4*>(a.part_o + (us * 128 + row) * 128 + hd);
+      const float4 v0 = __ldcg(po), v1 = __ldcg(po + 1), v2 = __ldcg(po + 2), v3 = __ldcg(po + 3);
+      if (ml.x == -INFINITY) continue;
+      const float mn = fmaxf(m, ml.x);
+      const float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
+      const float vv[16] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w,
+                            v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = acc[i] * s0 + vv[i] * s1;
+      ll = ll * s0 + ml.y * s1;
+      m = mn;
+    }
+    const float inv = 1.0f / ll;
+    const int r = qr / g, head = kvh * g + qr % g;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      *reinterpret_cast<uint4*>(a.out + la_act_off(r, head * 128 + hd + 8 * c)) =
+          make_uint4(pack_bf16(acc[8 * c] * inv, acc[8 * c + 1] * inv),
+                     pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
+                     pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
+                     pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
+  }
+  stamp(a, 6);
+}

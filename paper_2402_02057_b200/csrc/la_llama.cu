@@ -60,6 +60,8 @@ struct LlamaPath {
   bool fused = false;                     // GEMM-fused epilogues (LA_FUSED_EPI=1)
   int attn_rows = 64;                     // query rows per attention CTA (LA_ATTN_ROWS)
   int attn_min_chunk = 128;               // LA_ATTN_MIN_CHUNK
+  bool attn_fused = true;                 // fused QKV fix-up + attention + merge (LA_ATTN_FUSED=0: 3 kernels)
+  LaAttnFusedArgs af{};                   // its static arguments
   int skip = 0;                           // LA_SKIP: debug mask of per-layer launches to omit (timing only)
   bool mega = false;                      // persistent whole-forward kernel (LA_MEGA=1; experimental)
   LaMegaArgs ma{};
@@ -344,6 +346,30 @@ int llama_create(la_engine* e) {
     ce = cudaFuncSetAttribute(la_attn_chunks_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)la_attn_prefix_smem(64));
   if (ce != cudaSuccess) { la_set_error("attn smem attr: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
+  // fused attention: (KV head, 128 query rows, key chunk) units, one CTA per
+  // SM at most; prefix chunk count depends on the model only
+  p->attn_fused = !(getenv("LA_ATTN_FUSED") && atoi(getenv("LA_ATTN_FUSED")) == 0);
+  {
+    LaAttnFusedArgs& af = p->af;
+    af.H = p->H; af.KVH = p->KVH;
+    af.nrb_max = (LA_MAX_ROWS * g + 127) / 128;
+    int units = std::max(2, std::min(9, la_sm_count() / (p->KVH * af.nrb_max)));
+    if (getenv("LA_ATTN_SPLITS")) units = std::max(2, std::min(16, atoi(getenv("LA_ATTN_SPLITS")) + 1));
+    af.S = units - 1;
+    // co-residency (1 CTA per SM, grid <= SMs) makes the spread merge's wait safe
+    af.spread_merge = (p->KVH * af.nrb_max * units <= la_sm_count()) && !getenv("LA_ATTN_LAST_MERGE");
+    af.scale = 1.0f / sqrtf(128.0f);
+    af.q = p->q;
+    af.out = p->attn;
+    const size_t groups = (size_t)p->KVH * af.nrb_max;
+    RET_IF(lalloc(e, &af.part_o, groups * units * 128 * 128));
+    RET_IF(lalloc(e, &af.part_ml, groups * units * 128));
+    RET_IF(lalloc(e, &af.cnt, groups));
+    if (getenv("LA_ATTN_TRACE")) RET_IF(lalloc(e, &af.trace, groups * units * 8));
+    ce = cudaFuncSetAttribute(la_attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)la_attn_fused_smem());
+    if (ce != cudaSuccess) { la_set_error("fused attn smem attr: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
+  }
   p->mega = getenv("LA_MEGA") && atoi(getenv("LA_MEGA")) == 1;
   if (p->mega) RET_IF(mega_create(e));
   return LA_OK;
@@ -452,6 +478,27 @@ static int launch_attn(la_engine* e, int l, cudaStream_t st) {
   return LA_OK;
 }
 
+static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
+  LlamaPath* p = e->llama;
+  LaAttnFusedArgs a = p->af;
+  a.plan = e->d_plan;
+  {
+    // the O projection cannot be co-resident with attention (smem): stream its
+    // first weights into L2 meanwhile (LA_ATTN_PF = fraction; measured no gain, off)
+    static const float frac = getenv("LA_ATTN_PF") ? (float)atof(getenv("LA_ATTN_PF")) : 0.0f;
+    const LaGemm& g = p->o[l];
+    a.pf = LaPrefetch{g.args.a, g.args.n_tiles, g.args.kb, g.args.tpc, g.grid, frac};
+  }
+  const size_t lstride = (size_t)e->slots * p->KVH * 128;
+  a.kc = reinterpret_cast<__nv_bfloat16*>(e->kc) + l * lstride;
+  a.vc = reinterpret_cast<__nv_bfloat16*>(e->vc) + l * lstride;
+  KT_BEGIN(st);
+  CK(la_launch(la_attn_fused_kernel, dim3(p->KVH * a.nrb_max * (a.S + 1)), dim3(256), la_attn_fused_smem(), st,
+               p->pdl, a));
+  KT_END(st, "attn_fused");
+  return LA_OK;
+}
+
 static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool embed, cudaStream_t st,
                       const LaGemm* next) {
   LlamaPath* p = e->llama;
@@ -492,7 +539,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       KT_END(st, "qkv_epi");
       ++n;
     }
-      if (!(p->skip & 2)) RET_IF(launch_attn(e, l, st));
+      if (!(p->skip & 2)) RET_IF(p->attn_fused ? launch_attn_fused(e, l, st) : launch_attn(e, l, st));
     {
       KT_BEGIN(st);
       if (!(p->skip & 128)) RET_IF(la_gemm_launch(p->o[l], st, p->pdl));
@@ -520,7 +567,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
       if (!(p->skip & 32)) RET_IF(resid_norm(e, &p->down[l], next, false, st, l + 1 < p->L ? &p->qkv[l + 1] : &p->head));
     CK(cudaGetLastError());
-    n += 8;
+    n += p->attn_fused ? 7 : 8;   // 4 GEMMs + 2 residual norms + attention (1 fused, or chunks + merge)
   }
   *nk += n;
   return LA_OK;
@@ -722,6 +769,7 @@ bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes)
     case 13: *src = a.ss_mlp; *bytes = (size_t)p->d * 4; return a.ss_mlp != nullptr;
     case 14: *src = p->act; *bytes = R * p->ffn * 2; return true;
     case 15: *src = p->row_amax; *bytes = R * 4; return true;
+    case 17: *src = p->af.trace; *bytes = (size_t)p->KVH * p->af.nrb_max * (p->af.S + 1) * 64; return p->af.trace != nullptr;
     case 16: *src = a.trace; *bytes = (size_t)la_sm_count() * a.trace_slots * 64; return a.trace != nullptr;
     default: return false;
   }
