@@ -286,7 +286,7 @@ int llama_create(la_engine* e) {
   __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc);
   __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc);
   p->qkv.resize(D.layers); p->o.resize(D.layers); p->gu.resize(D.layers); p->down.resize(D.layers);
-  const int narrow_tpc = getenv("LA_NARROW_TPC") ? atoi(getenv("LA_NARROW_TPC")) : 1;
+  const int narrow_tpc = getenv("LA_NARROW_TPC") ? atoi(getenv("LA_NARROW_TPC")) : LA_TPC;   // measured: 2 > 1
   // stream-K fix-up + epilogue inside the GEMM (LA_FUSED_EPI=1) or in the
   // separate reduce kernels spread over the GPU (default: measured faster)
   const bool fused = getenv("LA_FUSED_EPI") && atoi(getenv("LA_FUSED_EPI"));
@@ -326,17 +326,19 @@ int llama_create(la_engine* e) {
   RET_IF(lalloc(e, &p->ws, ws_need));
   RET_IF(lalloc(e, &p->timing, 48));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
-  if (trace) RET_IF(lalloc(e, &p->trace, 4 * 256 * 4));
+  if (trace) RET_IF(lalloc(e, &p->trace, 5 * 256 * 4));   // qkv, o, gu, head, down
   const int dbg = getenv("LA_GEMM_DEBUG") ? atoi(getenv("LA_GEMM_DEBUG")) : 0;
-  auto fin = [&](LaGemm& gg, int kind) {
+  auto fin = [&](LaGemm& gg, int kind, int tkind) {
     gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.debug = dbg; gg.args.counters = counters;
     gg.args.timing = p->timing + 8 * kind;
-    gg.args.trace = trace ? p->trace + 256 * 4 * kind : nullptr;
+    gg.args.trace = trace ? p->trace + 256 * 4 * tkind : nullptr;
   };
-  for (int l = 0; l < D.layers; ++l) { fin(p->qkv[l], 0); fin(p->o[l], 1); fin(p->gu[l], 2); fin(p->down[l], 1); }
+  for (int l = 0; l < D.layers; ++l) {
+    fin(p->qkv[l], 0, 0); fin(p->o[l], 1, 1); fin(p->gu[l], 2, 2); fin(p->down[l], 1, 4);
+  }
   for (int l = 0; l < D.layers; ++l) { p->qkv[l].args.rstd = p->rstd; p->gu[l].args.rstd = p->rstd; }
   p->head.args.rstd = p->rstd;
-  fin(p->head, 3);
+  fin(p->head, 3, 3);
   CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
   p->pdl = !(getenv("LA_PDL") && !strcmp(getenv("LA_PDL"), "0"));
   p->skip = getenv("LA_SKIP") ? atoi(getenv("LA_SKIP")) : 0;
@@ -778,7 +780,7 @@ bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes)
 // debug: per-CTA trace of the last launch of each GEMM kind (LA_GEMM_TRACE=1)
 int llama_read_trace(la_engine* e, void* host, size_t bytes) {
   if (!e->llama || !e->llama->trace) { la_set_error("trace disabled (set LA_GEMM_TRACE=1)"); return LA_ERR_INVALID_CONFIG; }
-  CK(cudaMemcpy(host, e->llama->trace, std::min<size_t>(bytes, 4 * 256 * 4 * 8), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(host, e->llama->trace, std::min<size_t>(bytes, 5 * 256 * 4 * 8), cudaMemcpyDeviceToHost));
   return LA_OK;
 }
 
