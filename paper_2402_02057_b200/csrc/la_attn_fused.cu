@@ -146,19 +146,25 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
     cp_commit();
   }
   if (step_unit) {
-    // structured mask: a query row sees its chain's step keys and itself
-    for (int i = tid; i < LA_MAX_ROWS * 4; i += 256) sMask[i] = 0u;
-    __syncthreads();
-    for (int row = warp; row < LA_MAX_ROWS; row += 8) {
-      const int qr = rb * 128 + row;
-      if (qr >= nq) continue;
-      const int r = qr / g;
-      const int n = P->chain_n[r];
-      for (int jj = lane; jj <= n; jj += 32) {
-        const int key = (jj < n ? P->chain[r][jj] : P->slot[r]) - ctx;
-        atomicOr(&sMask[row * 4 + (key >> 5)], 1u << (key & 31));
+    // structured mask: a query row sees its chain's step keys and itself;
+    // one thread per row builds its 128-bit set in registers (independent loads)
+    if (tid < LA_MAX_ROWS) {
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+      const int qr = rb * 128 + tid;
+      if (qr < nq) {
+        const int r = qr / g;
+        const int n = P->chain_n[r];
+        const int own = P->slot[r] - ctx;
+        w[own >> 5] |= 1u << (own & 31);
+        for (int jj = 0; jj < n; ++jj) {
+          const int key = P->chain[r][jj] - ctx;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w[q] |= (key >> 5) == q ? 1u << (key & 31) : 0u;
+        }
       }
+      *reinterpret_cast<uint4*>(sMask + tid * 4) = make_uint4(w[0], w[1], w[2], w[3]);
     }
+    __syncthreads();
   }
 
   float o[16][4];
@@ -193,18 +199,27 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
           mma16816(s[2 * np + 1], qf[kk], b2, b3);
         }
       }
+      // 64-key visibility of this thread's two rows: the key range, and for
+      // the step block the rows' structured-mask words; pre-shifted by the
+      // lane's column so the per-element bit index is a constant
       const int kbase = k_begin + t * kKeyTile;
+      const int nvalid = min(kKeyTile, k_end - kbase);
+      unsigned long long vm0 = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull), vm1 = vm0;
+      if (step_unit) {
+        const uint32_t* w0 = sMask + qrow0 * 4 + 2 * t;
+        const uint32_t* w1 = sMask + (qrow0 + 8) * 4 + 2 * t;
+        vm0 &= ((unsigned long long)w0[1] << 32) | w0[0];
+        vm1 &= ((unsigned long long)w1[1] << 32) | w1[0];
+      }
+      vm0 >>= (lane & 3) * 2;
+      vm1 >>= (lane & 3) * 2;
       float mx0 = m0, mx1 = m1;
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
 #pragma unroll
         for (int e2 = 0; e2 < 4; ++e2) {
-          const int key = kbase + n * 8 + (lane & 3) * 2 + (e2 & 1);
-          bool vis = key < k_end;
-          if (step_unit && vis) {
-            const int kg = key - ctx, row = qrow0 + (e2 >> 1) * 8;
-            vis = (sMask[row * 4 + (kg >> 5)] >> (kg & 31)) & 1u;
-          }
+          const unsigned long long vm = (e2 >> 1) ? vm1 : vm0;
+          const bool vis = (vm >> (n * 8 + (e2 & 1))) & 1ull;
           s[n][e2] = vis ? s[n][e2] * sl2 : -INFINITY;
         }
         mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));

@@ -64,6 +64,16 @@ struct FwdPlan {
   int chain[LA_MAX_ROWS][LA_MAX_CHAIN];
 };
 
+// Deferred RMSNorm statistics: per 128-feature tile partial sums of x^2 of
+// each row ([tiles][128]); a consumer scales its projection accumulator by
+// rsqrt(sum / d + eps) (the projection consumed bf16(x * g)).
+struct LaRowNorm {
+  const float* ss;
+  int tiles;       // d / 128
+  float inv_d;     // 1 / d
+  float eps;
+};
+
 // ----------------------------------------------------------- decode state
 enum { LA_MODE_LOOKAHEAD = 0, LA_MODE_AUTOREGRESSIVE = 1 };
 

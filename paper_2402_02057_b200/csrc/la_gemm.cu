@@ -19,7 +19,8 @@ void la_set_error(const char* fmt, ...);
 
 namespace {
 
-constexpr int kStages = 4;
+constexpr int kStages = 4;                     // stages of 2-tile units (48 KB each)
+constexpr int kMaxStages = 6;                  // stages of 1-tile units (32 KB each), same ring
 constexpr int kTileBytes = 128 * 128;          // 128 rows x 64 bf16
 constexpr int kABytes = LA_TPC * kTileBytes;   // weight tiles per unit
 constexpr int kBBytes = 128 * 128;             // <= 128 rows x 64 bf16
@@ -27,7 +28,7 @@ constexpr int kThreads = 192;
 constexpr int kTmemCols = 512;                 // 2 buffers x LA_TPC tiles x 128 columns
 constexpr int kEpiLd = 33;                     // fused-epilogue staging [128 f][33]
 constexpr size_t kSmemBytes =
-    1024 + kStages * (kABytes + kBBytes) + 128 * kEpiLd * 4 + 2 * kStages * 8 + 4 * 8 + 16;
+    1024 + kStages * (kABytes + kBBytes) + 128 * kEpiLd * 4 + 2 * kMaxStages * 8 + 4 * 8 + 16 + 128 * 4;
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -142,18 +143,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const FwdPlan* P = args.plan;
   uint8_t* sm = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = sm;
-  uint8_t* sB = sA + kStages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  // one 192 KB ring: nst stages of (weights a_bytes | step rows 16 KB), the
+  // weight and row halves in two contiguous regions (1024-B aligned)
+  const int nst = args.tpc == LA_TPC ? kStages : kMaxStages;
+  const uint32_t a_stage = (uint32_t)args.tpc * kTileBytes;
+  uint8_t* sB = sA + nst * a_stage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + kStages * (kABytes + kBBytes));
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* sflag = reinterpret_cast<int*>(tmem_slot + 1);
   float* sEpi = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
+  float* sRstd = sEpi + 128 * kEpiLd;   // fused epilogues: per-row deferred-norm scale
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < nst; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
     ptx::fence_barrier_init();
   }
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long Pn = gridDim.x;
   const long u_begin = (long)blockIdx.x * U / Pn;
   const long u_end = (long)(blockIdx.x + 1) * U / Pn;
-  const int n_pre = (int)min((long)kStages, u_end - u_begin);
+  const int n_pre = (int)min((long)nst, u_end - u_begin);
 
   // PDL: the weights do not depend on the previous kernel, so the first
   // stages' weight tiles stream in while the previous kernel drains.
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     pol_w = ptx::policy_evict_first();   // weights: streamed once
     for (int i = 0; i < n_pre; ++i) {
       ptx::mbar_expect_tx_noarrive(&full[i], a_bytes);
-      ptx::bulk_load(sA + i * kABytes, a_src(u_begin + i), a_bytes, &full[i], pol_w);
+      ptx::bulk_load(sA + i * a_stage, a_src(u_begin + i), a_bytes, &full[i], pol_w);
     }
   }
   la_pdl_wait();
@@ -215,15 +221,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       long it = 0;
       for (long u = u_begin; u < u_end; ++u, ++it) {
         const int k = (int)(u % kb);
-        const int s = (int)(it % kStages);
-        const uint32_t r = (uint32_t)(it / kStages);
+        const int s = (int)(it % nst);
+        const uint32_t r = (uint32_t)(it / nst);
         const bool load_b = !(args.debug & 1);
         if (it < n_pre) {
           ptx::mbar_expect_tx(&full[s], load_b ? bbytes : 0);   // weights already in flight
         } else {
           ptx::mbar_wait(&empty[s], (r - 1) & 1);
           ptx::mbar_expect_tx(&full[s], a_bytes + (load_b ? bbytes : 0));
-          ptx::bulk_load(sA + s * kABytes, a_src(u), a_bytes, &full[s], pol_w);
+          ptx::bulk_load(sA + s * a_stage, a_src(u), a_bytes, &full[s], pol_w);
         }
         if (load_b)
           ptx::bulk_load(sB + s * kBBytes, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
@@ -244,10 +250,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t d_tmem = tmem + buf * (LA_TPC * 128);   // TMEM sized for LA_TPC
         for (; u < seg_end; ++u, ++it) {
-          const int s = (int)(it % kStages);
-          ptx::mbar_wait(&full[s], (uint32_t)(it / kStages) & 1);
+          const int s = (int)(it % nst);
+          ptx::mbar_wait(&full[s], (uint32_t)(it / nst) & 1);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(sA + s * kABytes);
+          const uint32_t a_addr = ptx::smem_u32(sA + s * a_stage);
           const uint32_t b_addr = ptx::smem_u32(sB + s * kBBytes);
           if (args.debug & 2) {
             ptx::mbar_arrive(&empty[s]);
@@ -315,6 +321,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::named_bar_sync(1, 128);
           __threadfence();
         }
+        if (et < n_rows) {
+          float s = 0.f;
+          for (int t = 0; t < args.nrm.tiles; ++t) s += __ldcg(args.nrm.ss + t * 128 + et);
+          sRstd[et] = rsqrtf(s * args.nrm.inv_d + args.nrm.eps);
+        }
+        ptx::named_bar_sync(1, 128);
         for (int tt = 0; tt < tpc; ++tt) {
           const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
           const int ftile = tile * tpc + tt;
@@ -332,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // deferred RMSNorm of the projection input: scale token columns
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj)
-              sEpi[f * kEpiLd + jj] = jj < nj ? v[jj] * __ldg(args.rstd + c0 + jj) : 0.f;
+              sEpi[f * kEpiLd + jj] = jj < nj ? v[jj] * sRstd[c0 + jj] : 0.f;
             ptx::named_bar_sync(1, 128);
             epi_apply<EPI>(args, P, ftile, c0, n_rows, sEpi, et);
             ptx::named_bar_sync(1, 128);

@@ -59,7 +59,7 @@ struct LaGemmArgs {
   unsigned long long* keys;          // LOGITS: [128] (value, -index) atomicMax keys
   float* logits;                     // LOGITS: [128][V] dump or null
   int V;
-  const float* rstd;                 // fused epilogues: deferred RMSNorm row scale [128]
+  LaRowNorm nrm;                     // fused epilogues: deferred RMSNorm of the input rows
 };
 
 enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_LOGITS = 3 };

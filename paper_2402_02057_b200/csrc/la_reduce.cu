@@ -72,6 +72,18 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
   return ((unsigned long long)u << 32) | (uint32_t)(0x7fffffff - idx);
 }
 
+// rsqrt(mean(x^2) + eps) of token tok from the per-tile sums; the 16 threads
+// of a half-warp (one token) split the tiles
+__device__ __forceinline__ float rstd16(const LaRowNorm& n, int tok) {
+  const int l16 = threadIdx.x & 15;
+  const unsigned mask = 0xffffu << (threadIdx.x & 16);
+  float s = 0.f;
+  for (int t = l16; t < n.tiles; t += 16) s += __ldcg(n.ss + t * 128 + tok);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+  return rsqrtf(s * n.inv_d + n.eps);
+}
+
 }  // namespace
 
 // grid = (H + 2*KVH tiles, rows/8), block = 128: thread = (token, 4 rotary pairs)
@@ -85,7 +97,7 @@ __global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
   const int i0 = (threadIdx.x & 15) * 4;
   float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
   float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
-  const float rs = e.rstd[tok];   // deferred RMSNorm of the projection input
+  const float rs = rstd16(e.nrm, tok);   // deferred RMSNorm of the projection input
   a.x *= rs; a.y *= rs; a.z *= rs; a.w *= rs;
   b.x *= rs; b.y *= rs; b.z *= rs; b.w *= rs;
   const bool v_tile = t >= e.H + e.KVH;
@@ -108,44 +120,38 @@ __global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
   *reinterpret_cast<uint2*>(dst + i0 + 64) = make_uint2(pack2(b.x, b.y), pack2(b.z, b.w));
 }
 
-// grid = rows, block = 512: x (+)= sum of segment partials (or := embedding
-// row), then RMSNorm -> bf16 GEMM input (packed LA rows)
-__global__ void __launch_bounds__(512) la_resid_norm_kernel(LaResidNorm e) {
+// grid = (d/128 tiles, rows/8), block = 256: warp = (row, 128-feature tile),
+// lane = 4 features.  x (+)= sum of segment partials (or := embedding row);
+// next GEMM input bf16(x * g) (deferred RMSNorm) and the tile's sum of x^2
+__global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
   LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
-  const int r = blockIdx.x;
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (r >= P->n_rows) return;
-  __shared__ float red[16];
+  const int t = blockIdx.x;
+  const int f = t * 128 + (threadIdx.x & 31) * 4;
   float* xr = e.x + (size_t)r * e.d;
-  float ss = 0.f;
-  for (int f = threadIdx.x * 4; f < e.d; f += blockDim.x * 4) {
-    float4 v;
-    if (e.embed) {
-      const __nv_bfloat16* er = e.embed + (size_t)P->ids[r] * e.d + f;
-      float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(er));
-      float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(er + 2));
-      v = make_float4(lo.x, lo.y, hi.x, hi.y);
-    } else {
-      v = *reinterpret_cast<const float4*>(xr + f);
-      if (e.ws) {
-        const int t = f >> 7;
-        const float4 p = seg_sum4(e.ws, t, e.sp.max_segs, tile_nseg(e.sp, t), r, f & 127);
-        v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
-      }
+  float4 v;
+  if (e.embed) {
+    const __nv_bfloat16* er = e.embed + (size_t)P->ids[r] * e.d + f;
+    const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(er));
+    const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(er + 2));
+    v = make_float4(lo.x, lo.y, hi.x, hi.y);
+  } else {
+    v = *reinterpret_cast<const float4*>(xr + f);
+    if (e.ws) {
+      const float4 p = seg_sum4(e.ws, t, e.sp.max_segs, tile_nseg(e.sp, t), r, f & 127);
+      v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
     }
-    *reinterpret_cast<float4*>(xr + f) = v;
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
-  // deferred RMSNorm: the next projection consumes bf16(x * g); its epilogue
-  // scales the accumulator by the row's rsqrt(mean(x^2) + eps)
-  const float inv = rsqrtf(block_sum(ss, red) / e.d + e.eps);
-  if (threadIdx.x == 0) e.rstd[r] = inv;
-  for (int f = threadIdx.x * 4; f < e.d; f += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + f);
-    const float4 g = *reinterpret_cast<const float4*>(e.g + f);
-    *reinterpret_cast<uint2*>(e.h + la_act_off(r, f)) =
-        make_uint2(pack2(v.x * g.x, v.y * g.y), pack2(v.z * g.z, v.w * g.w));
-  }
+  *reinterpret_cast<float4*>(xr + f) = v;
+  const float4 g = *reinterpret_cast<const float4*>(e.g + f);
+  *reinterpret_cast<uint2*>(e.h + la_act_off(r, f)) =
+      make_uint2(pack2(v.x * g.x, v.y * g.y), pack2(v.z * g.z, v.w * g.w));
+  float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) e.ss[t * 128 + r] = ss;
 }
 
 // grid = (ffn/64 tiles, rows/8), block = 128: thread = (token, 4 outputs)
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(128) la_swiglu_epi_kernel(LaSwigluEpi e) {
   const int t = blockIdx.x;
   const int nseg = tile_nseg(e.sp, t);
   const int i0 = (threadIdx.x & 15) * 4;
-  const float rs = e.rstd[tok];
+  const float rs = rstd16(e.nrm, tok);
   float4 g = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
   float4 u = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
   g.x *= rs; g.y *= rs; g.z *= rs; g.w *= rs;
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(128) la_logits_epi_kernel(LaLogitsEpi e) {
   if (valid) {
     const float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0);
     const float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0 + 4);
-    const float rs = e.rstd[tok];
+    const float rs = rstd16(e.nrm, tok);
     const float v[8] = {a.x * rs, a.y * rs, a.z * rs, a.w * rs, b.x * rs, b.y * rs, b.z * rs, b.w * rs};
 #pragma unroll
     for (int q = 0; q < 8; ++q) {

@@ -18,7 +18,7 @@ struct LaQkvEpi {
   __nv_bfloat16 *kc, *vc;        // layer base [slots][KVH][128]
   const float *rope_cos, *rope_sin;
   int H, KVH;
-  const float* rstd;             // [128] deferred RMSNorm row scale (la_resid_norm_kernel)
+  LaRowNorm nrm;                 // deferred RMSNorm of the projection input
 };
 
 struct LaResidNorm {
@@ -32,7 +32,7 @@ struct LaResidNorm {
   __nv_bfloat16* h;              // packed LA rows (la_act_off): bf16(x * g)
   int d;
   float eps;
-  float* rstd;                   // [128] rsqrt(mean(x^2) + eps), applied by the consumer
+  float* ss;                     // [d/128][128] per-tile sums of x^2 (LaRowNorm.ss)
 };
 
 struct LaSwigluEpi {
@@ -42,7 +42,7 @@ struct LaSwigluEpi {
   LaSplit sp;
   __nv_bfloat16* act;            // packed LA rows (la_act_off)
   int act_ld;
-  const float* rstd;
+  LaRowNorm nrm;
 };
 
 struct LaLogitsEpi {
@@ -52,7 +52,7 @@ struct LaLogitsEpi {
   unsigned long long* keys;      // [128] per-row (value, -index) atomicMax keys
   float* logits;                 // [128][V] or null
   int V;
-  const float* rstd;
+  LaRowNorm nrm;
 };
 
 __global__ void la_qkv_epi_kernel(LaQkvEpi e);
