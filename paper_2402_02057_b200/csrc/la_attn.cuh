@@ -36,6 +36,9 @@ struct LaAttnFusedArgs {
   int H, KVH, S, nrb_max;
   float scale;
   int spread_merge;              // grid <= SMs: every chunk CTA merges a share of the rows
+  int fuse_qkv;                  // grid <= SMs: the QKV epilogue runs here first (grid barrier)
+  LaQkvEpi qkv;                  // its arguments
+  unsigned* gbar;                // grid-barrier counter (monotonic; + grid per launch)
   unsigned long long* trace;     // optional [grid][8] globaltimer stamps (LA_ATTN_TRACE=1)
 };
 

@@ -19,6 +19,7 @@
 #include "la_attn.cuh"
 #include "la_common.cuh"
 #include "la_gemm.cuh"
+#include "la_reduce_dev.cuh"
 
 namespace {
 
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   const int kvh = e / (a.nrb_max * (S + 1));
   const int rb = (e / (S + 1)) % a.nrb_max;
   const int split = e % (S + 1);
-  if (rb >= n_rb) return;
+  const bool active = rb < n_rb;
   const bool step_unit = split == S;
   int k_begin, k_end;
   if (step_unit) {
@@ -121,6 +122,39 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
       cp_async16(smem_u32(kb + kKeyTile * 256) + swz(row, ch), a.vc + off, ok);
     }
   };
+  // prefix keys are cached K/V of earlier steps: start streaming them now
+  // (before the QKV epilogue), the step block's keys only after it
+  auto issue_first = [&]() {
+#pragma unroll 1
+    for (int t = 0; t < kStages - 1; ++t) {
+      if (t < n_tiles) load_kv(t);
+      cp_commit();
+    }
+  };
+  if (active && !step_unit) issue_first();
+  if (a.fuse_qkv) {
+    // QKV split-K epilogue (la_qkv_fix) spread over every CTA of the grid,
+    // then a grid barrier: all CTAs are resident (grid <= SMs, 1 CTA / SM)
+    const int T = a.H + 2 * a.KVH;
+    const long total = (long)T * n_rows * 16;
+    for (long idx = (long)blockIdx.x * 256 + tid; idx < total; idx += (long)gridDim.x * 256)
+      la_qkv_fix(a.qkv, P, (int)(idx / ((long)n_rows * 16)), (int)((idx >> 4) % n_rows));
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(a.gbar, 1u);
+      const unsigned target = (old / gridDim.x + 1) * gridDim.x;
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.gbar) : "memory");
+        if ((int)(v - target) < 0) __nanosleep(32);
+      } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+  }
+  if (!active) return;
+  if (step_unit) issue_first();
+
   // ---- q fragments straight from global (m16n8k16 A layout)
   const int qrow0 = warp * 16 + (lane >> 2);
   uint32_t qf[8][4];
@@ -131,20 +165,13 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const int col = kk * 16 + (lane & 3) * 2;
-      qf[kk][0] = pa ? __ldg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
-      qf[kk][1] = pb ? __ldg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
-      qf[kk][2] = pa ? __ldg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
-      qf[kk][3] = pb ? __ldg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
+      qf[kk][0] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
+      qf[kk][1] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
+      qf[kk][2] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
+      qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
     }
   }
 
-  // issue the chunk's first kStages-1 K/V tiles (all of it for <= 4 tiles);
-  // the step block's keys are the rows' own K/V at slots ctx + global row
-#pragma unroll 1
-  for (int t = 0; t < kStages - 1; ++t) {
-    if (t < n_tiles) load_kv(t);
-    cp_commit();
-  }
   if (step_unit) {
     // structured mask: a query row sees its chain's step keys and itself;
     // one thread per row builds its 128-bit set in registers (independent loads)

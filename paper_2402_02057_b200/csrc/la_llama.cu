@@ -362,6 +362,12 @@ int llama_create(la_engine* e) {
     af.S = units - 1;
     // co-residency (1 CTA per SM, grid <= SMs) makes the spread merge's wait safe
     af.spread_merge = (p->KVH * af.nrb_max * units <= la_sm_count()) && !getenv("LA_ATTN_LAST_MERGE");
+    // optional (LA_ATTN_FUSE_QKV=1): the QKV epilogue inside the attention
+    // kernel behind a grid barrier (needs every CTA co-resident).  Measured
+    // slower: 32K threads reduce the partials ~3x slower than the separate
+    // wide kernel, more than the saved dependency hop.
+    af.fuse_qkv = af.spread_merge && !p->fused && getenv("LA_ATTN_FUSE_QKV") && atoi(getenv("LA_ATTN_FUSE_QKV")) == 1;
+    RET_IF(lalloc(e, &af.gbar, 1));
     af.scale = 1.0f / sqrtf(128.0f);
     af.q = p->q;
     af.out = p->attn;
@@ -499,6 +505,12 @@ static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
   const size_t lstride = (size_t)e->slots * p->KVH * 128;
   a.kc = reinterpret_cast<__nv_bfloat16*>(e->kc) + l * lstride;
   a.vc = reinterpret_cast<__nv_bfloat16*>(e->vc) + l * lstride;
+  if (a.fuse_qkv) {
+    __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc) + l * lstride;
+    __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc) + l * lstride;
+    a.qkv = LaQkvEpi{LaPrefetch{}, e->d_plan, p->ws, split_of(p->qkv[l]), p->q, kc, vc, p->rope_cos,
+                     p->rope_sin, p->H, p->KVH, p->nrm};
+  }
   KT_BEGIN(st);
   CK(la_launch(la_attn_fused_kernel, dim3(p->KVH * a.nrb_max * (a.S + 1)), dim3(256), la_attn_fused_smem(), st,
                p->pdl, a));
@@ -537,7 +549,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       if (!(p->skip & 64)) RET_IF(la_gemm_launch(p->qkv[l], st, p->pdl));
       KT_END(st, "gemm_qkv");
     }
-    if (!p->fused) {
+    if (!p->fused && !(p->attn_fused && p->af.fuse_qkv)) {
       LaQkvEpi q{prefetch_of(p->o[l], pf_frac(p->o[l], 20e6)), e->d_plan, p->ws,
                  split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride, p->rope_cos,
                  p->rope_sin, p->H, p->KVH, p->nrm};

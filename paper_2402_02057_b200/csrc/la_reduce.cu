@@ -16,42 +16,9 @@
 
 #include "la_gemm.cuh"
 #include "la_reduce.cuh"
+#include "la_reduce_dev.cuh"
 
 namespace {
-
-constexpr int kMaxSegUnroll = 16;
-
-// sum over segments of 4 consecutive features (f4 = f/4) of token tok, tile t
-__device__ __forceinline__ float4 seg_sum4(const float* ws, int t, int max_segs, int nseg, int tok,
-                                           int f) {
-  const float4* p = reinterpret_cast<const float4*>(ws + ((size_t)t * max_segs * 128 + tok) * 128 + f);
-  constexpr size_t stride = 128 * 128 / 4;
-  float4 v[kMaxSegUnroll];
-#pragma unroll
-  for (int s = 0; s < kMaxSegUnroll; ++s)
-    if (s < nseg) v[s] = __ldcg(p + s * stride);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int s = 0; s < kMaxSegUnroll; ++s)
-    if (s < nseg) { acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w; }
-  for (int s = kMaxSegUnroll; s < nseg; ++s) {   // rare: very narrow GEMMs
-    float4 w = __ldcg(p + s * stride);
-    acc.x += w.x; acc.y += w.y; acc.z += w.z; acc.w += w.w;
-  }
-  return acc;
-}
-
-__device__ __forceinline__ int tile_nseg(const LaSplit& sp, int t) {
-  long c0;
-  int n;
-  la_tile_segs(t, sp.kb, sp.n_tiles, sp.grid, c0, n, sp.tpc);
-  return n;
-}
-
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
@@ -72,18 +39,6 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
   return ((unsigned long long)u << 32) | (uint32_t)(0x7fffffff - idx);
 }
 
-// rsqrt(mean(x^2) + eps) of token tok from the per-tile sums; the 16 threads
-// of a half-warp (one token) split the tiles
-__device__ __forceinline__ float rstd16(const LaRowNorm& n, int tok) {
-  const int l16 = threadIdx.x & 15;
-  const unsigned mask = 0xffffu << (threadIdx.x & 16);
-  float s = 0.f;
-  for (int t = l16; t < n.tiles; t += 16) s += __ldcg(n.ss + t * 128 + tok);
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
-  return rsqrtf(s * n.inv_d + n.eps);
-}
-
 }  // namespace
 
 // grid = (H + 2*KVH tiles, rows/8), block = 128: thread = (token, 4 rotary pairs)
@@ -92,32 +47,7 @@ __global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
   const FwdPlan* P = e.plan;
   const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
   if (tok >= P->n_rows) return;
-  const int t = blockIdx.x;
-  const int nseg = tile_nseg(e.sp, t);
-  const int i0 = (threadIdx.x & 15) * 4;
-  float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
-  float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
-  const float rs = rstd16(e.nrm, tok);   // deferred RMSNorm of the projection input
-  a.x *= rs; a.y *= rs; a.z *= rs; a.w *= rs;
-  b.x *= rs; b.y *= rs; b.z *= rs; b.w *= rs;
-  const bool v_tile = t >= e.H + e.KVH;
-  __nv_bfloat16* dst;
-  if (t < e.H) dst = e.q_out + ((size_t)tok * e.H + t) * 128;
-  else if (!v_tile) dst = e.kc + ((size_t)P->slot[tok] * e.KVH + (t - e.H)) * 128;
-  else dst = e.vc + ((size_t)P->slot[tok] * e.KVH + (t - e.H - e.KVH)) * 128;
-  if (!v_tile) {
-    // rotate-half RoPE at the row's absolute position
-    const float4 c = *reinterpret_cast<const float4*>(e.rope_cos + (size_t)P->pos[tok] * 64 + i0);
-    const float4 s = *reinterpret_cast<const float4*>(e.rope_sin + (size_t)P->pos[tok] * 64 + i0);
-    const float4 a2 = make_float4(a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y,
-                                  a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
-    const float4 b2 = make_float4(b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y,
-                                  b.z * c.z + a.z * s.z, b.w * c.w + a.w * s.w);
-    a = a2;
-    b = b2;
-  }
-  *reinterpret_cast<uint2*>(dst + i0) = make_uint2(pack2(a.x, a.y), pack2(a.z, a.w));
-  *reinterpret_cast<uint2*>(dst + i0 + 64) = make_uint2(pack2(b.x, b.y), pack2(b.z, b.w));
+  la_qkv_fix(e, P, blockIdx.x, tok);
 }
 
 // grid = (d/128 tiles, rows/8), block = 256: warp = (row, 128-feature tile),

@@ -1,0 +1,84 @@
+// Device helpers shared by the split-K reduce / epilogue kernels
+// (la_reduce.cu) and the fused attention kernel (la_attn_fused.cu).
+#pragma once
+#include <cuda_bf16.h>
+
+#include "la_gemm.cuh"
+#include "la_reduce.cuh"
+
+constexpr int kMaxSegUnroll = 16;
+
+// sum over segments of 4 consecutive features (f4 = f/4) of token tok, tile t
+static __device__ __forceinline__ float4 seg_sum4(const float* ws, int t, int max_segs, int nseg, int tok,
+                                           int f) {
+  const float4* p = reinterpret_cast<const float4*>(ws + ((size_t)t * max_segs * 128 + tok) * 128 + f);
+  constexpr size_t stride = 128 * 128 / 4;
+  float4 v[kMaxSegUnroll];
+#pragma unroll
+  for (int s = 0; s < kMaxSegUnroll; ++s)
+    if (s < nseg) v[s] = __ldcg(p + s * stride);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < kMaxSegUnroll; ++s)
+    if (s < nseg) { acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w; }
+  for (int s = kMaxSegUnroll; s < nseg; ++s) {   // rare: very narrow GEMMs
+    float4 w = __ldcg(p + s * stride);
+    acc.x += w.x; acc.y += w.y; acc.z += w.z; acc.w += w.w;
+  }
+  return acc;
+}
+
+static __device__ __forceinline__ int tile_nseg(const LaSplit& sp, int t) {
+  long c0;
+  int n;
+  la_tile_segs(t, sp.kb, sp.n_tiles, sp.grid, c0, n, sp.tpc);
+  return n;
+}
+
+static __device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// rsqrt(mean(x^2) + eps) of token tok from the per-tile sums; the 16 threads
+// of a half-warp (one token) split the tiles
+static __device__ __forceinline__ float rstd16(const LaRowNorm& n, int tok) {
+  const int l16 = threadIdx.x & 15;
+  const unsigned mask = 0xffffu << (threadIdx.x & 16);
+  float s = 0.f;
+  for (int t = l16; t < n.tiles; t += 16) s += __ldcg(n.ss + t * 128 + tok);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+  return rsqrtf(s * n.inv_d + n.eps);
+}
+
+// QKV epilogue of feature tile t, token tok, on the 16 threads of a half-warp
+// (lane & 15 -> 4 rotary pairs): piece sums in piece order, deferred-norm
+// scale, rotate-half RoPE on q / k; q to the Q buffer, k / v to the cache slot
+static __device__ __forceinline__ void la_qkv_fix(const LaQkvEpi& e, const FwdPlan* P, int t, int tok) {
+  const int nseg = tile_nseg(e.sp, t);
+  const int i0 = (threadIdx.x & 15) * 4;
+  float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
+  float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
+  const float rs = rstd16(e.nrm, tok);   // deferred RMSNorm of the projection input
+  a.x *= rs; a.y *= rs; a.z *= rs; a.w *= rs;
+  b.x *= rs; b.y *= rs; b.z *= rs; b.w *= rs;
+  const bool v_tile = t >= e.H + e.KVH;
+  __nv_bfloat16* dst;
+  if (t < e.H) dst = e.q_out + ((size_t)tok * e.H + t) * 128;
+  else if (!v_tile) dst = e.kc + ((size_t)P->slot[tok] * e.KVH + (t - e.H)) * 128;
+  else dst = e.vc + ((size_t)P->slot[tok] * e.KVH + (t - e.H - e.KVH)) * 128;
+  if (!v_tile) {
+    // rotate-half RoPE at the row's absolute position
+    const float4 c = *reinterpret_cast<const float4*>(e.rope_cos + (size_t)P->pos[tok] * 64 + i0);
+    const float4 s = *reinterpret_cast<const float4*>(e.rope_sin + (size_t)P->pos[tok] * 64 + i0);
+    const float4 a2 = make_float4(a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y,
+                                  a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
+    const float4 b2 = make_float4(b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y,
+                                  b.z * c.z + a.z * s.z, b.w * c.w + a.w * s.w);
+    a = a2;
+    b = b2;
+  }
+  *reinterpret_cast<uint2*>(dst + i0) = make_uint2(pack2(a.x, a.y), pack2(a.z, a.w));
+  *reinterpret_cast<uint2*>(dst + i0 + 64) = make_uint2(pack2(b.x, b.y), pack2(b.z, b.w));
+}
