@@ -339,3 +339,5 @@ __global__ void __launch_bounds__(512) la_attn_merge_kernel(LaAttnArgs a) {
 
 template __global__ void la_attn_chunks_kernel<64>(LaAttnArgs a);
 template __global__ void la_attn_chunks_kernel<128>(LaAttnArgs a);
+
+LA_TL_DEFINE_SETTER(attn)

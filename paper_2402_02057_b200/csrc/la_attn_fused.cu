@@ -383,3 +383,5 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   }
   stamp(a, 6);
 }
+
+LA_TL_DEFINE_SETTER(attnf)

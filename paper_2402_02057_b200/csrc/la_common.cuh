@@ -132,8 +132,26 @@ __device__ __forceinline__ int la_round16(int x) { return (x + 15) & ~15; }
 __device__ __forceinline__ void la_pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Optional in-graph timeline (LA_TIMELINE=1, profiling only): block 0 of
+// every kernel stamps globaltimer when its dependency wait returns, with the
+// launch shape as a signature.  buf[0] = record count, then pairs.
+#define LA_TL_CAP 8192
+#ifdef __CUDACC__
+static __constant__ unsigned long long* g_la_tl;
+#define LA_TL_DEFINE_SETTER(name)                                        \
+  void la_tl_set_##name(unsigned long long* p) { cudaMemcpyToSymbol(g_la_tl, &p, sizeof(p)); }
+#endif
 __device__ __forceinline__ void la_pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (g_la_tl && (threadIdx.x | threadIdx.y | blockIdx.x | blockIdx.y | blockIdx.z) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    const unsigned i = atomicAdd(reinterpret_cast<unsigned*>(g_la_tl), 1u);
+    if (i < LA_TL_CAP) {
+      g_la_tl[1 + 2 * i] = t;
+      g_la_tl[2 + 2 * i] = ((unsigned long long)(gridDim.x * gridDim.y) << 16) | blockDim.x;
+    }
+  }
 }
 #define LA_PDL_ENTRY() \
   do {                 \

@@ -508,3 +508,5 @@ extern "C" int32_t la_pack_weight(const void* src, int32_t rows, int32_t K, void
   if (e != cudaSuccess) { la_set_error("pack launch: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }
   return LA_OK;
 }
+
+LA_TL_DEFINE_SETTER(gemm)

@@ -147,6 +147,8 @@ static int lalloc(la_engine* e, T** p, size_t n) {
   return LA_OK;
 }
 
+static void tl_install(la_engine* e);   // LA_TIMELINE profiling hook (below)
+
 // ------------------------------------------------ persistent forward kernel
 static int mega_create(la_engine* e) {
   LlamaPath* p = e->llama;
@@ -381,6 +383,7 @@ int llama_create(la_engine* e) {
     if (ce != cudaSuccess) { la_set_error("fused attn smem attr: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
   }
   p->mega = getenv("LA_MEGA") && atoi(getenv("LA_MEGA")) == 1;
+  tl_install(e);
   if (p->mega) RET_IF(mega_create(e));
   return LA_OK;
 }
@@ -449,6 +452,24 @@ static void kt_report() {
             a.second.first * 1e3 / a.second.second, 100.0 * a.second.first / tot);
   fprintf(stderr, "[la ktime] total %.3f ms\n", tot);
   g_kt.marks.clear();
+}
+
+// ------------------------------------------------------------- timeline
+void la_tl_set_gemm(unsigned long long*);
+void la_tl_set_reduce(unsigned long long*);
+void la_tl_set_attnf(unsigned long long*);
+void la_tl_set_attn(unsigned long long*);
+void la_tl_set_llama(unsigned long long*);
+void la_tl_set_state(unsigned long long*);
+void la_tl_set_mega(unsigned long long*);
+static unsigned long long* g_tl_buf = nullptr;
+static void tl_install(la_engine* e) {
+  if (!getenv("LA_TIMELINE") || g_tl_buf) return;
+  (void)e;   // process-lifetime profiling buffer (not owned by an engine)
+  if (cudaMalloc(&g_tl_buf, (1 + 2 * LA_TL_CAP) * 8) != cudaSuccess) { g_tl_buf = nullptr; return; }
+  cudaMemset(g_tl_buf, 0, (1 + 2 * LA_TL_CAP) * 8);
+  la_tl_set_gemm(g_tl_buf); la_tl_set_reduce(g_tl_buf); la_tl_set_attnf(g_tl_buf); la_tl_set_attn(g_tl_buf);
+  la_tl_set_llama(g_tl_buf); la_tl_set_state(g_tl_buf); la_tl_set_mega(g_tl_buf);
 }
 
 // ------------------------------------------------------------- forward
@@ -574,7 +595,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       LaSwigluEpi sw{prefetch_of(p->down[l], pf_frac(p->down[l], 40e6)), e->d_plan, p->ws,
                      split_of(p->gu[l]), p->act, p->ffn, p->nrm};
       KT_BEGIN(st);
-      if (!(p->skip & 16)) CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, sw));
+      if (!(p->skip & 16)) CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 16), dim3(128), 0, st, p->pdl, sw));
       KT_END(st, "swiglu_epi");
       ++n;
     }
@@ -793,6 +814,7 @@ bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes)
     case 14: *src = p->act; *bytes = R * p->ffn * 2; return true;
     case 15: *src = p->row_amax; *bytes = R * 4; return true;
     case 17: *src = p->af.trace; *bytes = (size_t)p->KVH * p->af.nrb_max * (p->af.S + 1) * 64; return p->af.trace != nullptr;
+    case 18: *src = g_tl_buf; *bytes = (1 + 2 * LA_TL_CAP) * 8; return g_tl_buf != nullptr;
     case 16: *src = a.trace; *bytes = (size_t)la_sm_count() * a.trace_slots * 64; return a.trace != nullptr;
     default: return false;
   }
@@ -847,3 +869,5 @@ extern "C" int32_t la_gemm_timing_read(la_engine* e, double* out16) {
   }
   return LA_OK;
 }
+
+LA_TL_DEFINE_SETTER(llama)

@@ -1190,3 +1190,5 @@ cudaError_t la_mega_launch(const LaMegaArgs& a, int grid, cudaStream_t st, bool 
   }
   return la_launch(la_mega_kernel, dim3(grid), dim3(kThreads), kSmemBytes, st, pdl, a);
 }
+
+LA_TL_DEFINE_SETTER(mega)

@@ -42,7 +42,7 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
 }  // namespace
 
 // grid = (H + 2*KVH tiles, rows/8), block = 128: thread = (token, 4 rotary pairs)
-__global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
+__global__ void __launch_bounds__(128, 8) la_qkv_epi_kernel(LaQkvEpi e) {
   LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
   const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(128) la_qkv_epi_kernel(LaQkvEpi e) {
 // grid = (d/128 tiles, rows/8), block = 256: warp = (row, 128-feature tile),
 // lane = 4 features.  x (+)= sum of segment partials (or := embedding row);
 // next GEMM input bf16(x * g) (deferred RMSNorm) and the tile's sum of x^2
-__global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
+__global__ void __launch_bounds__(256, 4) la_resid_norm_kernel(LaResidNorm e) {
   LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
   const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
   const int t = blockIdx.x;
   const int f = t * 128 + (threadIdx.x & 31) * 4;
   float* xr = e.x + (size_t)r * e.d;
+  const float4 g = __ldg(reinterpret_cast<const float4*>(e.g + f));
   float4 v;
   if (e.embed) {
     const __nv_bfloat16* er = e.embed + (size_t)P->ids[r] * e.d + f;
@@ -75,7 +76,6 @@ __global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
     }
   }
   *reinterpret_cast<float4*>(xr + f) = v;
-  const float4 g = *reinterpret_cast<const float4*>(e.g + f);
   *reinterpret_cast<uint2*>(e.h + la_act_off(r, f)) =
       make_uint2(pack2(v.x * g.x, v.y * g.y), pack2(v.z * g.z, v.w * g.w));
   float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
@@ -84,30 +84,36 @@ __global__ void __launch_bounds__(256) la_resid_norm_kernel(LaResidNorm e) {
   if ((threadIdx.x & 31) == 0) e.ss[t * 128 + r] = ss;
 }
 
-// grid = (ffn/64 tiles, rows/8), block = 128: thread = (token, 4 outputs)
-__global__ void __launch_bounds__(128) la_swiglu_epi_kernel(LaSwigluEpi e) {
+// grid = (ffn/64 tiles, rows/16), block = 128: thread = (2 tokens, 4 outputs)
+// -- one wave over the GPU; every load issued before the first use
+__global__ void __launch_bounds__(128, 8) la_swiglu_epi_kernel(LaSwigluEpi e) {
   LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
-  const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
-  if (tok >= P->n_rows) return;
   const int t = blockIdx.x;
   const int nseg = tile_nseg(e.sp, t);
   const int i0 = (threadIdx.x & 15) * 4;
-  const float rs = rstd16(e.nrm, tok);
-  float4 g = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
-  float4 u = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
-  g.x *= rs; g.y *= rs; g.z *= rs; g.w *= rs;
-  u.x *= rs; u.y *= rs; u.z *= rs; u.w *= rs;
-  auto sw = [](float gg, float uu) { return gg / (1.0f + __expf(-gg)) * uu; };
-  *reinterpret_cast<uint2*>(e.act + la_act_off(tok, t * 64 + i0)) =
-      make_uint2(pack2(sw(g.x, u.x), sw(g.y, u.y)), pack2(sw(g.z, u.z), sw(g.w, u.w)));
+  const int tok0 = blockIdx.y * 16 + (threadIdx.x >> 4);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int tok = tok0 + 8 * h;
+    if (tok >= P->n_rows) return;
+    const LaSsLoads ssl = rstd16_issue(e.nrm, tok);
+    float4 g, u;
+    seg_sum4x2(e.ws, t, e.sp.max_segs, nseg, tok, i0, i0 + 64, g, u);
+    const float rs = rstd16_finish(e.nrm, tok, ssl);
+    g.x *= rs; g.y *= rs; g.z *= rs; g.w *= rs;
+    u.x *= rs; u.y *= rs; u.z *= rs; u.w *= rs;
+    auto sw = [](float gg, float uu) { return gg / (1.0f + __expf(-gg)) * uu; };
+    *reinterpret_cast<uint2*>(e.act + la_act_off(tok, t * 64 + i0)) =
+        make_uint2(pack2(sw(g.x, u.x), sw(g.y, u.y)), pack2(sw(g.z, u.z), sw(g.w, u.w)));
+  }
 }
 
 // grid = (LM-head tiles, rows/8), block = 128: thread = (token, 8 vocabulary
 // rows); the row's argmax is folded with one 64-bit atomicMax per (tile, row)
 // whose key orders by value then by LOWER index (sampling.py:17-19), so the
 // result does not depend on arrival order.
-__global__ void __launch_bounds__(128) la_logits_epi_kernel(LaLogitsEpi e) {
+__global__ void __launch_bounds__(128, 8) la_logits_epi_kernel(LaLogitsEpi e) {
   LA_PDL_ENTRY();
   const FwdPlan* P = e.plan;
   const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
@@ -117,9 +123,10 @@ __global__ void __launch_bounds__(128) la_logits_epi_kernel(LaLogitsEpi e) {
   const int f0 = (threadIdx.x & 15) * 8;
   unsigned long long best = 0ull;
   if (valid) {
-    const float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0);
-    const float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, f0 + 4);
-    const float rs = rstd16(e.nrm, tok);
+    const LaSsLoads ssl = rstd16_issue(e.nrm, tok);
+    float4 a, b;
+    seg_sum4x2(e.ws, t, e.sp.max_segs, nseg, tok, f0, f0 + 4, a, b);
+    const float rs = rstd16_finish(e.nrm, tok, ssl);
     const float v[8] = {a.x * rs, a.y * rs, a.z * rs, a.w * rs, b.x * rs, b.y * rs, b.z * rs, b.w * rs};
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -153,3 +160,5 @@ __global__ void la_argmax_finish_kernel(const FwdPlan* P, unsigned long long* ke
   row_amax[r] = idx;
   if (dp && P->own[r]) dp->amax[P->grow[r]] = idx;
 }
+
+LA_TL_DEFINE_SETTER(reduce)

@@ -6,7 +6,7 @@
 #include "la_gemm.cuh"
 #include "la_reduce.cuh"
 
-constexpr int kMaxSegUnroll = 16;
+constexpr int kMaxSegUnroll = 10;   // ~the piece count of the narrow projections (O / down)
 
 // sum over segments of 4 consecutive features (f4 = f/4) of token tok, tile t
 static __device__ __forceinline__ float4 seg_sum4(const float* ws, int t, int max_segs, int nseg, int tok,
@@ -40,6 +40,65 @@ static __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Single-round-trip variants: every load of the pieces (and of the norm
+// statistics) is issued before the first use, so a kernel pays one L2 latency.
+// (kSegBatch loads per group in flight: ~the piece count of the wide
+// projections; more would cost registers and occupancy)
+constexpr int kSegBatch = 4;
+// sums over the stream-K pieces of two 4-feature groups (f0, f1) of token tok
+static __device__ __forceinline__ void seg_sum4x2(const float* ws, int t, int max_segs, int nseg, int tok, int f0,
+                                                  int f1, float4& a, float4& b) {
+  const float* base = ws + ((size_t)t * max_segs * 128 + tok) * 128;
+  const float4* p0 = reinterpret_cast<const float4*>(base + f0);
+  const float4* p1 = reinterpret_cast<const float4*>(base + f1);
+  constexpr size_t stride = 128 * 128 / 4;
+  float4 va[kSegBatch], vb[kSegBatch];
+#pragma unroll
+  for (int s = 0; s < kSegBatch; ++s)
+    if (s < nseg) {
+      va[s] = __ldcg(p0 + s * stride);
+      vb[s] = __ldcg(p1 + s * stride);
+    }
+  a = make_float4(0.f, 0.f, 0.f, 0.f);
+  b = a;
+#pragma unroll
+  for (int s = 0; s < kSegBatch; ++s)
+    if (s < nseg) {
+      a.x += va[s].x; a.y += va[s].y; a.z += va[s].z; a.w += va[s].w;
+      b.x += vb[s].x; b.y += vb[s].y; b.z += vb[s].z; b.w += vb[s].w;
+    }
+  for (int s = kSegBatch; s < nseg; ++s) {   // narrow projections (O / down)
+    const float4 x = __ldcg(p0 + s * stride), y = __ldcg(p1 + s * stride);
+    a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+    b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+  }
+}
+
+// deferred-norm statistics of a token in two halves: issue the loads of the
+// per-tile sums (16 lanes of a half-warp split the tiles) ...
+struct LaSsLoads {
+  float v[4];
+};
+static __device__ __forceinline__ LaSsLoads rstd16_issue(const LaRowNorm& n, int tok) {
+  LaSsLoads r;
+  const int l16 = threadIdx.x & 15;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = l16 + 16 * i;
+    r.v[i] = t < n.tiles ? __ldcg(n.ss + t * 128 + tok) : 0.f;
+  }
+  return r;
+}
+// ... and finish: sum, reduce over the half-warp, rsqrt
+static __device__ __forceinline__ float rstd16_finish(const LaRowNorm& n, int tok, const LaSsLoads& r) {
+  const unsigned mask = 0xffffu << (threadIdx.x & 16);
+  float s = r.v[0] + r.v[1] + r.v[2] + r.v[3];
+  for (int t = (threadIdx.x & 15) + 64; t < n.tiles; t += 16) s += __ldcg(n.ss + t * 128 + tok);   // d > 8192
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+  return rsqrtf(s * n.inv_d + n.eps);
+}
+
 // rsqrt(mean(x^2) + eps) of token tok from the per-tile sums; the 16 threads
 // of a half-warp (one token) split the tiles
 static __device__ __forceinline__ float rstd16(const LaRowNorm& n, int tok) {
@@ -58,24 +117,30 @@ static __device__ __forceinline__ float rstd16(const LaRowNorm& n, int tok) {
 static __device__ __forceinline__ void la_qkv_fix(const LaQkvEpi& e, const FwdPlan* P, int t, int tok) {
   const int nseg = tile_nseg(e.sp, t);
   const int i0 = (threadIdx.x & 15) * 4;
-  float4 a = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0);
-  float4 b = seg_sum4(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 64);
-  const float rs = rstd16(e.nrm, tok);   // deferred RMSNorm of the projection input
+  const bool v_tile = t >= e.H + e.KVH;
+  // every independent load first: norm statistics, RoPE tables, pieces
+  const LaSsLoads ssl = rstd16_issue(e.nrm, tok);
+  const int pos = P->pos[tok];
+  float4 c = make_float4(1.f, 1.f, 1.f, 1.f), sn = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!v_tile) {
+    c = __ldg(reinterpret_cast<const float4*>(e.rope_cos + (size_t)pos * 64 + i0));
+    sn = __ldg(reinterpret_cast<const float4*>(e.rope_sin + (size_t)pos * 64 + i0));
+  }
+  float4 a, b;
+  seg_sum4x2(e.ws, t, e.sp.max_segs, nseg, tok, i0, i0 + 64, a, b);
+  const float rs = rstd16_finish(e.nrm, tok, ssl);   // deferred RMSNorm of the projection input
   a.x *= rs; a.y *= rs; a.z *= rs; a.w *= rs;
   b.x *= rs; b.y *= rs; b.z *= rs; b.w *= rs;
-  const bool v_tile = t >= e.H + e.KVH;
   __nv_bfloat16* dst;
   if (t < e.H) dst = e.q_out + ((size_t)tok * e.H + t) * 128;
   else if (!v_tile) dst = e.kc + ((size_t)P->slot[tok] * e.KVH + (t - e.H)) * 128;
   else dst = e.vc + ((size_t)P->slot[tok] * e.KVH + (t - e.H - e.KVH)) * 128;
   if (!v_tile) {
     // rotate-half RoPE at the row's absolute position
-    const float4 c = *reinterpret_cast<const float4*>(e.rope_cos + (size_t)P->pos[tok] * 64 + i0);
-    const float4 s = *reinterpret_cast<const float4*>(e.rope_sin + (size_t)P->pos[tok] * 64 + i0);
-    const float4 a2 = make_float4(a.x * c.x - b.x * s.x, a.y * c.y - b.y * s.y,
-                                  a.z * c.z - b.z * s.z, a.w * c.w - b.w * s.w);
-    const float4 b2 = make_float4(b.x * c.x + a.x * s.x, b.y * c.y + a.y * s.y,
-                                  b.z * c.z + a.z * s.z, b.w * c.w + a.w * s.w);
+    const float4 a2 = make_float4(a.x * c.x - b.x * sn.x, a.y * c.y - b.y * sn.y,
+                                  a.z * c.z - b.z * sn.z, a.w * c.w - b.w * sn.w);
+    const float4 b2 = make_float4(b.x * c.x + a.x * sn.x, b.y * c.y + a.y * sn.y,
+                                  b.z * c.z + a.z * sn.z, b.w * c.w + a.w * sn.w);
     a = a2;
     b = b2;
   }

@@ -122,3 +122,5 @@ __global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered
     *reinterpret_cast<uint4*>(cache + dst) = *reinterpret_cast<const uint4*>(src_base + src);
   }
 }
+
+LA_TL_DEFINE_SETTER(state)
