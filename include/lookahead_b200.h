@@ -128,6 +128,18 @@ int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_t n_prefix,
                           const int32_t* ids, const int32_t* rel, const int32_t* chain,
                           int32_t chain_stride, float* logits, void* stream);
 
+/* Jacobi decoding (replaces decode_jacobi, decoding.py:119-149): solve the
+ * m-token greedy continuation of `prompt` by parallel fixed-point iteration
+ * from the initial guess `init` (the caller draws it like the reference:
+ * rng.integers(0, V, m)).  Each iteration is one forward of the triangular
+ * chain layout (layout.py:185-194), m + 1 rows; stops when an iterate
+ * repeats, after at most m iterations.  out_tokens[m] = the fixed point,
+ * iterates[n_iterations][m] (may be null) = every iterate after the guess.
+ * m + 1 <= 128 rows; ValueError cases as the reference (empty prompt, m < 1). */
+int32_t la_decode_jacobi(la_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t m,
+                         const int32_t* init, int32_t* out_tokens, int32_t* iterates,
+                         int32_t* n_iterations, void* stream);
+
 /* ------------------------------------------------- lookahead parallelism */
 /* LP (parallel.py:145-192): rank `rank` of `world` replicas, each holding the
  * full model, evaluates its share of window columns and candidate branches;

@@ -309,6 +309,32 @@ def decode_autoregressive(model, prompt, max_tokens: int, eos=None) -> list[int]
     return out
 
 
+def decode_jacobi(model, prompt, m: int, rng: np.random.Generator):
+    """``decoding.py:119-149``: random initial guess from ``rng``, then
+    parallel fixed-point iteration over the triangular chain layout
+    (``layout.py:185-194``: token i sees query 0 and the tokens before it).
+    Returns (tokens, iterates incl. the guess, iterations)."""
+    if not len(prompt):
+        raise ValueError("prompt must be nonempty")
+    if m < 1:
+        raise ValueError("generation length m must be >= 1")
+    prefix = [int(t) for t in prompt]
+    current = [int(t) for t in rng.integers(0, model.vocab_size, size=m)]
+    iterates = [list(current)]
+    iterations = 0
+    new = current
+    for _ in range(m):
+        rows = Rows([prefix[-1]] + current, list(range(m + 1)),
+                    [list(range(i)) for i in range(m + 1)], [], [])
+        new = model.argmax_rows(prefix[:-1], rows)[:m]
+        iterations += 1
+        iterates.append(list(new))
+        if new == current:
+            break
+        current = new
+    return new, iterates, iterations
+
+
 # ------------------------------------------------ lookahead parallelism
 def lp_partition(W: int, N: int, D: int, n_cand: int) -> list[dict]:
     """``parallel.py:64-116``: contiguous column ranges (sizes differ by <=1),

@@ -272,8 +272,28 @@ def gen_lp(la):
                                 "(parallel.py:64-192)", "plans": plans, "runs": runs})
 
 
+def gen_jacobi(la):
+    # decode_jacobi (decoding.py:119-149) on the TinyTransformer of config 1;
+    # the rng is passed in the state the caller left it, so each case records
+    # the seed of a fresh default_rng
+    model = la.transformer_init(seed=0, vocab_size=256, d_model=16, n_layers=2, n_heads=2)
+    cases = []
+    for k, m in enumerate([1, 2, 3, 8, 16, 31, 64]):
+        prompt = [int(t) for t in np.random.default_rng(700 + k).integers(0, 256, 5 + 3 * k)]
+        seed = 900 + k
+        toks, traj, iters = la.decode_jacobi(model, prompt, m, np.random.default_rng(seed))
+        cases.append({"model": [0, 256], "prompt": prompt, "m": m, "rng_seed": seed,
+                      "tokens": toks, "iterates": traj.iterates, "iterations": iters})
+    _dump("jacobi.json", {"source": "decoding.decode_jacobi (decoding.py:119-149)", "cases": cases})
+
+
 def main():
     la = _ref()
+    if len(sys.argv) > 1:   # regenerate selected fixtures only, e.g. `make_golden.py jacobi`
+        for name in sys.argv[1:]:
+            globals()["gen_" + name](la)
+        print("golden vectors written to", OUT)
+        return
     gen_layouts(la)
     gen_pool(la)
     gen_window(la)
@@ -281,6 +301,7 @@ def main():
     gen_forward(la)
     gen_lp(la)
     gen_decode(la)
+    gen_jacobi(la)
     print("golden vectors written to", OUT)
 
 

@@ -8,14 +8,14 @@ C ABI (``include/lookahead_b200.h``).
 __version__ = "0.1.0"
 
 from .analytics import RunMetrics, compression_ratio, flops_proxy
-from .decoding import decode_autoregressive, decode_lookahead, window_rng_stream
+from .decoding import decode_autoregressive, decode_jacobi, decode_lookahead, window_rng_stream
 from .layout import CandidateBranch, QueryToken, StepLayout, chain_layout
 from .models import (CODELLAMA_7B, LLAMA2_13B, LLAMA2_70B, LLAMA2_7B, PRESETS, B200Model,
                      LlamaConfig, LlamaModel, TinyTransformer)
 from .parallel import CommStats, column_ranges, decode_lookahead_devices, lp_init, step_comm
 from .pool import NGramPool
-from .types import (DegenerateDistributionError, GenerationConfig, LayoutError, SamplerSpec,
-                    StepRecord)
+from .types import (DegenerateDistributionError, GenerationConfig, JacobiTrajectory, LayoutError,
+                    SamplerSpec, StepRecord)
 
 
 def transformer_init(seed, vocab_size, d_model=16, n_layers=2, n_heads=2, **kw):
@@ -31,10 +31,10 @@ def greedy_token(probs) -> int:
 
 __all__ = [
     "B200Model", "CODELLAMA_7B", "CandidateBranch", "CommStats", "DegenerateDistributionError",
-    "GenerationConfig", "LLAMA2_13B", "LLAMA2_70B", "LLAMA2_7B", "LayoutError", "LlamaConfig",
+    "GenerationConfig", "JacobiTrajectory", "LLAMA2_13B", "LLAMA2_70B", "LLAMA2_7B", "LayoutError", "LlamaConfig",
     "LlamaModel", "NGramPool", "PRESETS", "QueryToken", "RunMetrics", "SamplerSpec",
     "StepLayout", "StepRecord", "TinyTransformer", "chain_layout", "column_ranges",
-    "compression_ratio", "decode_autoregressive", "decode_lookahead",
+    "compression_ratio", "decode_autoregressive", "decode_jacobi", "decode_lookahead",
     "decode_lookahead_devices", "flops_proxy", "greedy_token", "lp_init", "step_comm",
     "transformer_init", "window_rng_stream",
 ]

@@ -33,6 +33,7 @@ EXPORTS = (
     "la_destroy", "la_decode_lookahead", "la_decode_autoregressive", "la_forward_layout",
     "la_lp_unique_id", "la_lp_init", "la_decode_lookahead_group", "la_debug_read",
     "la_gemm_timing_reset", "la_gemm_timing_read", "la_forward_timing_read", "la_packed_bytes",
+    "la_decode_jacobi",
     "la_pack_weight",
 )
 

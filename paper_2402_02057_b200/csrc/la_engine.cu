@@ -479,29 +479,21 @@ extern "C" int32_t la_decode_autoregressive(la_engine* e, int32_t max_tokens, in
 }
 
 // ------------------------------------------------------------- parity hook
-extern "C" int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_t n_prefix,
-                                     int32_t n_rows, const int32_t* ids, const int32_t* rel,
-                                     const int32_t* chain, int32_t chain_stride, float* logits,
-                                     void* stream) {
-  if (!e) { la_set_error("null engine"); return LA_ERR_INVALID_CONFIG; }
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  CK(cudaSetDevice(e->device));
+// Validate a query layout (models.py:33-64 contract: row 0 at rel 0; row i
+// sees one row per rel 0..rel[i]-1, listed in rel order) and build its plan.
+static int build_layout_plan(la_engine* e, int n_prefix, int n_rows, const int32_t* ids, const int32_t* rel,
+                             const int32_t* chain, int chain_stride, FwdPlan* P) {
   const int V = e->desc.vocab;
   if (n_rows < 1 || n_rows > LA_MAX_ROWS) { la_set_error("n_rows must be in [1, %d]", LA_MAX_ROWS); return LA_ERR_UNSUPPORTED; }
   if (n_prefix < 0 || n_prefix + n_rows + 1 > e->desc.max_context) { la_set_error("prefix too long"); return LA_ERR_CAPACITY; }
-  for (int i = 0; i < n_prefix; ++i)
-    if (prefix[i] < 0 || prefix[i] >= V) { la_set_error("token %d outside vocabulary of size %d", prefix[i], V); return LA_ERR_INVALID_CONFIG; }
   for (int i = 0; i < n_rows; ++i)
     if (ids[i] < 0 || ids[i] >= V) { la_set_error("token %d outside vocabulary of size %d", ids[i], V); return LA_ERR_INVALID_CONFIG; }
-  // layout contract (models.py:33-64): row 0 at rel 0; row i sees one row per
-  // rel 0..rel[i]-1, listed in rel order
   if (rel[0] != 0) { la_set_error("query 0 must sit at relative position 0"); return LA_ERR_LAYOUT; }
-  FwdPlan* P = new FwdPlan();
   memset(P, 0, sizeof(FwdPlan));
   P->n_rows = n_rows; P->n_pad = (n_rows + 15) & ~15; P->n_prefix = n_prefix; P->n_global = n_rows;
   P->want_logits = 1;
   for (int i = 0; i < n_rows; ++i) {
-    if (rel[i] < 0 || rel[i] >= LA_MAX_CHAIN) { delete P; la_set_error("rel_pos out of range"); return LA_ERR_LAYOUT; }
+    if (rel[i] < 0 || rel[i] >= LA_MAX_CHAIN) { la_set_error("rel_pos out of range"); return LA_ERR_LAYOUT; }
     P->ids[i] = ids[i];
     P->pos[i] = n_prefix + rel[i];
     P->slot[i] = n_prefix + i;
@@ -511,40 +503,123 @@ extern "C" int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_
     for (int j = 0; j < rel[i]; ++j) {
       int v = chain[(size_t)i * chain_stride + j];
       if (v < 0 || v >= n_rows || v == i || rel[v] != j) {
-        delete P;
         la_set_error("query %d has an invalid chain entry %d at rel_pos %d", i, v, j);
         return LA_ERR_LAYOUT;
       }
       P->chain[i][j] = n_prefix + v;
     }
   }
+  return LA_OK;
+}
+
+static int prefill_prefix(la_engine* e, const int32_t* prefix, int n_prefix, cudaStream_t st) {
+  const int V = e->desc.vocab;
+  for (int i = 0; i < n_prefix; ++i)
+    if (prefix[i] < 0 || prefix[i] >= V) { la_set_error("token %d outside vocabulary of size %d", prefix[i], V); return LA_ERR_INVALID_CONFIG; }
+  if (n_prefix == 0) return LA_OK;
+  int rc = dgrow(e, &e->d_tokens, &e->tokens_cap, n_prefix);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(e->d_tokens, prefix, (size_t)n_prefix * 4, cudaMemcpyHostToDevice, st));
+  return prefill(e, n_prefix, st);
+}
+
+// one forward of an uploaded plan: logits[n_rows][V] to host (if non-null)
+// and/or the per-row greedy argmax (ties -> lowest id) to host
+static int run_plan(la_engine* e, const FwdPlan* P, float* logits, int32_t* amax, cudaStream_t st) {
+  const int V = e->desc.vocab, n_rows = P->n_rows;
+  CK(cudaMemcpyAsync(e->d_plan, P, sizeof(FwdPlan), cudaMemcpyHostToDevice, st));
+  float* d_logits = nullptr;
+  const bool need_logits = logits != nullptr || e->is_tiny();
+  if (need_logits && cudaMallocAsync(&d_logits, (size_t)n_rows * V * 4, st) != cudaSuccess) {
+    la_set_error("cudaMallocAsync failed");
+    return LA_ERR_CUDA;
+  }
   int rc = LA_OK;
-  do {
-    if (n_prefix > 0) {
-      if ((rc = dgrow(e, &e->d_tokens, &e->tokens_cap, n_prefix))) break;
-      cudaMemcpyAsync(e->d_tokens, prefix, (size_t)n_prefix * 4, cudaMemcpyHostToDevice, st);
-      if ((rc = prefill(e, n_prefix, st))) break;
-    }
-    cudaMemcpyAsync(e->d_plan, P, sizeof(FwdPlan), cudaMemcpyHostToDevice, st);
-    float* d_logits = nullptr;
-    if (cudaMallocAsync(&d_logits, (size_t)n_rows * V * 4, st) != cudaSuccess) {
-      la_set_error("cudaMallocAsync failed"); rc = LA_ERR_CUDA; break;
-    }
-    if (e->is_tiny()) {
-      la_tiny_forward<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, d_logits);
-      if (cudaGetLastError() != cudaSuccess) { la_set_error("forward launch failed"); rc = LA_ERR_CUDA; }
-    } else {
-      rc = llama_forward_plan(e, d_logits, st);
-    }
-    if (rc == LA_OK) {
-      cudaError_t ce = cudaMemcpyAsync(logits, d_logits, (size_t)n_rows * V * 4, cudaMemcpyDeviceToHost, st);
-      if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
-      if (ce != cudaSuccess) { la_set_error("forward failed: %s", cudaGetErrorString(ce)); rc = LA_ERR_CUDA; }
-    }
-    cudaFreeAsync(d_logits, st);
-  } while (0);
+  std::vector<float> host;
+  if (e->is_tiny()) {
+    la_tiny_forward<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, d_logits);
+    if (cudaGetLastError() != cudaSuccess) { la_set_error("forward launch failed"); rc = LA_ERR_CUDA; }
+  } else {
+    rc = llama_forward_plan(e, d_logits, st);
+  }
+  if (rc == LA_OK) {
+    cudaError_t ce = cudaSuccess;
+    float* lg = logits;
+    if (e->is_tiny() && !lg) { host.resize((size_t)n_rows * V); lg = host.data(); }
+    if (lg) ce = cudaMemcpyAsync(lg, d_logits, (size_t)n_rows * V * 4, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && amax && !e->is_tiny()) ce = llama_copy_argmax(e, amax, n_rows, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) { la_set_error("forward failed: %s", cudaGetErrorString(ce)); rc = LA_ERR_CUDA; }
+    if (rc == LA_OK && amax && e->is_tiny())
+      for (int r = 0; r < n_rows; ++r) {   // np.argmax semantics: first maximum
+        const float* row = lg + (size_t)r * V;
+        int best = 0;
+        for (int v = 1; v < V; ++v)
+          if (row[v] > row[best]) best = v;
+        amax[r] = best;
+      }
+  }
+  if (d_logits) cudaFreeAsync(d_logits, st);
+  return rc;
+}
+
+extern "C" int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_t n_prefix,
+                                     int32_t n_rows, const int32_t* ids, const int32_t* rel,
+                                     const int32_t* chain, int32_t chain_stride, float* logits,
+                                     void* stream) {
+  if (!e) { la_set_error("null engine"); return LA_ERR_INVALID_CONFIG; }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  FwdPlan* P = new FwdPlan();
+  int rc = build_layout_plan(e, n_prefix, n_rows, ids, rel, chain, chain_stride, P);
+  if (rc == LA_OK) rc = prefill_prefix(e, prefix, n_prefix, st);
+  if (rc == LA_OK) rc = run_plan(e, P, logits, nullptr, st);
   delete P;
   return rc;
+}
+
+// Jacobi decoding (decoding.py:119-149): m-token greedy continuation by
+// parallel fixed-point iteration over the triangular chain layout
+// (layout.py:185-194); the prompt is prefilled once, every iteration is one
+// forward of m+1 rows whose per-row argmax (device) is the next iterate.
+extern "C" int32_t la_decode_jacobi(la_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t m,
+                                    const int32_t* init, int32_t* out_tokens, int32_t* iterates,
+                                    int32_t* n_iterations, void* stream) {
+  if (!e || !prompt || !init || !out_tokens || !n_iterations) { la_set_error("null argument"); return LA_ERR_INVALID_CONFIG; }
+  if (n_prompt < 1) { la_set_error("prompt must be nonempty"); return LA_ERR_INVALID_CONFIG; }
+  if (m < 1) { la_set_error("generation length m must be >= 1"); return LA_ERR_INVALID_CONFIG; }
+  if (m + 1 > LA_MAX_ROWS) { la_set_error("m + 1 must be <= %d rows", LA_MAX_ROWS); return LA_ERR_UNSUPPORTED; }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  const int V = e->desc.vocab;
+  for (int i = 0; i < m; ++i)
+    if (init[i] < 0 || init[i] >= V) { la_set_error("token %d outside vocabulary of size %d", init[i], V); return LA_ERR_INVALID_CONFIG; }
+  const int n_prefix = n_prompt - 1;
+  int rc = prefill_prefix(e, prompt, n_prefix, st);
+  if (rc) return rc;
+  std::vector<int32_t> ids(m + 1), rel(m + 1), chain((size_t)(m + 1) * (m + 1), 0), cur(init, init + m),
+      amax(m + 1);
+  for (int i = 0; i <= m; ++i) {
+    rel[i] = i;
+    for (int j = 0; j < i; ++j) chain[(size_t)i * (m + 1) + j] = j;
+  }
+  ids[0] = prompt[n_prompt - 1];
+  FwdPlan* P = new FwdPlan();
+  int it = 0;
+  for (; it < m; ++it) {
+    for (int i = 0; i < m; ++i) ids[i + 1] = cur[i];
+    if ((rc = build_layout_plan(e, n_prefix, m + 1, ids.data(), rel.data(), chain.data(), m + 1, P))) break;
+    if ((rc = run_plan(e, P, nullptr, amax.data(), st))) break;
+    if (iterates) memcpy(iterates + (size_t)it * m, amax.data(), (size_t)m * 4);
+    const bool same = std::equal(cur.begin(), cur.end(), amax.begin());
+    std::copy(amax.begin(), amax.begin() + m, cur.begin());
+    if (same) { ++it; break; }
+  }
+  delete P;
+  if (rc) return rc;
+  memcpy(out_tokens, cur.data(), (size_t)m * 4);
+  *n_iterations = it;
+  return LA_OK;
 }
 
 // ------------------------------------------------- in-process LP group

@@ -69,3 +69,4 @@ int llama_decode_loop(la_engine* e, cudaStream_t st, int* launches);
 int llama_forward_plan(la_engine* e, float* d_logits, cudaStream_t st);
 int llama_step_forward(la_engine* e, cudaStream_t st);   // K1 + forward + owned argmax
 int llama_mega_error(la_engine* e);                      // persistent-kernel dependency timeout flag
+cudaError_t llama_copy_argmax(la_engine* e, int32_t* host, int n, cudaStream_t st);   // last forward's row argmax

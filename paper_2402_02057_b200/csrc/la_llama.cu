@@ -847,6 +847,12 @@ extern "C" int32_t la_forward_timing_read(la_engine* e, double* out2) {
   return LA_OK;
 }
 
+// per-row greedy argmax of the last forward (la_argmax_finish_kernel / the
+// megakernel's head fix-up write row_amax)
+cudaError_t llama_copy_argmax(la_engine* e, int32_t* host, int n, cudaStream_t st) {
+  return cudaMemcpyAsync(host, e->llama->row_amax, (size_t)n * 4, cudaMemcpyDeviceToHost, st);
+}
+
 // spin-timeout flag of the persistent kernel (a dependency never satisfied)
 int llama_mega_error(la_engine* e) {
   LlamaPath* p = e->llama;

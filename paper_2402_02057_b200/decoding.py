@@ -17,7 +17,7 @@ from . import _lib
 from .analytics import RunMetrics
 from .models import B200Model
 from .pool import NGramPool
-from .types import GenerationConfig, SamplerSpec, StepRecord
+from .types import GenerationConfig, JacobiTrajectory, SamplerSpec, StepRecord
 
 
 def window_rng_draws(window: int, ngram: int, max_tokens: int) -> int:
@@ -159,3 +159,29 @@ def decode_autoregressive(model, prompt: Sequence[int], sampler: SamplerSpec, ma
                                               m.stream()))
     m.last_stats = io.stats()
     return io.tokens()
+
+
+def decode_jacobi(model, prompt: Sequence[int], m: int,
+                  rng: np.random.Generator) -> tuple[list[int], JacobiTrajectory, int]:
+    """Solve an m-token greedy continuation by parallel fixed-point iteration
+    (reference decoding.py:119-149).  The initial guess is drawn from ``rng``
+    exactly like the reference (``rng.integers(0, V, size=m)``); every
+    iteration is one device forward of the triangular chain layout
+    (layout.py:185-194) with the per-row argmax taken on the GPU, so the
+    fixed point equals greedy autoregressive decoding in <= m iterations."""
+    mdl = _require_b200(model)
+    if not len(prompt):
+        raise ValueError("prompt must be nonempty")
+    if m < 1:
+        raise ValueError("generation length m must be >= 1")
+    p = _prompt(prompt)
+    init = np.ascontiguousarray(rng.integers(0, mdl.vocab_size, size=m).astype(np.int32))
+    out = np.zeros(m, dtype=np.int32)
+    iterates = np.zeros((m, m), dtype=np.int32)
+    n_it = C.c_int32(0)
+    P32 = C.POINTER(C.c_int32)
+    _lib.check(mdl.lib.la_decode_jacobi(mdl.engine(), p.ctypes.data_as(P32), len(p), int(m),
+                                        init.ctypes.data_as(P32), out.ctypes.data_as(P32),
+                                        iterates.ctypes.data_as(P32), C.byref(n_it), mdl.stream()))
+    traj = [[int(t) for t in init]] + [[int(t) for t in iterates[i]] for i in range(n_it.value)]
+    return [int(t) for t in out], JacobiTrajectory(traj), int(n_it.value)

@@ -154,3 +154,20 @@ def test_lp_group_bit_identical(pair):
         tD, mD, comm = la.decode_lookahead_devices(m, prompt, cfg, la.SamplerSpec("greedy", seed=2), D)
         assert tD == t1 and mD.steps == m1.steps
         assert comm.sync_events == mD.steps
+
+
+def test_jacobi_fixed_point_equals_greedy(pair):
+    """Jacobi decoding on the bf16 path converges to the same GPU's greedy
+    output in <= m iterations, with a never-shrinking converged prefix."""
+    name, m, orc = pair
+    V = orc.vocab_size
+    prompt = [int(t) for t in np.random.default_rng(21).integers(0, V, 30)]
+    for mlen in (1, 7, 24):
+        toks, traj, iters = la.decode_jacobi(m, prompt, mlen, np.random.default_rng(mlen))
+        assert iters <= mlen
+        assert toks == la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), mlen)
+        prev = 0
+        for it in traj.iterates[1:]:
+            agree = next((i for i, (a, b) in enumerate(zip(it, toks)) if a != b), len(toks))
+            assert agree >= prev
+            prev = agree

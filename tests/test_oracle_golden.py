@@ -196,3 +196,20 @@ def test_bf16_round_is_rne():
     import torch
     ref = torch.tensor(x).to(torch.bfloat16).to(torch.float32).numpy()
     np.testing.assert_array_equal(bf16_round(x), ref)
+
+
+def test_jacobi_matches_reference():
+    """Oracle restatement of decode_jacobi pinned to the reference's iterates."""
+    g = load_golden("jacobi.json")
+    models = {}
+    for case in g["cases"]:
+        if case["m"] > 16:
+            continue   # longer chains are covered on the GPU (fp64 oracle recompute is slow)
+        mk = tuple(case["model"])
+        if mk not in models:
+            models[mk] = TinyTransformerOracle(*mk)
+        toks, iterates, iters = lo.decode_jacobi(models[mk], case["prompt"], case["m"],
+                                                 np.random.default_rng(case["rng_seed"]))
+        assert toks == case["tokens"]
+        assert iterates == case["iterates"]
+        assert iters == case["iterations"]

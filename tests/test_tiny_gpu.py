@@ -187,3 +187,25 @@ def test_tiny_llama_f32_matches_oracle():
         assert met.steps == len(run.steps)
     finally:
         m.close()
+
+
+def test_jacobi_matches_reference(models):
+    """decode_jacobi on the device (la_decode_jacobi): tokens, every iterate and
+    the iteration count equal the reference's (decoding.py:119-149)."""
+    g = load_golden("jacobi.json")
+    for case in g["cases"]:
+        m = models(*case["model"])
+        toks, traj, iters = la.decode_jacobi(m, case["prompt"], case["m"],
+                                             np.random.default_rng(case["rng_seed"]))
+        assert toks == case["tokens"], case["m"]
+        assert traj.iterates == case["iterates"], case["m"]
+        assert iters == case["iterations"]
+        assert toks == la.decode_autoregressive(m, case["prompt"], la.SamplerSpec("greedy"), case["m"])
+
+
+def test_jacobi_errors_match_reference(models):
+    m = models(0, 256)
+    with pytest.raises(ValueError):
+        la.decode_jacobi(m, [], 3, np.random.default_rng(0))
+    with pytest.raises(ValueError):
+        la.decode_jacobi(m, [1, 2], 0, np.random.default_rng(0))
