@@ -84,29 +84,31 @@ __global__ void __launch_bounds__(256, 4) la_resid_norm_kernel(LaResidNorm e) {
   if ((threadIdx.x & 31) == 0) e.ss[t * 128 + r] = ss;
 }
 
-// grid = (ffn/64 tiles, rows/16), block = 128: thread = (2 tokens, 4 outputs)
-// -- one wave over the GPU; every load issued before the first use
+// grid = (ffn/64 tiles, rows/16), block = 128: thread = (token, 8 outputs),
+// 8 threads per token -- one wave over the GPU, every load issued before use
 __global__ void __launch_bounds__(128, 8) la_swiglu_epi_kernel(LaSwigluEpi e) {
   LA_PDL_ENTRY_PF(e.pf);
   const FwdPlan* P = e.plan;
   const int t = blockIdx.x;
+  const int tok = blockIdx.y * 16 + (threadIdx.x >> 3);
+  if (tok >= P->n_rows) return;
   const int nseg = tile_nseg(e.sp, t);
-  const int i0 = (threadIdx.x & 15) * 4;
-  const int tok0 = blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int i0 = (threadIdx.x & 7) * 8;
+  const LaSsLoads ssl = rstd_issue<8>(e.nrm, tok);
+  float4 g0, u0, g1, u1;
+  seg_sum4x2(e.ws, t, e.sp.max_segs, nseg, tok, i0, i0 + 64, g0, u0);
+  seg_sum4x2(e.ws, t, e.sp.max_segs, nseg, tok, i0 + 4, i0 + 68, g1, u1);
+  const float rs = rstd_finish<8>(e.nrm, tok, ssl);
+  const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+  const float u[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+  float w[8];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int tok = tok0 + 8 * h;
-    if (tok >= P->n_rows) return;
-    const LaSsLoads ssl = rstd16_issue(e.nrm, tok);
-    float4 g, u;
-    seg_sum4x2(e.ws, t, e.sp.max_segs, nseg, tok, i0, i0 + 64, g, u);
-    const float rs = rstd16_finish(e.nrm, tok, ssl);
-    g.x *= rs; g.y *= rs; g.z *= rs; g.w *= rs;
-    u.x *= rs; u.y *= rs; u.z *= rs; u.w *= rs;
-    auto sw = [](float gg, float uu) { return gg / (1.0f + __expf(-gg)) * uu; };
-    *reinterpret_cast<uint2*>(e.act + la_act_off(tok, t * 64 + i0)) =
-        make_uint2(pack2(sw(g.x, u.x), sw(g.y, u.y)), pack2(sw(g.z, u.z), sw(g.w, u.w)));
+  for (int i = 0; i < 8; ++i) {
+    const float gg = g[i] * rs, uu = u[i] * rs;
+    w[i] = gg / (1.0f + __expf(-gg)) * uu;
   }
+  *reinterpret_cast<uint4*>(e.act + la_act_off(tok, t * 64 + i0)) =
+      make_uint4(pack2(w[0], w[1]), pack2(w[2], w[3]), pack2(w[4], w[5]), pack2(w[6], w[7]));
 }
 
 // grid = (LM-head tiles, rows/8), block = 128: thread = (token, 8 vocabulary

@@ -75,28 +75,37 @@ static __device__ __forceinline__ void seg_sum4x2(const float* ws, int t, int ma
 }
 
 // deferred-norm statistics of a token in two halves: issue the loads of the
-// per-tile sums (16 lanes of a half-warp split the tiles) ...
+// per-tile sums (the LANES threads of the token -- aligned lane groups --
+// split the tiles) ...
 struct LaSsLoads {
-  float v[4];
+  float v[8];
 };
-static __device__ __forceinline__ LaSsLoads rstd16_issue(const LaRowNorm& n, int tok) {
+template <int LANES = 16>
+static __device__ __forceinline__ LaSsLoads rstd_issue(const LaRowNorm& n, int tok) {
   LaSsLoads r;
-  const int l16 = threadIdx.x & 15;
+  const int l = threadIdx.x & (LANES - 1);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int t = l16 + 16 * i;
+  for (int i = 0; i < 64 / LANES; ++i) {
+    const int t = l + LANES * i;
     r.v[i] = t < n.tiles ? __ldcg(n.ss + t * 128 + tok) : 0.f;
   }
   return r;
 }
-// ... and finish: sum, reduce over the half-warp, rsqrt
-static __device__ __forceinline__ float rstd16_finish(const LaRowNorm& n, int tok, const LaSsLoads& r) {
-  const unsigned mask = 0xffffu << (threadIdx.x & 16);
-  float s = r.v[0] + r.v[1] + r.v[2] + r.v[3];
-  for (int t = (threadIdx.x & 15) + 64; t < n.tiles; t += 16) s += __ldcg(n.ss + t * 128 + tok);   // d > 8192
+// ... and finish: sum, reduce over the lane group, rsqrt
+template <int LANES = 16>
+static __device__ __forceinline__ float rstd_finish(const LaRowNorm& n, int tok, const LaSsLoads& r) {
+  const unsigned mask = ((LANES == 32) ? 0xffffffffu : ((1u << LANES) - 1u)) << (threadIdx.x & 31 & ~(LANES - 1));
+  float s = 0.f;
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
+  for (int i = 0; i < 64 / LANES; ++i) s += r.v[i];
+  for (int t = (threadIdx.x & (LANES - 1)) + 64; t < n.tiles; t += LANES) s += __ldcg(n.ss + t * 128 + tok);   // d > 8192
+#pragma unroll
+  for (int o = LANES / 2; o > 0; o >>= 1) s += __shfl_xor_sync(mask, s, o);
   return rsqrtf(s * n.inv_d + n.eps);
+}
+static __device__ __forceinline__ LaSsLoads rstd16_issue(const LaRowNorm& n, int tok) { return rstd_issue<16>(n, tok); }
+static __device__ __forceinline__ float rstd16_finish(const LaRowNorm& n, int tok, const LaSsLoads& r) {
+  return rstd_finish<16>(n, tok, r);
 }
 
 // rsqrt(mean(x^2) + eps) of token tok from the per-tile sums; the 16 threads
