@@ -78,9 +78,31 @@ size_t la_attn_fused_smem() { return (size_t)kStages * kTileBytes + LA_MAX_ROWS 
 // grid = KVH * nrb_max * (S + 1) units, block = 256 (8 warps x 16 query rows)
 __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a) {
   stamp(a, 0);
-  LA_PDL_ENTRY_PF(a.pf);
-  stamp(a, 1);
+  la_pdl_trigger();
+  la_l2_prefetch_gemm(a.pf);
   const FwdPlan* P = a.plan;
+  {
+    // before the dependency wait: pull this unit's prefix K/V rows into L2.
+    // Only a cache hint -- if the plan or cache is not final yet the lines
+    // are merely refetched after the wait -- so it is always safe.
+    const int S = a.S;
+    const int e = blockIdx.x;
+    const int split = e % (S + 1);
+    const int ctx = P->n_prefix;
+    if (split < S && P->n_rows > 0 && ctx > 0) {
+      const int kvh = e / (a.nrb_max * (S + 1));
+      const int CH = chunk_keys(ctx, S);
+      const int k0 = min(ctx, split * CH), k1 = min(ctx, (split + 1) * CH);
+      const size_t kv_ld = (size_t)a.KVH * 128;
+      for (int i = threadIdx.x; i < 2 * (k1 - k0); i += blockDim.x) {
+        const int key = k0 + (i >> 1);
+        const __nv_bfloat16* src = ((i & 1) ? a.vc : a.kc) + (size_t)key * kv_ld + kvh * 128;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(reinterpret_cast<uint64_t>(src)) : "memory");
+      }
+    }
+  }
+  la_pdl_wait();
+  stamp(a, 1);
   const int n_rows = P->n_rows, ctx = P->n_prefix;
   if (n_rows == 0) return;
   const int g = a.H / a.KVH;
