@@ -71,6 +71,12 @@ WORKLOAD = CONFIGS["cfg2"]["name"]
 PRESET = "llama2-7b"
 
 
+# dram__bytes_read.sum + dram__bytes_write.sum of one gate/up GEMM launch from
+# the committed ncu --set full capture (profiles/r01_gemm_gu.ncu-rep, cfg2
+# decode step, M=120): the dominant kernel's measured traffic per launch
+GU_TRAFFIC_BYTES = {"llama2-7b": 180.926976e6 + 5.477632e6}
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -350,7 +356,10 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "kernel": "la_gemm_kernel<SWIGLU> (gate/up, tcgen05)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                     "frac": (achieved / hbm) if achieved else None,
+                     "traffic": GU_TRAFFIC_BYTES.get(PRESET) if PRESET == "llama2-7b" and W == 15 else None,
+                     "traffic_unit": "bytes per launch (ncu, profiles/r01_gemm_gu.ncu-rep)",
+                     "algorithmic_bytes": gu_bytes,
                      "avg_launch_ms": gu_ms, "launches": int(gu_n), "peak_source": peak_src},
         "gpu_launches": int(sum(s["launches"] for s in stats)),
         "clocks": clocks.summary(),
