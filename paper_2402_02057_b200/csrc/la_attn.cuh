@@ -37,6 +37,8 @@ struct LaAttnFusedArgs {
   float scale;
   int spread_merge;              // grid <= SMs: every chunk CTA merges a share of the rows
   int fuse_qkv;                  // grid <= SMs: the QKV epilogue runs here first (grid barrier)
+  int tc;                        // tcgen05 QK^T / PV for chunks of <= 6 key tiles
+  int dbg;                       // LA_ATTN_DBG experiments: 1 skip PV MMAs, 2 skip QK^T MMAs
   LaQkvEpi qkv;                  // its arguments
   unsigned* gbar;                // grid-barrier counter (monotonic; + grid per launch)
   unsigned long long* trace;     // optional [grid][8] globaltimer stamps (LA_ATTN_TRACE=1)

@@ -20,6 +20,7 @@
 #include "la_common.cuh"
 #include "la_gemm.cuh"
 #include "la_reduce_dev.cuh"
+#include "la_ptx.cuh"
 
 namespace {
 
@@ -27,6 +28,14 @@ constexpr int kKeyTile = 64;
 constexpr int kStages = 5;                           // K/V tiles in flight
 constexpr int kTileBytes = 2 * kKeyTile * 256;       // K + V of 64 keys
 constexpr float kLog2e = 1.4426950408889634f;
+// tensor-core path (tcgen05): a chunk of <= kTcTiles key tiles in one pass.
+// smem: Q [2 dim blocks][128 rows][128 B] | K, later P [kTcTiles][16 KB] |
+// V [kTcTiles][2 dim blocks][64 keys][128 B]; TMEM: S tiles at 64 columns each,
+// O at columns 384..511.
+constexpr int kTcTiles = 6;
+constexpr int kTcQ = 0, kTcK = 32768, kTcV = kTcK + kTcTiles * 16384;
+constexpr int kTcSmem = kTcV + kTcTiles * 16384;                   // 224 KB
+constexpr int kMaskOff = kTcSmem > kStages * kTileBytes ? kTcSmem : kStages * kTileBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -63,17 +72,223 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 __device__ __forceinline__ int chunk_keys(int ctx, int S) {
   return ((ctx + S - 1) / S + kKeyTile - 1) / kKeyTile * kKeyTile;
 }
+// bounded mbarrier wait (debug safety: a stuck tensor-core stage records its
+// id in trace slot 7 instead of hanging the GPU)
+__device__ __forceinline__ void mbar_wait_bounded(const LaAttnFusedArgs& a, uint64_t* bar, uint32_t parity, int id) {
+  for (unsigned n = 0;; ++n) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (n > (1u << 22)) {
+      if (a.trace) a.trace[blockIdx.x * 8 + 7] = 1000 + id;
+      return;
+    }
+  }
+}
+
 __device__ __forceinline__ void stamp(const LaAttnFusedArgs& a, int k) {
   if (a.trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    a.trace[blockIdx.x * 8 + k] = t;
+    *reinterpret_cast<volatile unsigned long long*>(a.trace + blockIdx.x * 8 + k) = t;
+  }
+}
+// stamp from the first softmax warp (tensor-core path)
+__device__ __forceinline__ void stamp_w4(const LaAttnFusedArgs& a, int k) {
+  if (a.trace && threadIdx.x == 128) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    *reinterpret_cast<volatile unsigned long long*>(a.trace + blockIdx.x * 8 + k) = t;
+  }
+}
+// per-warp progress marks (debug): trace slot 6 holds one byte per warp
+__device__ __forceinline__ void wmark(const LaAttnFusedArgs& a, int v) {
+  if (a.trace && (a.dbg & 4) && (threadIdx.x & 31) == 0) {
+    reinterpret_cast<volatile uint8_t*>(a.trace + blockIdx.x * 8 + 6)[threadIdx.x >> 5] = (uint8_t)v;
+    __threadfence_system();
   }
 }
 
 }  // namespace
 
-size_t la_attn_fused_smem() { return (size_t)kStages * kTileBytes + LA_MAX_ROWS * 4 * 4 + 16; }
+size_t la_attn_fused_smem() { return (size_t)kMaskOff + LA_MAX_ROWS * 4 * 4 + 64; }
+
+// ---------------------------------------------------------------------------
+// Tensor-core chunk unit: S = Q K^T (tcgen05, M = 128 query rows, N = 64 keys
+// per tile, fp32 in TMEM) -> one-pass masked softmax by warps 4-7 (one TMEM
+// lane = one query row), P (bf16) written over the K tiles -> O = P V
+// (tcgen05, V as the MN-major B operand straight from its [key][dim] smem
+// image) -> unnormalised O and (max, sum) in log2 units, the same partial
+// format as the mma.sync path.
+__device__ void attn_tc_unit(const LaAttnFusedArgs& a, const FwdPlan* P, uint8_t* smem, const uint32_t* sMask,
+                             uint64_t* bars, uint32_t* tmem_slot, int kvh, int rb, int g, int nq, int ctx,
+                             int k_begin, int k_end, int n_tiles, bool step_unit, float* part_o, float2* part_ml) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* sQ = smem + kTcQ;
+  uint8_t* sK = smem + kTcK;
+  uint8_t* sV = smem + kTcV;
+  uint64_t* s_done = bars;
+  uint64_t* o_done = bars + 1;
+  if (tid == 0) {
+    ptx::mbar_init(s_done, 1);
+    ptx::mbar_init(o_done, 1);
+    ptx::fence_barrier_init();
+  }
+  wmark(a, 1);
+  if (warp == 0) ptx::tmem_alloc<512>(tmem_slot);
+  wmark(a, 2);
+  // ---- loads: Q rows (zero beyond the block), the chunk's K and V rows
+  const size_t kv_ld = (size_t)a.KVH * 128;
+  for (int i = tid; i < 128 * 16; i += 256) {
+    const int row = i >> 4, c = i & 15;
+    const int qr = rb * 128 + row;
+    const bool ok = qr < nq;
+    const __nv_bfloat16* src = ok ? a.q + ((size_t)(qr / g) * a.H + kvh * g + qr % g) * 128 + c * 8 : a.q;
+    cp_async16(smem_u32(sQ + (c >> 3) * 16384 + row * 128) + (((c & 7) ^ (row & 7)) << 4), src, ok);
+  }
+  for (int i = tid; i < n_tiles * 64 * 16; i += 256) {
+    const int t = i >> 10, row = (i >> 4) & 63, c = i & 15;
+    const int key = k_begin + t * 64 + row;
+    const bool ok = key < k_end;
+    const size_t off = (size_t)(ok ? key : k_begin) * kv_ld + kvh * 128 + c * 8;
+    const uint32_t o = t * 16384 + (c >> 3) * 8192 + row * 128 + (((c & 7) ^ (row & 7)) << 4);
+    cp_async16(smem_u32(sK) + o, a.kc + off, ok);
+    cp_async16(smem_u32(sV) + o, a.vc + off, ok);
+  }
+  cp_commit();
+  cp_wait<0>();
+  wmark(a, 3);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  stamp(a, 2);
+  wmark(a, 4);
+
+  // ---- S = Q K^T, one 64-column TMEM block per key tile
+  if (warp == 0 && lane == 0) {
+    const uint32_t idesc = ptx::umma_idesc_bf16(128, 64);
+    for (int t = 0; t < ((a.dbg & 2) ? 0 : n_tiles); ++t)
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        ptx::umma_bf16(tmem + t * 64,
+                       ptx::umma_desc_sw128(smem_u32(sQ) + (kk >> 2) * 16384 + (kk & 3) * 32),
+                       ptx::umma_desc_sw128(smem_u32(sK) + t * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32),
+                       idesc, kk > 0 ? 1u : 0u);
+    ptx::umma_commit(s_done);
+    stamp(a, 3);
+  }
+
+  // ---- softmax: all 8 warps; TMEM lane = query row (lane quadrant = warp % 4),
+  // warps w and w+4 take the two halves of the row's columns and exchange the
+  // row max / sum through shared memory
+  const int row = (warp & 3) * 32 + lane;
+  const int half = warp >> 2;
+  const int ncol = n_tiles * 32;                 // columns per half (multiple of 32)
+  const int cbeg = half * ncol;
+  float* sRed = reinterpret_cast<float*>(smem + kTcQ);   // Q is dead once the S MMAs completed
+  const uint32_t t_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const float sl2 = a.scale * kLog2e;
+  const int nvalid = k_end - k_begin;            // columns beyond are masked
+  uint32_t mw[4] = {~0u, ~0u, ~0u, ~0u};
+  if (step_unit) {
+    const uint4 w = *reinterpret_cast<const uint4*>(sMask + row * 4);
+    mw[0] = w.x; mw[1] = w.y; mw[2] = w.z; mw[3] = w.w;
+  }
+  auto vis_bits = [&](int c0) -> uint32_t {
+    const uint32_t r = c0 + 32 <= nvalid ? ~0u : (c0 >= nvalid ? 0u : ((1u << (nvalid - c0)) - 1u));
+    return step_unit ? (r & mw[c0 >> 5]) : r;
+  };
+  mbar_wait_bounded(a, s_done, 0, 1);
+  ptx::tc_fence_after();
+  float m = -INFINITY;
+  for (int c0 = cbeg; c0 < cbeg + ncol; c0 += 32) {
+    float v[32];
+    ptx::tmem_ld32(t_row + c0, v);
+    const uint32_t vis = vis_bits(c0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if ((vis >> j) & 1u) m = fmaxf(m, v[j]);
+  }
+  m *= sl2;                                       // positive scale: commutes with max
+  sRed[half * 128 + row] = m;                     // (S MMAs done: Q smem is free)
+  __syncthreads();
+  m = fmaxf(sRed[row], sRed[128 + row]);
+  const float mb = m == -INFINITY ? 0.f : m;
+  float l = 0.f;
+  for (int c0 = cbeg; c0 < cbeg + ncol; c0 += 32) {
+    float v[32];
+    ptx::tmem_ld32(t_row + c0, v);
+    const uint32_t vis = vis_bits(c0);
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const float p0 = ((vis >> j) & 1u) ? exp2f(fmaf(v[j], sl2, -mb)) : 0.f;
+      const float p1 = ((vis >> (j + 1)) & 1u) ? exp2f(fmaf(v[j + 1], sl2, -mb)) : 0.f;
+      l += p0 + p1;
+      pk[j >> 1] = pack_bf16(p0, p1);
+    }
+    // P tile c0/64 overwrites K tile c0/64 (its S MMAs are complete)
+    uint8_t* prow = sK + (c0 >> 6) * 16384 + row * 128;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int chunk = ((c0 & 63) >> 3) + q;
+      *reinterpret_cast<uint4*>(prow + ((chunk ^ (row & 7)) << 4)) =
+          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    }
+  }
+  sRed[256 + half * 128 + row] = l;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
+  ptx::tc_fence_before();
+  __syncthreads();
+  l = sRed[256 + row] + sRed[256 + 128 + row];
+  stamp_w4(a, 7);
+  // ---- O = P V (V: MN-major B operand, 64-dim blocks 8 KB apart, 8-key groups 1 KB apart)
+  if (warp == 0 && lane == 0) {
+    ptx::tc_fence_after();
+    const uint32_t idesc = ptx::umma_idesc_bf16_bmn(128, 128);
+    for (int t = 0; t < ((a.dbg & 1) ? 0 : n_tiles); ++t)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        ptx::umma_bf16(tmem + 384, ptx::umma_desc_sw128(smem_u32(sK) + t * 16384 + kk * 32),
+                       ptx::umma_desc_sw128_mn(smem_u32(sV) + t * 16384 + kk * 2048, 8192, 1024), idesc,
+                       (t > 0 || kk > 0) ? 1u : 0u);
+    ptx::umma_commit(o_done);
+    stamp(a, 5);
+  }
+  mbar_wait_bounded(a, o_done, 0, 2);
+  ptx::tc_fence_after();
+  {
+    // tcgen05.ld is warp-collective (.sync.aligned): every lane loads, only the
+    // block's valid rows store; the two warps of a quadrant split O's columns
+    const bool valid = rb * 128 + row < nq;
+    float4* dst = reinterpret_cast<float4*>(part_o + (size_t)row * 128);
+    for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
+      float v[32];
+      ptx::tmem_ld32(t_row + 384 + c0, v);
+      if (valid) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          __stcg(dst + (c0 >> 2) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+      }
+    }
+    if (valid && half == 0) __stcg(part_ml + row, make_float2(m, l));
+  }
+  ptx::tc_fence_before();
+  wmark(a, 10);
+  __syncthreads();
+  wmark(a, 11);
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+  wmark(a, 12);
+}
 
 // grid = KVH * nrb_max * (S + 1) units, block = 256 (8 warps x 16 query rows)
 __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a) {
@@ -127,11 +342,17 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sKV = smem;                                                   // [kStages][K | V]
-  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + kStages * kTileBytes);   // [128][4]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + kMaskOff);    // [128][4]
   int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
+  uint64_t* sBars = reinterpret_cast<uint64_t*>(sFlag + 4);           // tensor-core path
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBars + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t kv_ld = (size_t)a.KVH * 128;
   const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+  // tensor-core path when the chunk fits TMEM (<= 6 key tiles) and smem is
+  // 1024-B aligned (SW128 atoms); chunking depends on ctx only, so the path
+  // choice -- and every row's summation order -- is the same for every shard
+  const bool tc = a.tc && n_tiles <= kTcTiles && (smem_u32(smem) & 1023u) == 0u;
 
   auto load_kv = [&](int t) {
     uint8_t* kb = sKV + (t % kStages) * kTileBytes;
@@ -153,7 +374,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
       cp_commit();
     }
   };
-  if (active && !step_unit) issue_first();
+  if (active && !step_unit && !tc) issue_first();
   if (a.fuse_qkv) {
     // QKV split-K epilogue (la_qkv_fix) spread over every CTA of the grid,
     // then a grid barrier: all CTAs are resident (grid <= SMs, 1 CTA / SM)
@@ -175,25 +396,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
     __syncthreads();
   }
   if (!active) return;
-  if (step_unit) issue_first();
-
-  // ---- q fragments straight from global (m16n8k16 A layout)
-  const int qrow0 = warp * 16 + (lane >> 2);
-  uint32_t qf[8][4];
-  {
-    const int qa = rb * 128 + qrow0, qb = qa + 8;
-    const __nv_bfloat16* pa = qa < nq ? a.q + ((size_t)(qa / g) * a.H + kvh * g + qa % g) * 128 : nullptr;
-    const __nv_bfloat16* pb = qb < nq ? a.q + ((size_t)(qb / g) * a.H + kvh * g + qb % g) * 128 : nullptr;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int col = kk * 16 + (lane & 3) * 2;
-      qf[kk][0] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
-      qf[kk][1] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
-      qf[kk][2] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
-      qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
-    }
-  }
-
+  const size_t grp = (size_t)kvh * a.nrb_max + rb;
   if (step_unit) {
     // structured mask: a query row sees its chain's step keys and itself;
     // one thread per row builds its 128-bit set in registers (independent loads)
@@ -216,129 +419,152 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
     __syncthreads();
   }
 
-  float o[16][4];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  const float sl2 = a.scale * kLog2e;
-  stamp(a, 2);
-  const bool warp_active = rb * 128 + warp * 16 < nq;
+  if (tc) {
+    attn_tc_unit(a, P, smem, sMask, sBars, sTmem, kvh, rb, g, nq, ctx, k_begin, k_end, n_tiles, step_unit,
+                 a.part_o + (grp * (S + 1) + split) * 128 * 128, a.part_ml + (grp * (S + 1) + split) * 128);
+  } else {
+    if (step_unit) issue_first();
 
-  for (int t = 0; t < n_tiles; ++t) {
-    if (t + kStages - 1 < n_tiles) load_kv(t + kStages - 1);
-    cp_commit();
-    cp_wait<kStages - 1>();
-    __syncthreads();
-    if (t == 0) stamp(a, 3);
-    if (warp_active) {
-      const uint8_t* sK = sKV + (t % kStages) * kTileBytes;
-      const uint8_t* sV = sK + kKeyTile * 256;
-      float s[8][4];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
-#pragma unroll
+    // ---- q fragments straight from global (m16n8k16 A layout)
+    const int qrow0 = warp * 16 + (lane >> 2);
+    uint32_t qf[8][4];
+    {
+      const int qa = rb * 128 + qrow0, qb = qa + 8;
+      const __nv_bfloat16* pa = qa < nq ? a.q + ((size_t)(qa / g) * a.H + kvh * g + qa % g) * 128 : nullptr;
+      const __nv_bfloat16* pb = qb < nq ? a.q + ((size_t)(qb / g) * a.H + kvh * g + qb % g) * 128 : nullptr;
+  #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-#pragma unroll
-        for (int np = 0; np < 4; ++np) {
-          const int key = np * 16 + (lane & 7) + (lane >> 4) * 8;
-          const int ch = kk * 2 + ((lane >> 3) & 1);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(smem_u32(sK) + swz(key, ch), b0, b1, b2, b3);
-          mma16816(s[2 * np], qf[kk], b0, b1);
-          mma16816(s[2 * np + 1], qf[kk], b2, b3);
-        }
-      }
-      // 64-key visibility of this thread's two rows: the key range, and for
-      // the step block the rows' structured-mask words; pre-shifted by the
-      // lane's column so the per-element bit index is a constant
-      const int kbase = k_begin + t * kKeyTile;
-      const int nvalid = min(kKeyTile, k_end - kbase);
-      unsigned long long vm0 = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull), vm1 = vm0;
-      if (step_unit) {
-        const uint32_t* w0 = sMask + qrow0 * 4 + 2 * t;
-        const uint32_t* w1 = sMask + (qrow0 + 8) * 4 + 2 * t;
-        vm0 &= ((unsigned long long)w0[1] << 32) | w0[0];
-        vm1 &= ((unsigned long long)w1[1] << 32) | w1[0];
-      }
-      vm0 >>= (lane & 3) * 2;
-      vm1 >>= (lane & 3) * 2;
-      float mx0 = m0, mx1 = m1;
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-#pragma unroll
-        for (int e2 = 0; e2 < 4; ++e2) {
-          const unsigned long long vm = (e2 >> 1) ? vm1 : vm0;
-          const bool vis = (vm >> (n * 8 + (e2 & 1))) & 1ull;
-          s[n][e2] = vis ? s[n][e2] * sl2 : -INFINITY;
-        }
-        mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
-        mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
-      }
-#pragma unroll
-      for (int off = 1; off <= 2; off <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-      }
-      const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
-      const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
-      m0 = mx0;
-      m1 = mx1;
-      float rs0 = 0.f, rs1 = 0.f;
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        s[n][0] = exp2f(s[n][0] - b0);
-        s[n][1] = exp2f(s[n][1] - b0);
-        s[n][2] = exp2f(s[n][2] - b1);
-        s[n][3] = exp2f(s[n][3] - b1);
-        rs0 += s[n][0] + s[n][1];
-        rs1 += s[n][2] + s[n][3];
-      }
-      l0 = l0 * al0 + rs0;
-      l1 = l1 * al1 + rs1;
-#pragma unroll
-      for (int dd = 0; dd < 16; ++dd) {
-        o[dd][0] *= al0; o[dd][1] *= al0; o[dd][2] *= al1; o[dd][3] *= al1;
-      }
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        uint32_t pa[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]), pack_bf16(s[2 * kk][2], s[2 * kk][3]),
-                          pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]),
-                          pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
-#pragma unroll
-        for (int dp = 0; dp < 8; ++dp) {
-          const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-          const int ch = dp * 2 + (lane >> 4);
-          uint32_t v0, v1, v2, v3;
-          ldsm_x4_t(smem_u32(sV) + swz(key, ch), v0, v1, v2, v3);
-          mma16816(o[2 * dp], pa, v0, v1);
-          mma16816(o[2 * dp + 1], pa, v2, v3);
-        }
+        const int col = kk * 16 + (lane & 3) * 2;
+        qf[kk][0] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
+        qf[kk][1] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
+        qf[kk][2] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
+        qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
       }
     }
-    __syncthreads();
-  }
-  cp_wait<0>();
-  stamp(a, 4);
 
-  // ---- chunk partial: unnormalised O and (m, l) in log2 units
-#pragma unroll
-  for (int off = 1; off <= 2; off <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
-  }
-  const size_t grp = (size_t)kvh * a.nrb_max + rb;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const int row = qrow0 + half * 8;
-    if (rb * 128 + row >= nq) continue;
-    float* dst = a.part_o + ((grp * (S + 1) + split) * 128 + row) * 128;
-#pragma unroll
-    for (int dd = 0; dd < 16; ++dd) {
-      const int col = dd * 8 + (lane & 3) * 2;
-      __stcg(reinterpret_cast<float2*>(dst + col), make_float2(o[dd][half * 2], o[dd][half * 2 + 1]));
+    float o[16][4];
+  #pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    const float sl2 = a.scale * kLog2e;
+    stamp(a, 2);
+    const bool warp_active = rb * 128 + warp * 16 < nq;
+
+    for (int t = 0; t < n_tiles; ++t) {
+      if (t + kStages - 1 < n_tiles) load_kv(t + kStages - 1);
+      cp_commit();
+      cp_wait<kStages - 1>();
+      __syncthreads();
+      if (t == 0) stamp(a, 3);
+      if (warp_active) {
+        const uint8_t* sK = sKV + (t % kStages) * kTileBytes;
+        const uint8_t* sV = sK + kKeyTile * 256;
+        float s[8][4];
+  #pragma unroll
+        for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+  #pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+  #pragma unroll
+          for (int np = 0; np < 4; ++np) {
+            const int key = np * 16 + (lane & 7) + (lane >> 4) * 8;
+            const int ch = kk * 2 + ((lane >> 3) & 1);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(smem_u32(sK) + swz(key, ch), b0, b1, b2, b3);
+            mma16816(s[2 * np], qf[kk], b0, b1);
+            mma16816(s[2 * np + 1], qf[kk], b2, b3);
+          }
+        }
+        // 64-key visibility of this thread's two rows: the key range, and for
+        // the step block the rows' structured-mask words; pre-shifted by the
+        // lane's column so the per-element bit index is a constant
+        const int kbase = k_begin + t * kKeyTile;
+        const int nvalid = min(kKeyTile, k_end - kbase);
+        unsigned long long vm0 = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull), vm1 = vm0;
+        if (step_unit) {
+          const uint32_t* w0 = sMask + qrow0 * 4 + 2 * t;
+          const uint32_t* w1 = sMask + (qrow0 + 8) * 4 + 2 * t;
+          vm0 &= ((unsigned long long)w0[1] << 32) | w0[0];
+          vm1 &= ((unsigned long long)w1[1] << 32) | w1[0];
+        }
+        vm0 >>= (lane & 3) * 2;
+        vm1 >>= (lane & 3) * 2;
+        float mx0 = m0, mx1 = m1;
+  #pragma unroll
+        for (int n = 0; n < 8; ++n) {
+  #pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const unsigned long long vm = (e2 >> 1) ? vm1 : vm0;
+            const bool vis = (vm >> (n * 8 + (e2 & 1))) & 1ull;
+            s[n][e2] = vis ? s[n][e2] * sl2 : -INFINITY;
+          }
+          mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
+          mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
+        }
+  #pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
+        const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
+        m0 = mx0;
+        m1 = mx1;
+        float rs0 = 0.f, rs1 = 0.f;
+  #pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          s[n][0] = exp2f(s[n][0] - b0);
+          s[n][1] = exp2f(s[n][1] - b0);
+          s[n][2] = exp2f(s[n][2] - b1);
+          s[n][3] = exp2f(s[n][3] - b1);
+          rs0 += s[n][0] + s[n][1];
+          rs1 += s[n][2] + s[n][3];
+        }
+        l0 = l0 * al0 + rs0;
+        l1 = l1 * al1 + rs1;
+  #pragma unroll
+        for (int dd = 0; dd < 16; ++dd) {
+          o[dd][0] *= al0; o[dd][1] *= al0; o[dd][2] *= al1; o[dd][3] *= al1;
+        }
+  #pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          uint32_t pa[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]), pack_bf16(s[2 * kk][2], s[2 * kk][3]),
+                            pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                            pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+  #pragma unroll
+          for (int dp = 0; dp < 8; ++dp) {
+            const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+            const int ch = dp * 2 + (lane >> 4);
+            uint32_t v0, v1, v2, v3;
+            ldsm_x4_t(smem_u32(sV) + swz(key, ch), v0, v1, v2, v3);
+            mma16816(o[2 * dp], pa, v0, v1);
+            mma16816(o[2 * dp + 1], pa, v2, v3);
+          }
+        }
+      }
+      __syncthreads();
     }
-    if ((lane & 3) == 0)
-      __stcg(a.part_ml + (grp * (S + 1) + split) * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
+    cp_wait<0>();
+    stamp(a, 4);
+
+    // ---- chunk partial: unnormalised O and (m, l) in log2 units
+  #pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+  #pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int row = qrow0 + half * 8;
+      if (rb * 128 + row >= nq) continue;
+      float* dst = a.part_o + ((grp * (S + 1) + split) * 128 + row) * 128;
+  #pragma unroll
+      for (int dd = 0; dd < 16; ++dd) {
+        const int col = dd * 8 + (lane & 3) * 2;
+        __stcg(reinterpret_cast<float2*>(dst + col), make_float2(o[dd][half * 2], o[dd][half * 2 + 1]));
+      }
+      if ((lane & 3) == 0)
+        __stcg(a.part_ml + (grp * (S + 1) + split) * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
+    }
   }
   __syncthreads();
   // arrival of this chunk.  Counters only grow: an active group gains exactly

@@ -673,8 +673,13 @@ int llama_read_trace(la_engine* e, void* host, size_t bytes);
 bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes);
 
 // ------------------------------------------------------------ debug copy
+extern void* g_attn_trace_host;
 extern "C" int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t bytes) {
   if (!e || !host) { la_set_error("null engine or buffer"); return LA_ERR_INVALID_CONFIG; }
+  if (what == 19) {   // host address of the mapped attention trace (no device sync: usable on a hang)
+    *reinterpret_cast<void**>(host) = g_attn_trace_host;
+    return LA_OK;
+  }
   CK(cudaSetDevice(e->device));
   CK(cudaDeviceSynchronize());
   const void* src = nullptr;

@@ -197,6 +197,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::bulk_load(sA + i * a_stage, a_src(u_begin + i), a_bytes, &full[i], pol_w);
     }
   }
+  if (warp == 0 && lane == 0 && args.l2pf > 0) {
+    // keep HBM streaming while the previous kernel finishes: the units just
+    // beyond the smem ring go to L2 (a cache hint, always safe)
+    for (long u = u_begin + n_pre; u < min(u_end, u_begin + n_pre + args.l2pf); ++u)
+      ptx::bulk_prefetch_l2(a_src(u), a_bytes);
+  }
   la_pdl_wait();
   if (args.timing && threadIdx.x == 0) {
     if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();

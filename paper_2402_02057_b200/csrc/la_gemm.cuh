@@ -47,6 +47,7 @@ struct LaGemmArgs {
   // optional per-CTA trace [gridDim][4]: start, prologue done, MMA done, end
   unsigned long long* trace;
   int debug;   // experiments: bit0 skip step-row loads, bit1 skip MMAs
+  int l2pf;    // units beyond the smem ring prefetched to L2 before the dependency wait
   // ---- fused epilogue (LA_EPI_QKV / SWIGLU / LOGITS): stream-K fix-up in
   // the GEMM -- the CTA owning a tile's k = 0 piece adds the other pieces'
   // partials (in piece order) and applies the epilogue

@@ -149,6 +149,8 @@ static int lalloc(la_engine* e, T** p, size_t n) {
 
 static void tl_install(la_engine* e);   // LA_TIMELINE profiling hook (below)
 
+void* g_attn_trace_host = nullptr;   // LA_ATTN_TRACE=2 debug buffer (host view)
+
 // ------------------------------------------------ persistent forward kernel
 static int mega_create(la_engine* e) {
   LlamaPath* p = e->llama;
@@ -332,8 +334,10 @@ int llama_create(la_engine* e) {
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
   if (trace) RET_IF(lalloc(e, &p->trace, 5 * 256 * 4));   // qkv, o, gu, head, down
   const int dbg = getenv("LA_GEMM_DEBUG") ? atoi(getenv("LA_GEMM_DEBUG")) : 0;
+  const int l2pf = getenv("LA_GEMM_L2PF") ? atoi(getenv("LA_GEMM_L2PF")) : 0;
   auto fin = [&](LaGemm& gg, int kind, int tkind) {
     gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.debug = dbg; gg.args.counters = counters;
+    gg.args.l2pf = l2pf;
     gg.args.timing = p->timing + 8 * kind;
     gg.args.trace = trace ? p->trace + 256 * 4 * tkind : nullptr;
   };
@@ -370,6 +374,11 @@ int llama_create(la_engine* e) {
     // wide kernel, more than the saved dependency hop.
     af.fuse_qkv = af.spread_merge && !p->fused && getenv("LA_ATTN_FUSE_QKV") && atoi(getenv("LA_ATTN_FUSE_QKV")) == 1;
     RET_IF(lalloc(e, &af.gbar, 1));
+    // tcgen05 chunk attention (LA_ATTN_TC=1): correct (same outputs as the
+    // mma.sync path on the parity tests) but measured slower on cfg2 -- its
+    // S -> softmax -> PV phases serialise (no cross-tile pipelining yet)
+    af.tc = getenv("LA_ATTN_TC") && atoi(getenv("LA_ATTN_TC")) == 1;
+    af.dbg = getenv("LA_ATTN_DBG") ? atoi(getenv("LA_ATTN_DBG")) : 0;
     af.scale = 1.0f / sqrtf(128.0f);
     af.q = p->q;
     af.out = p->attn;
@@ -377,7 +386,18 @@ int llama_create(la_engine* e) {
     RET_IF(lalloc(e, &af.part_o, groups * units * 128 * 128));
     RET_IF(lalloc(e, &af.part_ml, groups * units * 128));
     RET_IF(lalloc(e, &af.cnt, groups));
-    if (getenv("LA_ATTN_TRACE")) RET_IF(lalloc(e, &af.trace, groups * units * 8));
+    if (getenv("LA_ATTN_TRACE")) {
+      if (atoi(getenv("LA_ATTN_TRACE")) == 2) {
+        // mapped host memory: readable by a host watchdog while a kernel hangs
+        void* hp = nullptr;
+        CK(cudaHostAlloc(&hp, groups * units * 64, cudaHostAllocMapped));
+        memset(hp, 0, groups * units * 64);
+        g_attn_trace_host = hp;
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&af.trace), hp, 0));
+      } else {
+        RET_IF(lalloc(e, &af.trace, groups * units * 8));
+      }
+    }
     ce = cudaFuncSetAttribute(la_attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)la_attn_fused_smem());
     if (ce != cudaSuccess) { la_set_error("fused attn smem attr: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
