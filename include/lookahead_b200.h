@@ -30,6 +30,8 @@ extern "C" {
 #define LA_ERR_NCCL (-4)
 #define LA_ERR_CAPACITY (-5) /* a device-side table or buffer would overflow */
 #define LA_ERR_UNSUPPORTED (-6)
+#define LA_ERR_DEGENERATE (-7) /* DegenerateDistributionError: types.py, sampling.py:52-65,
+                                  verification.py:108-110 */
 
 /* Thread-local description of the last error on this thread. */
 const char* la_last_error(void);
@@ -117,6 +119,51 @@ int32_t la_decode_lookahead(la_engine* e, const la_gen_config* cfg, la_decode_io
 /* decode_autoregressive (decoding.py:96-116), greedy. */
 int32_t la_decode_autoregressive(la_engine* e, int32_t max_tokens, int32_t eos_token,
                                  la_decode_io* io, void* stream);
+
+/* ------------------------------------------------------ temperature sampler
+ * SamplerSpec(mode="temperature") (types.py:43-67): p ** (1/T), top-k, top-p
+ * (sampling.py:22-66), distribution-preserving verification
+ * (verification.py:74-118).  The random stream is the session's numpy
+ * default_rng(seed) (PCG64): the caller draws the initial window exactly like
+ * start_session (decoding.py:83-84, window_init layout.py:117-125) into
+ * io->rng_stream / rng_len = (N-1)W-1 cells and passes the generator state
+ * AFTER those draws -- rng.bit_generator.state's 128-bit `state` and `inc`
+ * as hi/lo words, `has_uint32`, `uinteger`.  The device then consumes the
+ * identical stream: one random() per verification trial and draw, one
+ * integers(0, V) per vacated window cell. */
+typedef struct la_sampler {
+  double temperature;        /* > 0 */
+  int32_t top_k;             /* 0: none */
+  double top_p;              /* (0, 1]; 1: none */
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+  int32_t has_uint32;
+  uint32_t uinteger;
+} la_sampler;
+
+/* decode_lookahead (decoding.py:235-255) under a temperature sampler. */
+int32_t la_decode_lookahead_sampled(la_engine* e, const la_gen_config* cfg, const la_sampler* s,
+                                    la_decode_io* io, void* stream);
+
+/* decode_autoregressive (decoding.py:96-116) under a temperature sampler:
+ * one random() per token (sample_token, sampling.py:77-85); the generator
+ * is default_rng(seed) untouched (io->rng_stream unused). */
+int32_t la_decode_autoregressive_sampled(la_engine* e, int32_t max_tokens, int32_t eos_token,
+                                         const la_sampler* s, la_decode_io* io, void* stream);
+
+/* Parity hooks (tests only).  la_adjust_distributions: adjusted_distribution
+ * of n_rows fp64 probability rows [n_rows][V] on the device (host buffers;
+ * out may alias probs).  la_verify_sample_dists: verify_sample of c
+ * candidates (suffixes [c][S]) over fp64 distributions
+ * [1 + c*S][V] = base, then candidate b's S rows; out[<= S+1] accepted. */
+int32_t la_adjust_distributions(la_engine* e, const double* probs, int32_t n_rows, int32_t V,
+                                const la_sampler* s, double* out, void* stream);
+int32_t la_verify_sample_dists(la_engine* e, const double* dists, int32_t V, int32_t S,
+                               int32_t c, const int32_t* suffixes, const la_sampler* s,
+                               int32_t* out, int32_t* n_out, void* stream);
+
+/* The generator as the device advances it, evaluated on the HOST (no GPU):
+ * kind 0 random(), kind 1 integers(0, high); writes n values. */
+int32_t la_pcg64_draws(const la_sampler* s, int32_t kind, int32_t high, int32_t n, double* out);
 
 /* ModelInterface.forward parity hook (models.py:80-89): logits of n_rows
  * queries after `prefix`.  Row i has token ids[i], relative position rel[i]

@@ -287,6 +287,77 @@ def gen_jacobi(la):
     _dump("jacobi.json", {"source": "decoding.decode_jacobi (decoding.py:119-149)", "cases": cases})
 
 
+def gen_sampling(la):
+    """Temperature sampler: adjusted distributions (sampling.py:22-66),
+    verify_sample (verification.py:74-118) and whole sampled decodes
+    (decoding.py:96-116,160-204) on the config-1 TinyTransformer."""
+    from lookahead.sampling import adjusted_distribution
+    from lookahead.verification import verify_sample
+    rng = np.random.default_rng(77)
+    adjust = []
+    for i in range(60):
+        V = int(rng.integers(2, 40))
+        p = rng.random(V) ** 3
+        if i % 4 == 1:                       # ties: quantised probabilities
+            p = np.round(p * 4) / 4 + 1e-3
+        if i % 7 == 3:                       # zeros
+            p[rng.integers(0, V, size=max(1, V // 3))] = 0.0
+        p = p / p.sum()
+        T = [1.0, 0.5, 0.7, 1.5, 2.0][i % 5]
+        k = [None, 1, 2, 5, 17, 100][i % 6]
+        tp = [None, 0.9, 0.5, 0.99, 0.01, 1.0, 0.3][i % 7]
+        spec = la.SamplerSpec(mode="temperature", temperature=T, top_k=k, top_p=tp, seed=0)
+        adjust.append({"probs": p.tolist(), "T": T, "top_k": k, "top_p": tp,
+                       "out": adjusted_distribution(p, spec).tolist()})
+    verify = []
+    for i in range(120):
+        V = int(rng.integers(2, 7))
+        S = int(rng.integers(1, 5))
+        c = int(rng.integers(0, 6))
+
+        def dist():
+            q = rng.random(V) ** 2
+            if rng.random() < 0.2:
+                q[int(rng.integers(0, V))] = 0.0
+            q[int(rng.integers(0, V))] += 0.05
+            return q / q.sum()
+
+        base = dist()
+        cands = []
+        for _ in range(c):
+            suf = [int(t) for t in rng.integers(0, V, size=S)]
+            cands.append((tuple(suf), [base] + [dist() for _ in range(S)]))
+        seed = 1000 + i
+        acc = verify_sample(base, cands, np.random.default_rng(seed))
+        verify.append({"V": V, "base": base.tolist(), "seed": seed,
+                       "cands": [[list(s), [d.tolist() for d in ds]] for s, ds in cands],
+                       "accepted": acc})
+    decode = []
+    model = la.transformer_init(seed=0, vocab_size=256, d_model=16, n_layers=2, n_heads=2)
+    prompt = [int(t) for t in np.random.default_rng(1234).integers(0, 256, 32)]
+    for j, (T, k, tp) in enumerate([(1.0, None, None), (0.7, None, None), (0.5, 20, None),
+                                    (1.0, None, 0.9), (0.8, 50, 0.95), (1.3, None, None)]):
+        spec = la.SamplerSpec(mode="temperature", temperature=T, top_k=k, top_p=tp, seed=j)
+        for W, N, G in [(5, 3, 5), (15, 5, 15), (1, 2, 0)]:
+            cfg = la.GenerationConfig(window=W, ngram=N, max_candidates=G, max_tokens=48)
+            toks, metrics = la.decode_lookahead(model, prompt, cfg, spec)
+            out, steps = _trace_decode(la, model, prompt, cfg, spec)
+            assert out == toks
+            decode.append({"prompt": prompt, "W": W, "N": N, "G": G, "max_tokens": 48,
+                           "T": T, "top_k": k, "top_p": tp, "seed": j, "tokens": toks,
+                           "metrics": _metrics(metrics), "steps": steps})
+    ar = []
+    for j, (T, k, tp) in enumerate([(1.0, None, None), (0.6, 10, 0.9), (2.0, None, 0.8)]):
+        spec = la.SamplerSpec(mode="temperature", temperature=T, top_k=k, top_p=tp, seed=40 + j)
+        ar.append({"prompt": prompt, "T": T, "top_k": k, "top_p": tp, "seed": 40 + j,
+                   "max_tokens": 64, "tokens": la.decode_autoregressive(model, prompt, spec, 64)})
+    _dump("sampling.json", {"source": "sampling.adjusted_distribution, verification.verify_sample, "
+                                      "decoding.decode_lookahead / decode_autoregressive "
+                                      "(temperature SamplerSpec)",
+                            "model": [0, 256], "adjust": adjust, "verify": verify,
+                            "decode": decode, "ar": ar})
+
+
 def main():
     la = _ref()
     if len(sys.argv) > 1:   # regenerate selected fixtures only, e.g. `make_golden.py jacobi`
@@ -302,6 +373,7 @@ def main():
     gen_lp(la)
     gen_decode(la)
     gen_jacobi(la)
+    gen_sampling(la)
     print("golden vectors written to", OUT)
 
 

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-from .types import LayoutError
+from .types import DegenerateDistributionError, LayoutError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "liblookahead_b200.so"
 
@@ -22,6 +22,7 @@ LA_ERR_CUDA = -3
 LA_ERR_NCCL = -4
 LA_ERR_CAPACITY = -5
 LA_ERR_UNSUPPORTED = -6
+LA_ERR_DEGENERATE = -7
 
 ARCH_GPT_F32 = 0
 ARCH_LLAMA_F32 = 1
@@ -33,7 +34,8 @@ EXPORTS = (
     "la_destroy", "la_decode_lookahead", "la_decode_autoregressive", "la_forward_layout",
     "la_lp_unique_id", "la_lp_init", "la_decode_lookahead_group", "la_debug_read",
     "la_gemm_timing_reset", "la_gemm_timing_read", "la_forward_timing_read", "la_packed_bytes",
-    "la_decode_jacobi",
+    "la_decode_jacobi", "la_decode_lookahead_sampled", "la_decode_autoregressive_sampled",
+    "la_adjust_distributions", "la_verify_sample_dists", "la_pcg64_draws",
     "la_pack_weight",
 )
 
@@ -56,6 +58,25 @@ class la_gen_config(C.Structure):
 
 
 _P32 = C.POINTER(C.c_int32)
+
+
+class la_sampler(C.Structure):
+    _fields_ = [("temperature", C.c_double), ("top_k", C.c_int32), ("top_p", C.c_double),
+                ("state_hi", C.c_uint64), ("state_lo", C.c_uint64), ("inc_hi", C.c_uint64),
+                ("inc_lo", C.c_uint64), ("has_uint32", C.c_int32), ("uinteger", C.c_uint32)]
+
+
+def make_sampler(temperature: float, top_k, top_p, rng) -> la_sampler:
+    """la_sampler from a SamplerSpec's knobs and a numpy Generator (PCG64) in
+    its current state."""
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValueError("the device generator restates numpy's PCG64 (default_rng)")
+    m64 = (1 << 64) - 1
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    return la_sampler(float(temperature), 0 if top_k is None else int(top_k),
+                      1.0 if top_p is None else float(top_p), s >> 64, s & m64, inc >> 64,
+                      inc & m64, int(st["has_uint32"]), int(st["uinteger"]))
 
 
 class la_decode_io(C.Structure):
@@ -107,6 +128,16 @@ def load(path: str | os.PathLike | None = None):
     lib.la_packed_bytes.restype = C.c_int64
     lib.la_pack_weight.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                    C.c_int32, C.c_void_p]
+    SP = C.POINTER(la_sampler)
+    lib.la_decode_lookahead_sampled.argtypes = [C.c_void_p, C.POINTER(la_gen_config), SP,
+                                                C.POINTER(la_decode_io), C.c_void_p]
+    lib.la_decode_autoregressive_sampled.argtypes = [C.c_void_p, C.c_int32, C.c_int32, SP,
+                                                     C.POINTER(la_decode_io), C.c_void_p]
+    lib.la_adjust_distributions.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, SP,
+                                            C.c_void_p, C.c_void_p]
+    lib.la_verify_sample_dists.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                           C.c_int32, _P32, SP, _P32, _P32, C.c_void_p]
+    lib.la_pcg64_draws.argtypes = [SP, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
     lib.la_gemm_timing_reset.argtypes = [C.c_void_p]
     lib.la_gemm_timing_read.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     for name in EXPORTS:
@@ -128,6 +159,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == LA_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == LA_ERR_DEGENERATE:
+        raise DegenerateDistributionError(msg)
     if rc == LA_ERR_CAPACITY:
         raise ValueError(f"capacity: {msg}")
     raise CudaEngineError(f"engine error {rc}: {msg}")

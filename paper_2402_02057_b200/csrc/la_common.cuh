@@ -77,6 +77,14 @@ struct LaRowNorm {
 // ----------------------------------------------------------- decode state
 enum { LA_MODE_LOOKAHEAD = 0, LA_MODE_AUTOREGRESSIVE = 1 };
 
+// numpy PCG64 bit-generator state (128-bit LCG + the buffered upper half that
+// next_uint32 hands out on its second call); la_sample.cuh advances it
+struct LaPcg64 {
+  unsigned long long s_hi, s_lo, i_hi, i_lo;
+  int has32;
+  unsigned u32;
+};
+
 struct DevDecode {
   // configuration (GenerationConfig, types.py:70-97)
   int mode, W, N, G, V, max_tokens, eos;   // eos < 0: none
@@ -104,6 +112,17 @@ struct DevDecode {
   int* amax;      // [LA_MAX_ROWS] argmax per *global* row (-1 = not computed here)
   int* accepted;  // [N]
   DevPool pool;
+  // temperature sampler (SamplerSpec, types.py:43-67; sampling.py:22-85);
+  // sample == 0: greedy and none of the fields below is read
+  int sample;
+  int top_k;            // 0: no top-k
+  double temperature;   // p ** (1/T) unless T == 1
+  double top_p;         // >= 1: no nucleus
+  LaPcg64 pcg;          // the session generator after window_init
+  int degenerate;       // DegenerateDistributionError raised on the device
+  const float* logits;  // [LA_MAX_ROWS][V] this step's rows (global row order)
+  double* adj;          // [1 + G(N-1)][V]: row 0, then branch b offset k at 1 + b(N-1) + k-1
+  double* work;         // [V] verification's renormalised distribution
 };
 
 // ---------------------------------------------------------------- utils

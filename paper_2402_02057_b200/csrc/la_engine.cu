@@ -11,6 +11,7 @@
 
 #include "la_engine.h"
 #include "la_kernels.h"
+#include "la_sample.cuh"
 
 static thread_local char g_err[2048];
 
@@ -271,7 +272,33 @@ extern "C" int32_t la_destroy(la_engine* e) {
 struct DecodeArgs {
   int mode;
   int W, N, G, max_tokens, eos, seed_pool;
+  const la_sampler* smp = nullptr;   // temperature sampler (null: greedy)
 };
+
+// SamplerSpec.__post_init__ (types.py:59-67)
+static int validate_sampler(const la_sampler* s) {
+  if (!(s->temperature > 0.0)) { la_set_error("temperature must be positive"); return LA_ERR_INVALID_CONFIG; }
+  if (s->top_k < 0) { la_set_error("top_k must be a positive integer"); return LA_ERR_INVALID_CONFIG; }
+  if (!(s->top_p > 0.0 && s->top_p <= 1.0)) { la_set_error("top_p must lie in (0, 1]"); return LA_ERR_INVALID_CONFIG; }
+  return LA_OK;
+}
+
+static LaPcg64 pcg_of(const la_sampler* s) {
+  LaPcg64 g;
+  g.s_hi = s->state_hi; g.s_lo = s->state_lo; g.i_hi = s->inc_hi; g.i_lo = s->inc_lo;
+  g.has32 = s->has_uint32 ? 1 : 0; g.u32 = s->uinteger;
+  return g;
+}
+
+// sampler buffers: logits of every step row, adjusted rows, working row
+static int sampler_buffers(la_engine* e, int adj_rows) {
+  const size_t V = (size_t)e->desc.vocab;
+  RET_IF(dgrow(e, &e->d_logits, &e->logits_cap, (size_t)LA_MAX_ROWS * V));
+  RET_IF(dgrow(e, &e->d_adj, &e->adj_cap, (size_t)adj_rows * V));
+  RET_IF(dgrow(e, &e->d_work, &e->work_cap, V));
+  RET_IF(dgrow(e, &e->d_flag, &e->flag_cap, (size_t)LA_MAX_ROWS));
+  return LA_OK;
+}
 
 static int validate_gen(const la_engine* e, const DecodeArgs& a, const la_decode_io* io) {
   if (!io || !io->prompt || io->n_prompt < 1) { la_set_error("prompt must be nonempty"); return LA_ERR_INVALID_CONFIG; }
@@ -290,6 +317,13 @@ static int validate_gen(const la_engine* e, const DecodeArgs& a, const la_decode
       return LA_ERR_UNSUPPORTED;
     }
     if (a.W + a.N - 2 >= LA_MAX_CHAIN) { la_set_error("chain too long"); return LA_ERR_UNSUPPORTED; }
+  }
+  if (a.smp) {
+    RET_IF(validate_sampler(a.smp));
+    if (e->world > 1) {
+      la_set_error("lookahead parallelism exchanges argmax ids only: temperature sampling is single-replica");
+      return LA_ERR_UNSUPPORTED;
+    }
   }
   long need = (long)io->n_prompt + a.max_tokens + LA_MAX_NGRAM;
   if (need > e->desc.max_context) {
@@ -379,6 +413,15 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
   d.pool.log_cap = (int)e->p_log_cap;
   d.pool.lead_keys = e->p_lead; d.pool.bkt_cnt = e->p_cnt; d.pool.bkt_suf = e->p_suf;
   d.pool.set_keys = e->p_set; d.pool.counters = e->p_counters; d.pool.log = e->p_log;
+  if (a.smp) {
+    RET_IF(sampler_buffers(e, a.mode == LA_MODE_LOOKAHEAD ? 1 + d.G * (N - 1) : 1));
+    d.sample = 1;
+    d.temperature = a.smp->temperature;
+    d.top_k = a.smp->top_k;
+    d.top_p = a.smp->top_p;
+    d.pcg = pcg_of(a.smp);
+    d.logits = e->d_logits; d.adj = e->d_adj; d.work = e->d_work;
+  }
   CK(cudaMemcpyAsync(e->d_dec, &d, sizeof(d), cudaMemcpyHostToDevice, st));
   if (!grams.empty()) {
     la_pool_seed_kernel<<<1, 32, 0, st>>>(e->d_dec, e->d_grams, (int)(grams.size() / N), (int)n_init);
@@ -404,6 +447,7 @@ static int readback(la_engine* e, la_decode_io* io, cudaStream_t st) {
   CK(cudaMemcpyAsync(counters, e->p_counters, sizeof(counters), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (d.overflow) { la_set_error("device capacity exceeded (pool table, log or RNG stream)"); return LA_ERR_CAPACITY; }
+  if (d.degenerate) { la_set_error("all probability mass truncated away (degenerate distribution)"); return LA_ERR_DEGENERATE; }
   if (!e->is_tiny() && llama_mega_error(e)) {
     la_set_error("persistent forward kernel: dependency wait timed out (engine state is invalid)");
     return LA_ERR_CUDA;
@@ -448,7 +492,8 @@ static int run_decode(la_engine* e, const DecodeArgs& a, la_decode_io* io, void*
   if (e->world > 1) {
     RET_IF(lp_decode_loop(e, st, &launches));
   } else if (e->is_tiny()) {
-    la_tiny_decode<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_dec);
+    la_tiny_decode<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_dec,
+                                       e->h_dec.sample ? e->d_logits : nullptr);
     CK(cudaGetLastError());
     launches = 1;
   } else {
@@ -476,6 +521,87 @@ extern "C" int32_t la_decode_autoregressive(la_engine* e, int32_t max_tokens, in
   if (!e) { la_set_error("null engine"); return LA_ERR_INVALID_CONFIG; }
   DecodeArgs a{LA_MODE_AUTOREGRESSIVE, 1, 2, 0, max_tokens, eos_token < 0 ? -1 : eos_token, 0};
   return run_decode(e, a, io, stream);
+}
+
+extern "C" int32_t la_decode_lookahead_sampled(la_engine* e, const la_gen_config* cfg,
+                                               const la_sampler* s, la_decode_io* io, void* stream) {
+  if (!e || !cfg || !s) { la_set_error("null engine, config or sampler"); return LA_ERR_INVALID_CONFIG; }
+  DecodeArgs a{LA_MODE_LOOKAHEAD, cfg->window, cfg->ngram, cfg->max_candidates,
+               cfg->max_tokens, cfg->eos_token < 0 ? -1 : cfg->eos_token,
+               cfg->seed_pool_from_prompt, s};
+  return run_decode(e, a, io, stream);
+}
+
+extern "C" int32_t la_decode_autoregressive_sampled(la_engine* e, int32_t max_tokens,
+                                                    int32_t eos_token, const la_sampler* s,
+                                                    la_decode_io* io, void* stream) {
+  if (!e || !s) { la_set_error("null engine or sampler"); return LA_ERR_INVALID_CONFIG; }
+  DecodeArgs a{LA_MODE_AUTOREGRESSIVE, 1, 2, 0, max_tokens, eos_token < 0 ? -1 : eos_token, 0, s};
+  return run_decode(e, a, io, stream);
+}
+
+// ---------------------------------------------------------- sampler hooks
+extern "C" int32_t la_adjust_distributions(la_engine* e, const double* probs, int32_t n_rows,
+                                           int32_t V, const la_sampler* s, double* out,
+                                           void* stream) {
+  if (!e || !probs || !out || !s || n_rows < 1 || V < 1) { la_set_error("bad arguments"); return LA_ERR_INVALID_CONFIG; }
+  RET_IF(validate_sampler(s));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  RET_IF(dgrow(e, &e->d_adj, &e->adj_cap, (size_t)n_rows * V));
+  RET_IF(dgrow(e, &e->d_flag, &e->flag_cap, (size_t)n_rows));
+  CK(cudaMemcpyAsync(e->d_adj, probs, (size_t)n_rows * V * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(e->d_flag, 0, (size_t)n_rows * 4, st));
+  la_adjust_probs_kernel<<<n_rows, 1024, 0, st>>>(e->d_adj, V, s->temperature, s->top_k, s->top_p,
+                                                  e->d_flag);
+  CK(cudaGetLastError());
+  std::vector<int> flags(n_rows);
+  CK(cudaMemcpyAsync(out, e->d_adj, (size_t)n_rows * V * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(flags.data(), e->d_flag, (size_t)n_rows * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int f : flags)
+    if (f) { la_set_error("all probability mass truncated away"); return LA_ERR_DEGENERATE; }
+  return LA_OK;
+}
+
+extern "C" int32_t la_verify_sample_dists(la_engine* e, const double* dists, int32_t V, int32_t S,
+                                          int32_t c, const int32_t* suffixes, const la_sampler* s,
+                                          int32_t* out, int32_t* n_out, void* stream) {
+  if (!e || !dists || !s || !out || !n_out || V < 1 || S < 1 || S > LA_MAX_SUFFIX || c < 0 ||
+      c > 32 || (c > 0 && !suffixes)) {
+    la_set_error("bad arguments (S <= %d, c <= 32)", LA_MAX_SUFFIX);
+    return LA_ERR_INVALID_CONFIG;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  const size_t rows = 1 + (size_t)c * S;
+  RET_IF(dgrow(e, &e->d_adj, &e->adj_cap, rows * V));
+  RET_IF(dgrow(e, &e->d_work, &e->work_cap, (size_t)V));
+  CK(cudaMemcpyAsync(e->d_adj, dists, rows * V * 8, cudaMemcpyHostToDevice, st));
+  if (c) CK(cudaMemcpyAsync(e->d_cand, suffixes, (size_t)c * S * 4, cudaMemcpyHostToDevice, st));
+  DevDecode d;
+  memset(&d, 0, sizeof(d));
+  d.mode = LA_MODE_LOOKAHEAD; d.N = S + 1; d.W = 1; d.V = V; d.c = c;
+  d.cand = e->d_cand; d.accepted = e->d_acc; d.adj = e->d_adj; d.work = e->d_work;
+  d.sample = 1; d.pcg = pcg_of(s); d.winner = -1;
+  CK(cudaMemcpyAsync(e->d_dec, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+  la_verify_hook_kernel<<<1, 1024, 0, st>>>(e->d_dec);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&d, e->d_dec, sizeof(d), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (d.degenerate) { la_set_error("verification renormalized to zero mass"); return LA_ERR_DEGENERATE; }
+  CK(cudaMemcpy(out, e->d_acc, (size_t)d.k * 4, cudaMemcpyDeviceToHost));
+  *n_out = d.k;
+  return LA_OK;
+}
+
+extern "C" int32_t la_pcg64_draws(const la_sampler* s, int32_t kind, int32_t high, int32_t n,
+                                  double* out) {
+  if (!s || !out || n < 0 || (kind == 1 && high < 1)) { la_set_error("bad arguments"); return LA_ERR_INVALID_CONFIG; }
+  LaPcg64 g = pcg_of(s);
+  for (int i = 0; i < n; ++i)
+    out[i] = kind == 0 ? la_pcg_random(g) : (double)la_pcg_integers(g, (unsigned)high);
+  return LA_OK;
 }
 
 // ------------------------------------------------------------- parity hook

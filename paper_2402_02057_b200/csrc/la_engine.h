@@ -29,6 +29,11 @@ struct la_engine {
   int *d_tokens = nullptr; int tokens_cap = 0;
   int *d_grams = nullptr; int grams_cap = 0;
   int out_cap = 0, rec_cap = 0;
+  // temperature sampler buffers (grown on demand)
+  float* d_logits = nullptr; int logits_cap = 0;   // [LA_MAX_ROWS][V]
+  double* d_adj = nullptr; int adj_cap = 0;        // [rows][V]
+  double* d_work = nullptr; int work_cap = 0;      // [V]
+  int* d_flag = nullptr; int flag_cap = 0;
   // pool arrays (grown on demand)
   int *p_lead = nullptr, *p_cnt = nullptr, *p_suf = nullptr, *p_set = nullptr;
   int *p_counters = nullptr, *p_log = nullptr;

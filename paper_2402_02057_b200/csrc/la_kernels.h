@@ -14,3 +14,8 @@ __global__ void la_kv_pack_kernel(const DevDecode* dp, const uint8_t* kc, const 
 __global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered, size_t seg,
                                     uint8_t* kc, uint8_t* vc, int layers, int slots,
                                     int row_bytes);
+__global__ void la_sample_adjust_kernel(DevDecode* dp);
+__global__ void la_sample_verify_kernel(DevDecode* dp);
+__global__ void la_adjust_probs_kernel(double* rows, int V, double temperature, int top_k,
+                                       double top_p, int* degenerate);
+__global__ void la_verify_hook_kernel(DevDecode* dp);

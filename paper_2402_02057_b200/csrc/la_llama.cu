@@ -57,6 +57,7 @@ struct LlamaPath {
   LaGemm head{};
   int head_tiles = 0;
   int kernels_per_step = 0;
+  int loop_key = 0;                       // sampler shape the loop graph was built for
   bool pdl = true;                        // programmatic dependent launch (LA_PDL=0: off)
   bool fused = false;                     // GEMM-fused epilogues (LA_FUSED_EPI=1)
   int attn_rows = 64;                     // query rows per attention CTA (LA_ATTN_ROWS)
@@ -482,6 +483,7 @@ void la_tl_set_attn(unsigned long long*);
 void la_tl_set_llama(unsigned long long*);
 void la_tl_set_state(unsigned long long*);
 void la_tl_set_mega(unsigned long long*);
+void la_tl_set_sample(unsigned long long*);
 static unsigned long long* g_tl_buf = nullptr;
 static void tl_install(la_engine* e) {
   if (!getenv("LA_TIMELINE") || g_tl_buf) return;
@@ -490,6 +492,7 @@ static void tl_install(la_engine* e) {
   cudaMemset(g_tl_buf, 0, (1 + 2 * LA_TL_CAP) * 8);
   la_tl_set_gemm(g_tl_buf); la_tl_set_reduce(g_tl_buf); la_tl_set_attnf(g_tl_buf); la_tl_set_attn(g_tl_buf);
   la_tl_set_llama(g_tl_buf); la_tl_set_state(g_tl_buf); la_tl_set_mega(g_tl_buf);
+  la_tl_set_sample(g_tl_buf);
 }
 
 // ------------------------------------------------------------- forward
@@ -711,11 +714,23 @@ static int record_step(la_engine* e, cudaStream_t st, bool finish, int* nk) {
   }
   CK(cudaGetLastError());
   *nk += 1;
-  if (p->mega) {
-    RET_IF(mega_forward(e, st, true, true, nk));
-  } else {
-    RET_IF(forward_layers(e, st, nk));
-    RET_IF(forward_head(e, st, true, nk));
+  // temperature sampler: the LM head also dumps every row's logits for the
+  // adjust kernel (one CTA per row verification may read), then one CTA
+  // runs verify_sample (la_sample.cu)
+  const bool smp = e->h_dec.sample != 0;
+  if (smp) p->logits = e->d_logits;
+  int rc = p->mega ? mega_forward(e, st, true, true, nk) : forward_layers(e, st, nk);
+  if (rc == LA_OK && !p->mega) rc = forward_head(e, st, true, nk);
+  if (smp) p->logits = nullptr;
+  RET_IF(rc);
+  if (finish && smp) {
+    const DevDecode& h = e->h_dec;
+    const int rows = h.mode == LA_MODE_LOOKAHEAD ? 1 + h.G * (h.N - 1) : 1;
+    KT_BEGIN(st);
+    CK(la_launch(la_sample_adjust_kernel, dim3(rows), dim3(1024), 0, st, p->pdl, e->d_dec));
+    CK(la_launch(la_sample_verify_kernel, dim3(1), dim3(1024), 0, st, p->pdl, e->d_dec));
+    KT_END(st, "sample_adjust+verify");
+    *nk += 2;
   }
   if (finish) {
     KT_BEGIN(st);
@@ -788,7 +803,17 @@ int llama_decode_loop(la_engine* e, cudaStream_t st, int* launches) {
   LlamaPath* p = e->llama;
   const char* mode = getenv("LA_LAUNCH_MODE");
   if (mode && !strcmp(mode, "eager")) return eager_loop(e, st, launches);
+  // the step graph differs per sampler shape: rebuild when it changes
+  const DevDecode& h = e->h_dec;
+  const int key = h.sample ? 1 + (h.mode == LA_MODE_LOOKAHEAD ? 1 + h.G * (h.N - 1) : 1) : 0;
+  if (p->loop_exec && p->loop_key != key) {
+    cudaGraphExecDestroy(p->loop_exec);
+    cudaGraphDestroy(p->loop_graph);
+    p->loop_exec = nullptr;
+    p->loop_graph = nullptr;
+  }
   if (!p->loop_exec) RET_IF(build_loop_graph(e));
+  p->loop_key = key;
   CK(cudaGraphLaunch(p->loop_exec, st));
   // kernels launched = per-step kernels x steps; the host learns the step
   // count only at readback, so report it there (engine->h_dec is refreshed)

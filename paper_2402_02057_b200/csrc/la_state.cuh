@@ -7,6 +7,7 @@
 // bookkeeping code.
 #pragma once
 #include "la_common.cuh"
+#include "la_sample.cuh"
 
 // ================================================================ pool
 __device__ __forceinline__ uint32_t la_gram_hash(const int* g, int n) {
@@ -253,14 +254,18 @@ static __device__ void la_step_finish(DevDecode& d) {
   __shared__ int s_oldwin[64 * LA_MAX_SUFFIX];
   __shared__ int s_acc[LA_MAX_SUFFIX + 2];
   const int tid = threadIdx.x, nth = blockDim.x;
-  if (tid == 0) s_done = d.done;
+  if (tid == 0) {
+    s_done = d.done;
+    if (!s_done && d.degenerate) s_done = d.done = 1;   // host raises DegenerateDistributionError
+  }
   __syncthreads();
   if (s_done) return;
   const int W = d.W, N = d.N, S = N - 1;
   if (d.mode == LA_MODE_AUTOREGRESSIVE) {
-    // decode_autoregressive (decoding.py:96-116)
+    // decode_autoregressive (decoding.py:96-116): argmax, or sample_token's
+    // draw made by la_verify_sample (sampling.py:77-85)
     if (tid == 0) {
-      int t = d.amax[0];
+      int t = d.sample ? d.accepted[0] : d.amax[0];
       d.out[d.n_out] = t;
       d.n_out += 1;
       d.ctx += 1;           // q0's K/V already sit at slot ctx
@@ -277,9 +282,14 @@ static __device__ void la_step_finish(DevDecode& d) {
   for (int f = tid; f < ncell; f += nth) s_oldwin[f] = d.window[f];
   __syncthreads();
   if (tid == 0) {
-    // verify_greedy (verification.py:43-71) on argmax ids
+    // verify_greedy (verification.py:43-71) on argmax ids; under a
+    // temperature sampler la_verify_sample already ran verify_sample
     int k = 0, win = -1;
-    if (c == 0) {
+    if (d.sample) {
+      k = d.k;
+      win = d.winner;
+      for (int i = 0; i < k; ++i) s_acc[i] = d.accepted[i];
+    } else if (c == 0) {
       s_acc[k++] = d.amax[0];
     } else {
       unsigned alive = (c >= 32) ? 0xffffffffu : ((1u << c) - 1u);
@@ -332,6 +342,8 @@ static __device__ void la_step_finish(DevDecode& d) {
     int val;
     if (sc <= W) {
       val = (level + 1 <= N - 2) ? s_oldwin[la_cell_index(level + 1, sc, W)] : s_newtop[sc - 1];
+    } else if (d.sample) {
+      continue;   // drawn below, in cell order, from the session generator
     } else {
       int idx = (level == 0) ? (col - max(2, W - sft + 1))
                              : v0 + (level - 1) * v1 + (col - max(1, W - sft + 1));
@@ -340,6 +352,17 @@ static __device__ void la_step_finish(DevDecode& d) {
       if (r >= d.rng_len) d.overflow = 1;
     }
     d.window[f] = val;
+  }
+  if (d.sample && tid == 0 && sft > 0) {
+    // rng.integers(0, V) per vacated cell, level-major / column-ascending
+    // (layout.py:243-250) -- f order is exactly that order
+    LaPcg64 g = d.pcg;
+    for (int f = 0; f < ncell; ++f) {
+      int level, col;
+      la_cell_level_col(f, W, level, col);
+      if (col + sft > W) d.window[f] = la_pcg_integers(g, (unsigned)d.V);
+    }
+    d.pcg = g;
   }
   __syncthreads();
   if (tid == 0) {

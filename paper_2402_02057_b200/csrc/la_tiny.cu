@@ -265,19 +265,32 @@ __global__ void __launch_bounds__(1024) la_tiny_prefill(TinyModel m, TinyScratch
 }
 
 // The decode loop: K1 build -> forward -> argmax -> K10 finish -> KV commit,
-// until done (EOS / max_tokens) -- entirely on the device.
+// until done (EOS / max_tokens) -- entirely on the device.  Under a
+// temperature sampler (logits != null) the step also adjusts row 0 and the
+// branch rows and runs verify_sample, in this CTA (la_sample.cuh).
 __global__ void __launch_bounds__(1024) la_tiny_decode(TinyModel m, TinyScratch s, FwdPlan* P,
-                                                      DevDecode* dp) {
+                                                      DevDecode* dp, float* logits) {
+  __shared__ LaSampleSmem sm;
   DevDecode& d = *dp;
   for (int it = 0; it < d.max_steps; ++it) {
     __syncthreads();
     if (d.done) break;
     la_step_build(d, *P);
     if (P->n_rows == 0) break;
-    forward_rows(m, s, *P, nullptr);
+    forward_rows(m, s, *P, d.sample ? logits : nullptr);
     for (int r = threadIdx.x; r < P->n_rows; r += blockDim.x)
       if (P->own[r]) d.amax[P->grow[r]] = s.row_amax[r];
     __syncthreads();
+    if (d.sample) {
+      const int nr = la_sample_rows(d);
+      bool ok = true;
+      for (int j = 0; j < nr && ok; ++j)
+        ok = la_adjust_row(logits + (size_t)la_sample_row(d, j) * m.V, m.V, d.temperature,
+                           d.top_k, d.top_p, d.adj + (size_t)j * m.V, sm);
+      if (ok) ok = la_verify_sample(d, sm);
+      if (!ok && threadIdx.x == 0) d.degenerate = 1;
+      __syncthreads();
+    }
     la_step_finish(d);
     if (d.mode == LA_MODE_LOOKAHEAD) commit_kv(m, d);
     __syncthreads();

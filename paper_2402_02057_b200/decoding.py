@@ -4,6 +4,13 @@
 caller pool once, runs every lookahead step on the GPU (device-resident
 window, n-gram pool, KV cache; no token returns to the host inside the
 loop), then reads the tokens, per-step records and pool log once.
+
+Both samplers of the reference run on the device.  Greedy: argmax ids, the
+window's random stream pre-generated on the host.  Temperature
+(``SamplerSpec(mode="temperature")``): the host draws only the initial window
+from ``default_rng(seed)`` exactly like ``start_session`` and hands the
+generator state to the device, which consumes the identical PCG64 stream for
+verify_sample's trials / draws and the window refills (``la_sample.cuh``).
 """
 
 from __future__ import annotations
@@ -44,10 +51,8 @@ def _require_b200(model) -> B200Model:
     return model
 
 
-def _require_greedy(sampler: SamplerSpec) -> None:
-    if sampler.mode != "greedy":
-        raise NotImplementedError("the B200 engine implements greedy lookahead decoding; "
-                                  "SamplerSpec(mode='temperature') is not on the device path")
+def _device_sampler(sampler: SamplerSpec, rng: np.random.Generator) -> _lib.la_sampler:
+    return _lib.make_sampler(sampler.temperature, sampler.top_k, sampler.top_p, rng)
 
 
 def _prompt(prompt) -> np.ndarray:
@@ -64,6 +69,7 @@ class _IO:
         P32 = C.POINTER(C.c_int32)
         self.prompt = prompt
         self.rng = rng
+        self.sampler = None
         self.pool_init = pool_init
         self.out = np.zeros(max_tokens, dtype=np.int32)
         self.rec = np.zeros((max_tokens + 1, 4), dtype=np.int32)
@@ -104,7 +110,6 @@ def _gen_config(config: GenerationConfig) -> _lib.la_gen_config:
 
 
 def _prepare_lookahead(model, prompt, config, sampler, pool):
-    _require_greedy(sampler)
     p = _prompt(prompt)
     if pool is not None and pool.ngram != config.ngram:
         raise ValueError("pool n-gram size does not match the generation config")
@@ -114,11 +119,22 @@ def _prepare_lookahead(model, prompt, config, sampler, pool):
     init = None
     if pool is not None and len(pool):
         init = np.ascontiguousarray(np.asarray(pool.entries_oldest_first(), dtype=np.int32))
-    rng = window_rng_stream(sampler.seed, model.vocab_size, config.window, config.ngram,
-                            config.max_tokens)
+    dev_sampler = None
+    if sampler.mode == "greedy":
+        rng = window_rng_stream(sampler.seed, model.vocab_size, config.window, config.ngram,
+                                config.max_tokens)
+    else:
+        # start_session (decoding.py:83-84): window_init's draws, then the
+        # generator continues on the device
+        gen = np.random.default_rng(sampler.seed)
+        ncell = max((config.ngram - 1) * config.window - 1, 0)
+        cells = gen.integers(0, model.vocab_size, size=ncell).astype(np.int32)
+        rng = np.ascontiguousarray(cells if ncell else np.zeros(1, dtype=np.int32))
+        dev_sampler = _device_sampler(sampler, gen)
     n_seed = max(0, len(p) - config.ngram + 1) if config.seed_pool_from_prompt else 0
     log_cap = n_seed + config.max_tokens * config.window + 1
     io = _IO(p, config.max_tokens, rng, init, config.ngram, log_cap)
+    io.sampler = dev_sampler
     return io
 
 
@@ -133,30 +149,43 @@ def _finish_lookahead(io: _IO, config: GenerationConfig, pool: NGramPool | None)
 
 def decode_lookahead(model, prompt: Sequence[int], config: GenerationConfig,
                      sampler: SamplerSpec, pool: NGramPool | None = None):
-    """Greedy lookahead decode on the GPU; returns (tokens, RunMetrics).
+    """Lookahead decode on the GPU; returns (tokens, RunMetrics).
 
-    Token-for-token equal to ``decode_autoregressive`` on the same model
-    (exactness guarantee, reference decoding.py:235-241)."""
+    Greedy: token-for-token equal to ``decode_autoregressive`` on the same
+    model (exactness guarantee, reference decoding.py:235-241).  Temperature:
+    distribution-preserving verification (verification.py:74-118) on the
+    same random stream as the reference session seeded with ``sampler.seed``."""
     m = _require_b200(model)
     io = _prepare_lookahead(m, prompt, config, sampler, pool)
-    _lib.check(m.lib.la_decode_lookahead(m.engine(), C.byref(_gen_config(config)),
-                                         C.byref(io.io), m.stream()))
+    if io.sampler is None:
+        rc = m.lib.la_decode_lookahead(m.engine(), C.byref(_gen_config(config)),
+                                       C.byref(io.io), m.stream())
+    else:
+        rc = m.lib.la_decode_lookahead_sampled(m.engine(), C.byref(_gen_config(config)),
+                                               C.byref(io.sampler), C.byref(io.io), m.stream())
+    _lib.check(rc)
     m.last_stats = io.stats()
     return _finish_lookahead(io, config, pool)
 
 
 def decode_autoregressive(model, prompt: Sequence[int], sampler: SamplerSpec, max_tokens: int,
                           eos_token: int | None = None) -> list[int]:
-    """Plain greedy decoding, one token per step (reference decoding.py:96-116)."""
+    """One token per forward (reference decoding.py:96-116): argmax, or one
+    ``sample_token`` draw from ``default_rng(sampler.seed)`` per token."""
     m = _require_b200(model)
-    _require_greedy(sampler)
     p = _prompt(prompt)
     if max_tokens < 1:
         return []      # the reference loop `while len(out) < max_tokens` never runs
     io = _IO(p, max_tokens)
     eos = -1 if eos_token is None else int(eos_token)
-    _lib.check(m.lib.la_decode_autoregressive(m.engine(), max_tokens, eos, C.byref(io.io),
-                                              m.stream()))
+    if sampler.mode == "greedy":
+        rc = m.lib.la_decode_autoregressive(m.engine(), max_tokens, eos, C.byref(io.io),
+                                            m.stream())
+    else:
+        smp = _device_sampler(sampler, np.random.default_rng(sampler.seed))
+        rc = m.lib.la_decode_autoregressive_sampled(m.engine(), max_tokens, eos, C.byref(smp),
+                                                    C.byref(io.io), m.stream())
+    _lib.check(rc)
     m.last_stats = io.stats()
     return io.tokens()
 

@@ -131,6 +131,10 @@ def decode_lookahead_devices(model, prompt: Sequence[int], config: GenerationCon
     m = _require_b200(model)
     if not 1 <= devices <= config.window:
         raise ValueError(f"device count must lie in [1, {config.window}], got {devices}")
+    if sampler.mode != "greedy":
+        # the per-step exchange carries argmax ids, not distributions
+        raise NotImplementedError("lookahead parallelism runs the greedy sampler; a temperature "
+                                  "SamplerSpec decodes on one device (decode_lookahead)")
     io = _prepare_lookahead(m, prompt, config, sampler, pool)
     dist, rank, world = _dist_world()
     if dist is not None and world == devices and devices > 1:
