@@ -334,6 +334,18 @@ def run_ours(args):
         ar_toks = la.decode_autoregressive(model, prompt, sampler, 128)
         ar_ms_step = model.last_stats["decode_ms"] / max(1, model.last_stats["steps"])
         ar_match = ar_toks == toks_all[0][:128]
+    # temperature sampler on the same workload (verify_sample on the device)
+    sampled = None
+    if world == 1:
+        ssp = la.SamplerSpec("temperature", temperature=1.0, top_p=0.9, seed=0)
+        la.decode_lookahead(model, prompt, gcfg, ssp)
+        st_toks, st_met = la.decode_lookahead(model, prompt, gcfg, ssp)
+        st = model.last_stats
+        s_ms = st["decode_ms"] / max(1, st_met.steps)
+        sampled = {"sampler": "temperature T=1.0 top_p=0.9 seed=0", "ms_per_step": s_ms,
+                   "tokens_per_s": len(st_toks) / (st["decode_ms"] / 1e3),
+                   "step_compression": st_met.compression,
+                   "step_over_greedy_lookahead_step": s_ms / ms_step}
     cpu = None
     if world == 1 and not args.no_cpu:
         cpu = cpu_reference_sample(cfg, int(ctx_mean), mean_M, S, budget_s=10.0)
@@ -365,6 +377,7 @@ def run_ours(args):
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
         "prefill_ms": statistics.mean(s["prefill_ms"] for s in stats),
+        "sampled": sampled,
         "greedy": ({"ms_per_step": ar_ms_step, "tokens_per_s": 1e3 / ar_ms_step,
                     "la_step_over_greedy_step": ms_step / ar_ms_step,
                     "first_128_tokens_equal_lookahead": ar_match} if ar_ms_step else None),

@@ -726,10 +726,14 @@ static int record_step(la_engine* e, cudaStream_t st, bool finish, int* nk) {
   if (finish && smp) {
     const DevDecode& h = e->h_dec;
     const int rows = h.mode == LA_MODE_LOOKAHEAD ? 1 + h.G * (h.N - 1) : 1;
+    {
+      KT_BEGIN(st);
+      CK(la_launch(la_sample_adjust_kernel, dim3(rows), dim3(1024), 0, st, p->pdl, e->d_dec));
+      KT_END(st, "sample_adjust");
+    }
     KT_BEGIN(st);
-    CK(la_launch(la_sample_adjust_kernel, dim3(rows), dim3(1024), 0, st, p->pdl, e->d_dec));
     CK(la_launch(la_sample_verify_kernel, dim3(1), dim3(1024), 0, st, p->pdl, e->d_dec));
-    KT_END(st, "sample_adjust+verify");
+    KT_END(st, "sample_verify");
     *nk += 2;
   }
   if (finish) {

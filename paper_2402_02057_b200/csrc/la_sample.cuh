@@ -78,7 +78,8 @@ __host__ __device__ __forceinline__ int la_pcg_integers(LaPcg64& g, unsigned hig
 #ifdef __CUDACC__
 // ------------------------------------------------------- block primitives
 struct LaSampleSmem {
-  unsigned long long hist[256];
+  unsigned long long hist[32][16];   // per-warp radix histograms (4-bit digits)
+  unsigned long long tot[16];
   double red[32];
   unsigned long long ured[32];
   int ired[32];
@@ -157,57 +158,70 @@ __device__ __forceinline__ unsigned long long la_pbits(double p) {
 // Radix select over the order (-p, id) restricted to values: finds the value
 // key T with  weight(p > T) < need <= weight(p >= T), weight = 1 per element
 // (mass == false) or floor(p * scale) (mass == true).  Returns false when the
-// total weight stays below `need`.  *above = weight(p > T).
+// total weight stays below `need`.  *above = weight(p > T).  4-bit digits
+// counted in per-thread registers and reduced by warp shuffles: near-uniform
+// distributions put almost every element in the same top digits, where
+// shared-memory atomics would serialise the CTA on one address.
 static __device__ bool la_radix_select(const double* p, int V, bool mass, double scale,
                                 unsigned long long need, LaSampleSmem& sm,
                                 unsigned long long* T, unsigned long long* above) {
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
+  const int nw = nth >> 5;
   unsigned long long prefix = 0ull, mask = 0ull, acc_above = 0ull;
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = tid; i < 256; i += nth) sm.hist[i] = 0ull;
-    __syncthreads();
-    for (int i = tid; i < V; i += nth) {
-      const double v = p[i];
-      const unsigned long long b = la_pbits(v);
-      if ((b & mask) == prefix) {
-        const unsigned long long wgt = mass ? (unsigned long long)(v * scale) : 1ull;
-        if (wgt) atomicAdd(&sm.hist[(b >> shift) & 255ull], wgt);
+  for (int shift = 60; shift >= 0; shift -= 4) {
+    unsigned long long loc[16];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) loc[d] = 0ull;
+    for (int i0 = tid; i0 < V; i0 += 8 * nth) {
+      double vb[8];   // 8 loads in flight per thread (the pass is L2-latency bound)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) vb[u] = (i0 + u * nth < V) ? p[i0 + u * nth] : -1.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double v = vb[u];
+        const unsigned long long b = la_pbits(v);
+        if (v >= 0.0 && (b & mask) == prefix) {
+          const unsigned long long wgt = mass ? (unsigned long long)(v * scale) : 1ull;
+          const int dg = (int)((b >> shift) & 15ull);
+#pragma unroll
+          for (int d = 0; d < 16; ++d) loc[d] += (dg == d) ? wgt : 0ull;
+        }
       }
     }
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      unsigned long long v = loc[d];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      loc[d] = v;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < 16; ++d) sm.hist[w][d] = loc[d];
+    }
     __syncthreads();
-    if (tid < 32) {
-      // lane l holds digits 255-8l .. 248-8l (descending value order)
-      unsigned long long loc[8], sum = 0ull;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) { loc[j] = sm.hist[255 - (lane * 8 + j)]; sum += loc[j]; }
-      unsigned long long inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long n = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += n;
+    if (tid < 16) {
+      unsigned long long t = 0ull;
+      for (int j = 0; j < nw; ++j) t += sm.hist[j][tid];
+      sm.tot[tid] = t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long acc = acc_above;
+      int sel = -1;
+      for (int dg = 15; dg >= 0; --dg) {
+        if (acc + sm.tot[dg] >= need) { sel = dg; break; }
+        acc += sm.tot[dg];
       }
-      const unsigned hit = __ballot_sync(0xffffffffu, acc_above + inc >= need);
-      if (!hit) {
-        if (lane == 0) sm.sel = -1;
-      } else if (lane == __ffs(hit) - 1) {
-        unsigned long long acc = acc_above + inc - sum;
-        int sel = 255 - lane * 8 - 7;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (acc + loc[j] >= need) { sel = 255 - (lane * 8 + j); break; }
-          acc += loc[j];
-        }
-        sm.sel = sel;
-        sm.sel_acc = acc;
-      }
+      sm.sel = sel;
+      sm.sel_acc = acc;
     }
     __syncthreads();
     const int sel = sm.sel;
     if (sel < 0) return false;
     acc_above = sm.sel_acc;
     prefix |= (unsigned long long)sel << shift;
-    mask |= 255ull << shift;
-    __syncthreads();
+    mask |= 15ull << shift;
   }
   *T = prefix;
   *above = acc_above;
