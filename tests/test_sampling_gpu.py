@@ -138,3 +138,54 @@ def test_bf16_sampled_first_token_law(llama):
     assert counts[want == 0].sum() == 0
     tv = 0.5 * np.abs(counts / n - want).sum()
     assert tv < 0.12, tv
+
+
+def _verify(m, base, cands, seed):
+    """device verify_sample; cands = [(suffix, [d_1 .. d_S])] (base shared)."""
+    V = len(base)
+    S = len(cands[0][0]) if cands else 1
+    rows = [base] + [d for _, ds in cands for d in ds]
+    dists = np.ascontiguousarray(np.array(rows, dtype=np.float64))
+    suf = np.ascontiguousarray(np.array([s for s, _ in cands] if cands else [[0]], dtype=np.int32))
+    out = np.zeros(S + 2, dtype=np.int32)
+    n = C.c_int32(0)
+    smp = _lib.make_sampler(1.0, None, None, np.random.default_rng(seed))
+    P32 = C.POINTER(C.c_int32)
+    _lib.check(m.lib.la_verify_sample_dists(m.engine(), dists.ctypes.data, V, S, len(cands),
+                                            suf.ctypes.data_as(P32), C.byref(smp),
+                                            out.ctypes.data_as(P32), C.byref(n), m.stream()))
+    return out[: n.value].tolist()
+
+
+def test_verify_sample_law_on_device(tiny):
+    """test_verification.py:103-132 / test_acceptance.py:113-127: the first
+    emitted token follows the base law whatever the speculations."""
+    cases = [
+        (np.array([0.4, 0.3, 0.2, 0.1]), []),                                        # no candidates
+        (np.array([0.4, 0.3, 0.2, 0.1]), [((2,), [np.full(4, 0.25)])]),              # single candidate
+        (np.array([0.5, 0.3, 0.2]), [((1,), [np.array([0.5, 0.3, 0.2])])] * 2),      # duplicates
+        (np.array([0.1, 0.2, 0.3, 0.4]), [((3, 1), [np.full(4, 0.25)] * 2), ((0, 2), [np.full(4, 0.25)] * 2),
+                                          ((3, 3), [np.full(4, 0.25)] * 2)]),
+    ]
+    runs = 30000
+    for base, cands in cases:
+        counts = np.zeros(len(base))
+        for seed in range(runs):
+            counts[_verify(tiny, base, cands, seed)[0]] += 1
+        tv = 0.5 * np.abs(counts / runs - base).sum()
+        assert tv < 0.01, (cands, tv)
+
+
+def test_verify_sample_edge_cases_on_device(tiny):
+    oh = lambda i: np.eye(3)[i]  # noqa: E731
+    # one-hot distributions accept every speculation, any seed (test_verification.py:92-101)
+    for seed in range(25):
+        assert _verify(tiny, oh(2), [((2, 0), [oh(0), oh(1)])], seed) == [2, 0, 1]
+    # deterministic given the generator state (:134-139)
+    base = np.array([0.4, 0.3, 0.2, 0.1])
+    c = [((2,), [np.full(4, 0.25)])]
+    assert _verify(tiny, base, c, 42) == _verify(tiny, base, c, 42)
+    # zero-mass base raises DegenerateDistributionError (:141-144)
+    dead = np.zeros(2)
+    with pytest.raises(la.DegenerateDistributionError):
+        _verify(tiny, dead, [((1,), [dead])], 0)
