@@ -358,6 +358,43 @@ def gen_sampling(la):
                             "decode": decode, "ar": ar})
 
 
+def gen_cli(la):
+    """Reports of the reference CLI (cli.py:174-297) on the config-1 transformer,
+    run with relative paths from a scratch directory so the config echo is
+    location independent; the GPU test re-runs the same argv on our CLI."""
+    import shutil
+    import tempfile
+    from lookahead import cli
+    prompts = "hello lookahead\nthe quick brown fox jumps\nabcabcabcabc\n"
+    cases = [
+        ["decode", "--mode", "lookahead", "-W", "5", "-N", "3", "--max-tokens", "40"],
+        ["decode", "--mode", "autoregressive", "--max-tokens", "24", "--format", "csv"],
+        ["decode", "--mode", "jacobi", "--max-tokens", "16"],
+        ["decode", "--mode", "lookahead", "-W", "4", "-N", "4", "-G", "2", "--max-tokens", "32",
+         "--pool-from-prompt", "--temperature", "0.8", "--top-p", "0.9", "--seed", "3"],
+        ["bench", "-W", "5", "-N", "3", "--max-tokens", "20", "--pool-from-prompt"],
+        ["simulate", "--devices", "2", "-W", "6", "-N", "3", "--max-tokens", "24"],
+    ]
+    out = []
+    d = tempfile.mkdtemp()
+    cwd = os.getcwd()
+    try:
+        os.chdir(d)
+        for argv in cases:
+            for f in os.listdir("."):
+                os.remove(f)
+            Path("prompts.txt").write_text(prompts)
+            full = argv + ["--model", "transformer", "--prompts", "prompts.txt", "--out", "report.json"]
+            assert cli.main(full) == 0
+            files = {f: Path(f).read_text() for f in sorted(os.listdir(".")) if f != "prompts.txt"}
+            out.append({"argv": full, "files": files})
+    finally:
+        os.chdir(cwd)
+        shutil.rmtree(d)
+    _dump("cli.json", {"source": "cli.main (cli.py:174-330), --model transformer", "prompts": prompts,
+                       "cases": out})
+
+
 def main():
     la = _ref()
     if len(sys.argv) > 1:   # regenerate selected fixtures only, e.g. `make_golden.py jacobi`
@@ -374,6 +411,7 @@ def main():
     gen_decode(la)
     gen_jacobi(la)
     gen_sampling(la)
+    gen_cli(la)
     print("golden vectors written to", OUT)
 
 
