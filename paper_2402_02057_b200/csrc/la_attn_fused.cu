@@ -374,6 +374,24 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
       cp_commit();
     }
   };
+  // ---- q fragments straight from global (m16n8k16 A layout); issued before
+  // the K/V ring so their L2 latency overlaps the cp.async issue
+  const int qrow0 = warp * 16 + (lane >> 2);
+  uint32_t qf[8][4];
+  auto load_q = [&]() {
+    const int qa = rb * 128 + qrow0, qb = qa + 8;
+    const __nv_bfloat16* pa = qa < nq ? a.q + ((size_t)(qa / g) * a.H + kvh * g + qa % g) * 128 : nullptr;
+    const __nv_bfloat16* pb = qb < nq ? a.q + ((size_t)(qb / g) * a.H + kvh * g + qb % g) * 128 : nullptr;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int col = kk * 16 + (lane & 3) * 2;
+      qf[kk][0] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
+      qf[kk][1] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
+      qf[kk][2] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
+      qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
+    }
+  };
+  if (active && !tc && !a.fuse_qkv) load_q();
   if (active && !step_unit && !tc) issue_first();
   if (a.fuse_qkv) {
     // QKV split-K epilogue (la_qkv_fix) spread over every CTA of the grid,
@@ -425,22 +443,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   } else {
     if (step_unit) issue_first();
 
-    // ---- q fragments straight from global (m16n8k16 A layout)
-    const int qrow0 = warp * 16 + (lane >> 2);
-    uint32_t qf[8][4];
-    {
-      const int qa = rb * 128 + qrow0, qb = qa + 8;
-      const __nv_bfloat16* pa = qa < nq ? a.q + ((size_t)(qa / g) * a.H + kvh * g + qa % g) * 128 : nullptr;
-      const __nv_bfloat16* pb = qb < nq ? a.q + ((size_t)(qb / g) * a.H + kvh * g + qb % g) * 128 : nullptr;
-  #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const int col = kk * 16 + (lane & 3) * 2;
-        qf[kk][0] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
-        qf[kk][1] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
-        qf[kk][2] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
-        qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
-      }
-    }
+    if (a.fuse_qkv) load_q();   // q is produced by the fused epilogue above
 
     float o[16][4];
   #pragma unroll
@@ -592,32 +595,51 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   if (!*sFlag) return;
 
   // ---- merge the S+1 chunk partials of this group in chunk order: rows
-  // [r0, r1) of the group, 8 threads per row x 16 dims
-  const int rows_per = a.spread_merge ? (128 + S) / (S + 1) : 128;
+  // [r0, r1) of the group's valid rows, 8 threads per row x 16 dims
+  const int nqb = min(128, nq - rb * 128);
+  const int rows_per = a.spread_merge ? (nqb + S) / (S + 1) : nqb;
   const int r0 = a.spread_merge ? split * rows_per : 0;
-  const int r1 = min(128, r0 + rows_per);
+  const int r1 = min(nqb, r0 + rows_per);
   for (int row = r0 + (tid >> 3); row < r1; row += 32) {
     const int qr = rb * 128 + row;
-    if (qr >= nq) break;
     const int hd = (tid & 7) * 16;
     float m = -INFINITY, ll = 0.f;
     float acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-    for (int sp = 0; sp <= S; ++sp) {
-      const size_t us = grp * (S + 1) + sp;
-      const float2 ml = __ldcg(a.part_ml + us * 128 + row);
-      const float4* po = reinterpret_cast<const float4*>(a.part_o + (us * 128 + row) * 128 + hd);
-      const float4 v0 = __ldcg(po), v1 = __ldcg(po + 1), v2 = __ldcg(po + 2), v3 = __ldcg(po + 3);
-      if (ml.x == -INFINITY) continue;
-      const float mn = fmaxf(m, ml.x);
-      const float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
-      const float vv[16] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w,
-                            v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};
+    // partials in batches of 4 with every load of a batch in flight together
+    // (a dependent L2 round trip per partial otherwise); same combine order
+    for (int sp0 = 0; sp0 <= S; sp0 += 4) {
+      float2 mlv[4];
+      float4 pv[4][4];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) acc[i] = acc[i] * s0 + vv[i] * s1;
-      ll = ll * s0 + ml.y * s1;
-      m = mn;
+      for (int j = 0; j < 4; ++j) {
+        const int sp = sp0 + j;
+        if (sp <= S) {
+          const size_t us = grp * (S + 1) + sp;
+          mlv[j] = __ldcg(a.part_ml + us * 128 + row);
+          const float4* po = reinterpret_cast<const float4*>(a.part_o + (us * 128 + row) * 128 + hd);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pv[j][q] = __ldcg(po + q);
+        } else {
+          mlv[j] = make_float2(-INFINITY, 0.f);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 ml = mlv[j];
+        if (ml.x == -INFINITY) continue;
+        const float mn = fmaxf(m, ml.x);
+        const float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
+        const float vv[16] = {pv[j][0].x, pv[j][0].y, pv[j][0].z, pv[j][0].w,
+                              pv[j][1].x, pv[j][1].y, pv[j][1].z, pv[j][1].w,
+                              pv[j][2].x, pv[j][2].y, pv[j][2].z, pv[j][2].w,
+                              pv[j][3].x, pv[j][3].y, pv[j][3].z, pv[j][3].w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = acc[i] * s0 + vv[i] * s1;
+        ll = ll * s0 + ml.y * s1;
+        m = mn;
+      }
     }
     const float inv = 1.0f / ll;
     const int r = qr / g, head = kvh * g + qr % g;

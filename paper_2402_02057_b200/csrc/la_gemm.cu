@@ -203,11 +203,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (long u = u_begin + n_pre; u < min(u_end, u_begin + n_pre + args.l2pf); ++u)
       ptx::bulk_prefetch_l2(a_src(u), a_bytes);
   }
+  const unsigned long long t_entry = args.trace ? globaltimer() : 0ull;
   la_pdl_wait();
   if (args.timing && threadIdx.x == 0) {
     if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();
   }
-  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 0] = globaltimer();
+  // trace: [0] CTA entry (before the dependency wait), [1] wait returned
+  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 0] = t_entry;
   const int n_rows = P->n_rows;
   const int n_pad = P->n_pad;
   if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
