@@ -20,10 +20,13 @@ steps = int(os.environ.get("STEPS", "2"))
 m = la.LlamaModel(LLAMA2_7B, dtype="bf16", seed=0, max_context=1088)
 prompt = [int(t) for t in np.random.default_rng(0).integers(0, 32000, 512)]
 cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=steps)
-la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy"))
+# SAMPLER=temperature: T=1, top_p=0.9 (adds the sampler's adjust / verify kernels)
+spec = (la.SamplerSpec("temperature", temperature=1.0, top_p=0.9, seed=0)
+        if os.environ.get("SAMPLER") == "temperature" else la.SamplerSpec("greedy"))
+la.decode_lookahead(m, prompt, cfg, spec)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy"))
+la.decode_lookahead(m, prompt, cfg, spec)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("ok")
