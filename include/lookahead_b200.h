@@ -30,6 +30,7 @@ extern "C" {
 #define LA_ERR_NCCL (-4)
 #define LA_ERR_CAPACITY (-5) /* a device-side table or buffer would overflow */
 #define LA_ERR_UNSUPPORTED (-6)
+#define LA_MAX_ACCEPT 9         /* N <= 8: a step accepts <= N tokens */
 #define LA_ERR_DEGENERATE (-7) /* DegenerateDistributionError: types.py, sampling.py:52-65,
                                   verification.py:108-110 */
 
@@ -149,6 +150,33 @@ int32_t la_decode_lookahead_sampled(la_engine* e, const la_gen_config* cfg, cons
  * is default_rng(seed) untouched (io->rng_stream unused). */
 int32_t la_decode_autoregressive_sampled(la_engine* e, int32_t max_tokens, int32_t eos_token,
                                          const la_sampler* s, la_decode_io* io, void* stream);
+
+/* ------------------------------------------------------------ step session
+ * start_session / lookahead_step (decoding.py:67-93,152-211): the decode
+ * state stays on the device between steps.  greedy != 0: greedy
+ * verification; else sampling verification with s's temperature / top-k /
+ * top-p.  Either way s carries the session generator AFTER window_init
+ * (io->rng_stream / rng_len = the (N-1)W-1 window cells drawn by the
+ * caller); window refills continue that stream on the device.  Steps never
+ * stop on EOS / max_tokens (the caller folds tokens, collect_output
+ * decoding.py:214-232); a step past the engine's max_context fails with
+ * LA_ERR_CAPACITY.  A whole-decode call on the engine ends the session. */
+typedef struct la_step_outcome {   /* StepOutcome + StepRecord (decoding.py:44-50, types.py) */
+  int32_t accepted[LA_MAX_ACCEPT]; /* 1..N tokens */
+  int32_t n_accepted;
+  int32_t new_top[64];             /* greedy tokens of the W generator rows */
+  int32_t n_new_top;
+  int32_t candidate_count, query_count;
+  int32_t pool_size;               /* len(pool) after the step's inserts */
+  int32_t pool_log_n;              /* pool inserts so far (incl. prompt seeding) */
+} la_step_outcome;
+
+int32_t la_session_start(la_engine* e, const la_gen_config* cfg, int32_t greedy,
+                         const la_sampler* s, la_decode_io* io, void* stream);
+int32_t la_session_step(la_engine* e, la_step_outcome* out, void* stream);
+/* what 0: the window's (N-1)W-1 cells (SURVEY A.1 order); what 1: pool-log
+ * n-grams [offset, offset + n), N ints each (inserts in order) */
+int32_t la_session_read(la_engine* e, int32_t what, int32_t offset, int32_t n, int32_t* out);
 
 /* Parity hooks (tests only).  la_adjust_distributions: adjusted_distribution
  * of n_rows fp64 probability rows [n_rows][V] on the device (host buffers;

@@ -8,14 +8,15 @@ C ABI (``include/lookahead_b200.h``).
 __version__ = "0.1.0"
 
 from .analytics import RunMetrics, compression_ratio, flops_proxy
-from .decoding import decode_autoregressive, decode_jacobi, decode_lookahead, window_rng_stream
+from .decoding import (DecodeState, collect_output, decode_autoregressive, decode_jacobi,
+                       decode_lookahead, lookahead_step, start_session, window_rng_stream)
 from .layout import CandidateBranch, QueryToken, StepLayout, chain_layout
 from .models import (CODELLAMA_7B, LLAMA2_13B, LLAMA2_70B, LLAMA2_7B, PRESETS, B200Model,
                      LlamaConfig, LlamaModel, TinyTransformer)
 from .parallel import CommStats, column_ranges, decode_lookahead_devices, lp_init, step_comm
 from .pool import NGramPool
 from .types import (DegenerateDistributionError, GenerationConfig, JacobiTrajectory, LayoutError,
-                    SamplerSpec, StepRecord)
+                    SamplerSpec, StepOutcome, StepRecord, Window2D)
 
 
 def transformer_init(seed, vocab_size, d_model=16, n_layers=2, n_heads=2, **kw):
@@ -30,6 +31,7 @@ def greedy_token(probs) -> int:
 
 
 __all__ = [
+    "DecodeState", "StepOutcome", "Window2D", "collect_output", "lookahead_step", "start_session",
     "B200Model", "CODELLAMA_7B", "CandidateBranch", "CommStats", "DegenerateDistributionError",
     "GenerationConfig", "JacobiTrajectory", "LLAMA2_13B", "LLAMA2_70B", "LLAMA2_7B", "LayoutError", "LlamaConfig",
     "LlamaModel", "NGramPool", "PRESETS", "QueryToken", "RunMetrics", "SamplerSpec",

@@ -36,6 +36,7 @@ EXPORTS = (
     "la_gemm_timing_reset", "la_gemm_timing_read", "la_forward_timing_read", "la_packed_bytes",
     "la_decode_jacobi", "la_decode_lookahead_sampled", "la_decode_autoregressive_sampled",
     "la_adjust_distributions", "la_verify_sample_dists", "la_pcg64_draws",
+    "la_session_start", "la_session_step", "la_session_read",
     "la_pack_weight",
 )
 
@@ -64,6 +65,13 @@ class la_sampler(C.Structure):
     _fields_ = [("temperature", C.c_double), ("top_k", C.c_int32), ("top_p", C.c_double),
                 ("state_hi", C.c_uint64), ("state_lo", C.c_uint64), ("inc_hi", C.c_uint64),
                 ("inc_lo", C.c_uint64), ("has_uint32", C.c_int32), ("uinteger", C.c_uint32)]
+
+
+class la_step_outcome(C.Structure):
+    _fields_ = [("accepted", C.c_int32 * 9), ("n_accepted", C.c_int32),
+                ("new_top", C.c_int32 * 64), ("n_new_top", C.c_int32),
+                ("candidate_count", C.c_int32), ("query_count", C.c_int32),
+                ("pool_size", C.c_int32), ("pool_log_n", C.c_int32)]
 
 
 def make_sampler(temperature: float, top_k, top_p, rng) -> la_sampler:
@@ -138,6 +146,10 @@ def load(path: str | os.PathLike | None = None):
     lib.la_verify_sample_dists.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                            C.c_int32, _P32, SP, _P32, _P32, C.c_void_p]
     lib.la_pcg64_draws.argtypes = [SP, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
+    lib.la_session_start.argtypes = [C.c_void_p, C.POINTER(la_gen_config), C.c_int32, SP,
+                                     C.POINTER(la_decode_io), C.c_void_p]
+    lib.la_session_step.argtypes = [C.c_void_p, C.POINTER(la_step_outcome), C.c_void_p]
+    lib.la_session_read.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _P32]
     lib.la_gemm_timing_reset.argtypes = [C.c_void_p]
     lib.la_gemm_timing_read.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     for name in EXPORTS:

@@ -115,6 +115,7 @@ struct DevDecode {
   // temperature sampler (SamplerSpec, types.py:43-67; sampling.py:22-85);
   // sample == 0: greedy and none of the fields below is read
   int sample;
+  int pcg_window;       // window refills from `pcg` (step sessions) instead of the rng stream
   int top_k;            // 0: no top-k
   double temperature;   // p ** (1/T) unless T == 1
   double top_p;         // >= 1: no nucleus

@@ -273,6 +273,8 @@ struct DecodeArgs {
   int mode;
   int W, N, G, max_tokens, eos, seed_pool;
   const la_sampler* smp = nullptr;   // temperature sampler (null: greedy)
+  bool greedy_verify = false;        // smp only carries the generator (greedy step session)
+  bool pcg_window = false;           // window refills from the generator (step sessions)
 };
 
 // SamplerSpec.__post_init__ (types.py:59-67)
@@ -318,7 +320,7 @@ static int validate_gen(const la_engine* e, const DecodeArgs& a, const la_decode
     }
     if (a.W + a.N - 2 >= LA_MAX_CHAIN) { la_set_error("chain too long"); return LA_ERR_UNSUPPORTED; }
   }
-  if (a.smp) {
+  if (a.smp && !a.greedy_verify) {
     RET_IF(validate_sampler(a.smp));
     if (e->world > 1) {
       la_set_error("lookahead parallelism exchanges argmax ids only: temperature sampling is single-replica");
@@ -414,6 +416,10 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
   d.pool.lead_keys = e->p_lead; d.pool.bkt_cnt = e->p_cnt; d.pool.bkt_suf = e->p_suf;
   d.pool.set_keys = e->p_set; d.pool.counters = e->p_counters; d.pool.log = e->p_log;
   if (a.smp) {
+    d.pcg = pcg_of(a.smp);
+    d.pcg_window = a.pcg_window ? 1 : 0;
+  }
+  if (a.smp && !a.greedy_verify) {
     RET_IF(sampler_buffers(e, a.mode == LA_MODE_LOOKAHEAD ? 1 + d.G * (N - 1) : 1));
     d.sample = 1;
     d.temperature = a.smp->temperature;
@@ -479,6 +485,7 @@ int lp_decode_loop(la_engine* e, cudaStream_t st, int* launches);
 static int run_decode(la_engine* e, const DecodeArgs& a, la_decode_io* io, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(e->device));
+  e->session = false;   // a whole decode reuses (and ends) any step session's state
   RET_IF(validate_gen(e, a, io));
   if (a.mode == LA_MODE_AUTOREGRESSIVE && e->world > 1) {
     la_set_error("autoregressive decode is single-replica");
@@ -538,6 +545,105 @@ extern "C" int32_t la_decode_autoregressive_sampled(la_engine* e, int32_t max_to
   if (!e || !s) { la_set_error("null engine or sampler"); return LA_ERR_INVALID_CONFIG; }
   DecodeArgs a{LA_MODE_AUTOREGRESSIVE, 1, 2, 0, max_tokens, eos_token < 0 ? -1 : eos_token, 0, s};
   return run_decode(e, a, io, stream);
+}
+
+// ------------------------------------------------------------ step session
+// start_session (decoding.py:67-93): pool reset + seeding, window from the
+// caller's generator (io->rng_stream = window_init's (N-1)W-1 cells), the
+// generator state after it in *s, prompt prefill.  The device never stops on
+// its own (no EOS, the budget is the engine's context): the caller folds the
+// steps' tokens (collect_output, decoding.py:214-232).
+extern "C" int32_t la_session_start(la_engine* e, const la_gen_config* cfg, int32_t greedy,
+                                    const la_sampler* s, la_decode_io* io, void* stream) {
+  if (!e || !cfg || !s || !io) { la_set_error("null engine, config, sampler or io"); return LA_ERR_INVALID_CONFIG; }
+  if (e->world > 1) { la_set_error("step sessions are single-replica"); return LA_ERR_UNSUPPORTED; }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  e->session = false;
+  const int budget = e->desc.max_context - (io->n_prompt > 0 ? io->n_prompt : 0) - LA_MAX_NGRAM;
+  if (budget < 1) { la_set_error("prompt does not fit the engine's max_context"); return LA_ERR_CAPACITY; }
+  DecodeArgs a{LA_MODE_LOOKAHEAD, cfg->window, cfg->ngram, cfg->max_candidates,
+               std::min(budget, e->rec_cap - 1), -1, cfg->seed_pool_from_prompt, s,
+               greedy != 0, true};
+  io->out_tokens = nullptr;
+  io->step_records = nullptr;
+  RET_IF(validate_gen(e, a, io));
+  RET_IF(setup_decode(e, a, io, st));
+  RET_IF(prefill(e, io->n_prompt - 1, st));
+  CK(cudaMemcpyAsync(&e->sess, e->d_dec, sizeof(DevDecode), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  e->session = true;
+  return LA_OK;
+}
+
+// lookahead_step (decoding.py:207-211): one step on the device, outcome read back
+extern "C" int32_t la_session_step(la_engine* e, la_step_outcome* out, void* stream) {
+  if (!e || !out) { la_set_error("null engine or outcome"); return LA_ERR_INVALID_CONFIG; }
+  if (!e->session) { la_set_error("no active step session (la_session_start)"); return LA_ERR_INVALID_CONFIG; }
+  const DevDecode& h = e->sess;
+  if (h.done || h.ctx + h.N + 1 > e->desc.max_context) {
+    la_set_error("session reached the engine's max_context (%d)", e->desc.max_context);
+    return LA_ERR_CAPACITY;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(e->device));
+  if (e->is_tiny()) {
+    la_tiny_step_forward<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_dec,
+                                             h.sample ? e->d_logits : nullptr);
+    if (h.sample) {
+      la_sample_adjust_kernel<<<1 + h.G * (h.N - 1), 1024, 0, st>>>(e->d_dec);
+      la_sample_verify_kernel<<<1, 1024, 0, st>>>(e->d_dec);
+    }
+    la_step_finish_kernel<<<1, 256, 0, st>>>(e->d_dec);
+    la_kv_commit_kernel<<<std::max(1, std::min(148, e->desc.layers * e->row_bytes / 16 / 256)), 256, 0, st>>>(
+        e->d_dec, (uint8_t*)e->kc, (uint8_t*)e->vc, e->desc.layers, e->slots, e->row_bytes);
+    CK(cudaGetLastError());
+  } else {
+    RET_IF(llama_session_step(e, st));
+  }
+  DevDecode d;
+  int counters[4];
+  CK(cudaMemcpyAsync(&d, e->d_dec, sizeof(d), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(counters, e->p_counters, sizeof(counters), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out->accepted, e->d_acc, sizeof(int32_t) * (LA_MAX_NGRAM + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out->new_top, e->d_amax + (h.N - 2) * h.W, sizeof(int32_t) * h.W,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (d.overflow) { la_set_error("device capacity exceeded (pool table or log)"); return LA_ERR_CAPACITY; }
+  if (d.degenerate) { la_set_error("all probability mass truncated away (degenerate distribution)"); return LA_ERR_DEGENERATE; }
+  if (!e->is_tiny() && llama_mega_error(e)) { la_set_error("persistent forward kernel: dependency wait timed out"); return LA_ERR_CUDA; }
+  if (d.n_steps != h.n_steps + 1) { la_set_error("session step did not run"); return LA_ERR_CUDA; }
+  e->sess = d;
+  out->n_accepted = d.k;
+  out->n_new_top = h.W;
+  out->candidate_count = d.c;
+  out->query_count = d.M;
+  out->pool_size = counters[0];
+  out->pool_log_n = counters[1];
+  return LA_OK;
+}
+
+// session state readers: what 0 = window cells ((N-1)W-1), 1 = pool-log
+// n-grams [offset, offset+n) (N ints each)
+extern "C" int32_t la_session_read(la_engine* e, int32_t what, int32_t offset, int32_t n,
+                                   int32_t* out) {
+  if (!e || !out || offset < 0 || n < 0) { la_set_error("bad arguments"); return LA_ERR_INVALID_CONFIG; }
+  if (!e->session) { la_set_error("no active step session"); return LA_ERR_INVALID_CONFIG; }
+  CK(cudaSetDevice(e->device));
+  const DevDecode& h = e->sess;
+  if (what == 0) {
+    const int ncell = (h.N - 1) * h.W - 1;
+    if (offset + n > ncell) { la_set_error("window has %d cells", ncell); return LA_ERR_INVALID_CONFIG; }
+    if (n) CK(cudaMemcpy(out, e->d_window + offset, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    return LA_OK;
+  }
+  if (what == 1) {
+    if ((size_t)(offset + n) > e->p_log_cap) { la_set_error("pool log holds %zu entries", e->p_log_cap); return LA_ERR_CAPACITY; }
+    if (n) CK(cudaMemcpy(out, e->p_log + (size_t)offset * h.N, (size_t)n * h.N * 4, cudaMemcpyDeviceToHost));
+    return LA_OK;
+  }
+  la_set_error("unknown session field %d", what);
+  return LA_ERR_INVALID_CONFIG;
 }
 
 // ---------------------------------------------------------- sampler hooks
@@ -694,6 +800,7 @@ extern "C" int32_t la_forward_layout(la_engine* e, const int32_t* prefix, int32_
                                      const int32_t* chain, int32_t chain_stride, float* logits,
                                      void* stream) {
   if (!e) { la_set_error("null engine"); return LA_ERR_INVALID_CONFIG; }
+  e->session = false;   // the parity forward reuses the plan and KV cache
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(e->device));
   FwdPlan* P = new FwdPlan();
@@ -712,6 +819,7 @@ extern "C" int32_t la_decode_jacobi(la_engine* e, const int32_t* prompt, int32_t
                                     const int32_t* init, int32_t* out_tokens, int32_t* iterates,
                                     int32_t* n_iterations, void* stream) {
   if (!e || !prompt || !init || !out_tokens || !n_iterations) { la_set_error("null argument"); return LA_ERR_INVALID_CONFIG; }
+  e->session = false;
   if (n_prompt < 1) { la_set_error("prompt must be nonempty"); return LA_ERR_INVALID_CONFIG; }
   if (m < 1) { la_set_error("generation length m must be >= 1"); return LA_ERR_INVALID_CONFIG; }
   if (m + 1 > LA_MAX_ROWS) { la_set_error("m + 1 must be <= %d rows", LA_MAX_ROWS); return LA_ERR_UNSUPPORTED; }
@@ -756,6 +864,8 @@ extern "C" int32_t la_decode_lookahead_group(la_engine* const* es, int32_t n,
                                              const la_gen_config* cfg, la_decode_io* io,
                                              void* stream) {
   if (!es || n < 1 || !cfg) { la_set_error("need >= 1 engine and a config"); return LA_ERR_INVALID_CONFIG; }
+  for (int r = 0; r < n; ++r)
+    if (es[r]) es[r]->session = false;
   if (n > cfg->window) {
     la_set_error("device count must lie in [1, %d], got %d", cfg->window, n);
     return LA_ERR_INVALID_CONFIG;

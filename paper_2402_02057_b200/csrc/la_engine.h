@@ -61,6 +61,10 @@ struct la_engine {
 
   cudaEvent_t ev[4] = {};
 
+  // ---- step session (la_session_start / la_session_step)
+  bool session = false;
+  DevDecode sess{};                    // device state after the last step
+
   bool is_tiny() const { return desc.arch != LA_ARCH_LLAMA_BF16; }
 };
 
@@ -73,5 +77,6 @@ int llama_prefill(la_engine* e, const int* d_tokens, int n, cudaStream_t st);
 int llama_decode_loop(la_engine* e, cudaStream_t st, int* launches);
 int llama_forward_plan(la_engine* e, float* d_logits, cudaStream_t st);
 int llama_step_forward(la_engine* e, cudaStream_t st);   // K1 + forward + owned argmax
+int llama_session_step(la_engine* e, cudaStream_t st);   // one eager step (K1 .. commit)
 int llama_mega_error(la_engine* e);                      // persistent-kernel dependency timeout flag
 cudaError_t llama_copy_argmax(la_engine* e, int32_t* host, int n, cudaStream_t st);   // last forward's row argmax

@@ -749,6 +749,12 @@ static int record_step(la_engine* e, cudaStream_t st, bool finish, int* nk) {
   return LA_OK;
 }
 
+// one whole step (K1 .. KV commit) as plain launches: step sessions
+int llama_session_step(la_engine* e, cudaStream_t st) {
+  int nk = 0;
+  return record_step(e, st, true, &nk);
+}
+
 static int build_loop_graph(la_engine* e) {
   LlamaPath* p = e->llama;
   cudaGraph_t g;

@@ -342,7 +342,7 @@ static __device__ void la_step_finish(DevDecode& d) {
     int val;
     if (sc <= W) {
       val = (level + 1 <= N - 2) ? s_oldwin[la_cell_index(level + 1, sc, W)] : s_newtop[sc - 1];
-    } else if (d.sample) {
+    } else if (d.sample || d.pcg_window) {
       continue;   // drawn below, in cell order, from the session generator
     } else {
       int idx = (level == 0) ? (col - max(2, W - sft + 1))
@@ -353,7 +353,7 @@ static __device__ void la_step_finish(DevDecode& d) {
     }
     d.window[f] = val;
   }
-  if (d.sample && tid == 0 && sft > 0) {
+  if ((d.sample || d.pcg_window) && tid == 0 && sft > 0) {
     // rng.integers(0, V) per vacated cell, level-major / column-ascending
     // (layout.py:243-250) -- f order is exactly that order
     LaPcg64 g = d.pcg;

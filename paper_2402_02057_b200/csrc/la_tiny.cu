@@ -307,11 +307,11 @@ __global__ void __launch_bounds__(1024) la_tiny_forward(TinyModel m, TinyScratch
 // phase A = K1 build + forward + owned-row argmax; the host-side group then
 // exchanges the argmax table and the winner's K/V; phase B = K10 finish.
 __global__ void __launch_bounds__(1024) la_tiny_step_forward(TinyModel m, TinyScratch s,
-                                                            FwdPlan* P, DevDecode* dp) {
+                                                            FwdPlan* P, DevDecode* dp, float* logits) {
   DevDecode& d = *dp;
   la_step_build(d, *P);
   if (P->n_rows == 0) return;
-  forward_rows(m, s, *P, nullptr);
+  forward_rows(m, s, *P, logits);
   for (int r = threadIdx.x; r < P->n_rows; r += blockDim.x)
     if (P->own[r]) d.amax[P->grow[r]] = s.row_amax[r];
 }

@@ -37,5 +37,6 @@ __global__ void la_tiny_prefill(TinyModel m, TinyScratch s, FwdPlan* P, const in
 __global__ void la_tiny_decode(TinyModel m, TinyScratch s, FwdPlan* P, DevDecode* dp,
                                float* logits);
 __global__ void la_tiny_forward(TinyModel m, TinyScratch s, FwdPlan* P, float* logits);
-__global__ void la_tiny_step_forward(TinyModel m, TinyScratch s, FwdPlan* P, DevDecode* dp);
+__global__ void la_tiny_step_forward(TinyModel m, TinyScratch s, FwdPlan* P, DevDecode* dp,
+                                     float* logits);
 __global__ void la_tiny_step_finish(DevDecode* dp);

@@ -24,7 +24,8 @@ from . import _lib
 from .analytics import RunMetrics
 from .models import B200Model
 from .pool import NGramPool
-from .types import GenerationConfig, JacobiTrajectory, SamplerSpec, StepRecord
+from .types import (GenerationConfig, JacobiTrajectory, SamplerSpec, StepOutcome, StepRecord,
+                    Window2D)
 
 
 def window_rng_draws(window: int, ngram: int, max_tokens: int) -> int:
@@ -214,3 +215,103 @@ def decode_jacobi(model, prompt: Sequence[int], m: int,
                                         iterates.ctypes.data_as(P32), C.byref(n_it), mdl.stream()))
     traj = [[int(t) for t in init]] + [[int(t) for t in iterates[i]] for i in range(n_it.value)]
     return [int(t) for t in out], JacobiTrajectory(traj), int(n_it.value)
+
+
+# ------------------------------------------------------------ step sessions
+class DecodeState:
+    """Per-session state (reference decoding.py:53-64).  The window, pool and
+    KV cache live on the device between steps; ``prefix``, ``records`` and the
+    caller-visible ``pool`` are kept in step on the host, ``window`` is read
+    back on access.  One active session per model: a whole-decode call or a
+    newer session on the same model ends it."""
+
+    def __init__(self, model, prefix, pool, config, sampler, rng):
+        self.model = model
+        self.prefix = prefix
+        self.pool = pool
+        self.config = config
+        self.sampler = sampler
+        self.rng = rng              # host generator after window_init (the device continues it)
+        self.records: list[StepRecord] = []
+        self._log_n = 0
+
+    @property
+    def window(self) -> Window2D:
+        m, W, N = self.model, self.config.window, self.config.ngram
+        cells = np.zeros(max((N - 1) * W - 1, 1), dtype=np.int32)
+        _lib.check(m.lib.la_session_read(m.engine(), 0, 0, (N - 1) * W - 1,
+                                         cells.ctypes.data_as(C.POINTER(C.c_int32))))
+        levels = [cells[: W - 1].tolist()] + [cells[W - 1 + l * W: W - 1 + (l + 1) * W].tolist()
+                                              for l in range(N - 2)]
+        return Window2D(W, N, m.vocab_size, levels)
+
+    def _sync_pool(self, log_n: int) -> None:
+        n = log_n - self._log_n
+        if n > 0:
+            buf = np.zeros((n, self.config.ngram), dtype=np.int32)
+            _lib.check(self.model.lib.la_session_read(self.model.engine(), 1, self._log_n, n,
+                                                      buf.ctypes.data_as(C.POINTER(C.c_int32))))
+            self.pool.insert_all(buf.tolist())
+        self._log_n = log_n
+
+
+def start_session(model, prompt: Sequence[int], config: GenerationConfig, sampler: SamplerSpec,
+                  pool: NGramPool | None = None) -> DecodeState:
+    """Initialise window, pool and generator for step-by-step decoding
+    (reference decoding.py:67-93); the prompt is prefilled on the device."""
+    m = _require_b200(model)
+    p = _prompt(prompt)
+    if pool is None:
+        pool = NGramPool(config.ngram)
+    elif pool.ngram != config.ngram:
+        raise ValueError("pool n-gram size does not match the generation config")
+    if pool.capacity is not None:
+        raise NotImplementedError("NGramPool(capacity=...) global LRU eviction is not "
+                                  "implemented on the device pool")
+    init = None
+    if len(pool):
+        init = np.ascontiguousarray(np.asarray(pool.entries_oldest_first(), dtype=np.int32))
+    rng = np.random.default_rng(sampler.seed)
+    ncell = (config.ngram - 1) * config.window - 1
+    cells = rng.integers(0, m.vocab_size, size=ncell).astype(np.int32)   # window_init
+    stream = np.ascontiguousarray(cells if ncell else np.zeros(1, dtype=np.int32))
+    n_seed = max(0, len(p) - config.ngram + 1) if config.seed_pool_from_prompt else 0
+    io = _IO(p, 1, stream, init, config.ngram, 1)
+    smp = _lib.make_sampler(sampler.temperature, sampler.top_k, sampler.top_p, rng)
+    _lib.check(m.lib.la_session_start(m.engine(), C.byref(_gen_config(config)),
+                                      1 if sampler.mode == "greedy" else 0, C.byref(smp),
+                                      C.byref(io.io), m.stream()))
+    state = DecodeState(m, [int(t) for t in p], pool, config, sampler, rng)
+    # a caller pool's replay is not a new insert; prompt seeding is (pool.py:83-90)
+    state._log_n = 0
+    state._sync_pool(n_seed)
+    m._session = state
+    return state
+
+
+def lookahead_step(state: DecodeState) -> StepOutcome:
+    """One generate-and-verify step on the device (reference decoding.py:207-211)."""
+    m = state.model
+    if getattr(m, "_session", None) is not state:
+        raise RuntimeError("this session was ended by a later decode or session on the same model")
+    out = _lib.la_step_outcome()
+    _lib.check(m.lib.la_session_step(m.engine(), C.byref(out), m.stream()))
+    accepted = [int(out.accepted[i]) for i in range(out.n_accepted)]
+    state._sync_pool(int(out.pool_log_n))
+    state.prefix.extend(accepted)
+    state.records.append(StepRecord(out.n_accepted, int(out.candidate_count),
+                                    int(out.query_count), int(out.pool_size)))
+    return StepOutcome(accepted, [int(out.new_top[i]) for i in range(out.n_new_top)],
+                       int(out.candidate_count), int(out.query_count))
+
+
+def collect_output(out: list[int], accepted: Sequence[int], max_tokens: int,
+                   eos_token: int | None) -> bool:
+    """Fold one step's tokens into the output (reference decoding.py:214-232)."""
+    for token in accepted:
+        out.append(int(token))
+        if eos_token is not None and token == eos_token:
+            return True
+        if len(out) >= max_tokens:
+            return True
+    return False
