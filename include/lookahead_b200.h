@@ -111,6 +111,7 @@ typedef struct la_decode_io {
   float prefill_ms;          /* written: CUDA-event time of the prompt prefill */
   float decode_ms;           /* written: CUDA-event time of the decode loop */
   int32_t launches;          /* written: kernels launched by the decode loop */
+  int32_t pool_capacity;     /* NGramPool(capacity=...): global LRU cap (pool.py:41-61); 0 = none */
 } la_decode_io;
 
 /* decode_lookahead (decoding.py:235-255), greedy sampler only. */

@@ -374,6 +374,8 @@ def gen_cli(la):
          "--pool-from-prompt", "--temperature", "0.8", "--top-p", "0.9", "--seed", "3"],
         ["bench", "-W", "5", "-N", "3", "--max-tokens", "20", "--pool-from-prompt"],
         ["simulate", "--devices", "2", "-W", "6", "-N", "3", "--max-tokens", "24"],
+        ["decode", "--mode", "lookahead", "-W", "5", "-N", "3", "--max-tokens", "40",
+         "--pool-capacity", "6", "--pool-from-prompt"],
     ]
     out = []
     d = tempfile.mkdtemp()

@@ -94,7 +94,8 @@ class la_decode_io(C.Structure):
                 ("out_tokens", _P32), ("out_cap", C.c_int32), ("n_out", C.c_int32),
                 ("step_records", _P32), ("rec_cap", C.c_int32), ("n_steps", C.c_int32),
                 ("pool_log", _P32), ("pool_log_cap", C.c_int32), ("pool_log_n", C.c_int32),
-                ("prefill_ms", C.c_float), ("decode_ms", C.c_float), ("launches", C.c_int32)]
+                ("prefill_ms", C.c_float), ("decode_ms", C.c_float), ("launches", C.c_int32),
+                ("pool_capacity", C.c_int32)]
 
 
 _lib = None

@@ -27,15 +27,19 @@
 //    reference (decoding.py:72-82).
 struct DevPool {
   int ngram;       // N
-  int C;           // bucket capacity (>= G, <= 32)
+  int C;           // bucket capacity: >= G (newest-C per lead suffices for lookups);
+                   // with an LRU cap every live entry of a lead (evictions surface older ones)
   int lt_mask;     // lead table size - 1 (power of two)
   int st_mask;     // distinct set size - 1 (power of two)
   int log_cap;
+  int capacity;    // NGramPool(capacity=...) global LRU cap; 0 = unbounded
   int* lead_keys;  // [LT]   -1 = empty
   int* bkt_cnt;    // [LT]
   int* bkt_suf;    // [LT][C][N-1]
   int* set_keys;   // [ST][N]  key[0] == -1 -> empty
-  int* counters;   // [0] = distinct n-grams, [1] = log length
+  int* set_stamp;  // [ST] last-touch stamp, -1 = evicted (capacity mode)
+  int* fifo;       // [log_cap] set slot touched by stamp s (capacity mode)
+  int* counters;   // [0] = distinct n-grams, [1] = log length, [2] = stamps issued, [3] = fifo head
   int* log;        // [log_cap][N]
 };
 

@@ -356,10 +356,21 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
   long inserts = n_init + n_seed + (long)max_steps * W + 1;
   size_t LT = pow2_at_least(2 * std::min<long>(V, inserts) + 2);
   size_t ST = pow2_at_least(2 * inserts + 2);
-  size_t C = std::max(1, a.G);
+  // LRU cap (pool.py:41-61): only a cap the decode can reach changes anything;
+  // then a bucket must hold every live entry of its lead
+  int cap = (a.mode == LA_MODE_LOOKAHEAD && io->pool_capacity > 0 && io->pool_capacity < inserts)
+                ? io->pool_capacity : 0;
+  if (io->pool_capacity < 0) { la_set_error("capacity must be a positive integer"); return LA_ERR_INVALID_CONFIG; }
+  size_t C = std::max(std::max(1, a.G), cap);
+  if ((double)LT * C * (LA_MAX_NGRAM - 1) * 4 > (double)(1ull << 30)) {
+    la_set_error("pool capacity %d: per-lead buckets would need %.1f GB", cap,
+                 (double)LT * C * (LA_MAX_NGRAM - 1) * 4 / 1e9);
+    return LA_ERR_UNSUPPORTED;
+  }
   size_t logc = (size_t)inserts + 1;
   if (!e->p_lead || LT > e->p_lt || ST > e->p_st || C > e->p_C || logc > e->p_log_cap) {
-    for (int* p : {e->p_lead, e->p_cnt, e->p_suf, e->p_set, e->p_counters, e->p_log}) {
+    for (int* p : {e->p_lead, e->p_cnt, e->p_suf, e->p_set, e->p_counters, e->p_log, e->p_stamp,
+                   e->p_fifo}) {
       if (!p) continue;
       auto it = std::find(e->owned.begin(), e->owned.end(), (void*)p);
       if (it != e->owned.end()) e->owned.erase(it);
@@ -373,9 +384,11 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
     RET_IF(dalloc(e, &e->p_set, ST * LA_MAX_NGRAM));
     RET_IF(dalloc(e, &e->p_counters, 4));
     RET_IF(dalloc(e, &e->p_log, logc * LA_MAX_NGRAM));
+    RET_IF(dalloc(e, &e->p_stamp, ST));
+    RET_IF(dalloc(e, &e->p_fifo, logc));
     e->p_lt = LT; e->p_st = ST; e->p_C = C; e->p_N = LA_MAX_NGRAM; e->p_log_cap = logc;
   }
-  C = std::max(1, a.G);
+  C = std::max(std::max(1, a.G), cap);
   LT = e->p_lt; ST = e->p_st;
   CK(cudaMemsetAsync(e->p_lead, 0xff, LT * sizeof(int), st));
   CK(cudaMemsetAsync(e->p_cnt, 0, LT * sizeof(int), st));
@@ -415,6 +428,7 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
   d.pool.log_cap = (int)e->p_log_cap;
   d.pool.lead_keys = e->p_lead; d.pool.bkt_cnt = e->p_cnt; d.pool.bkt_suf = e->p_suf;
   d.pool.set_keys = e->p_set; d.pool.counters = e->p_counters; d.pool.log = e->p_log;
+  d.pool.capacity = cap; d.pool.set_stamp = e->p_stamp; d.pool.fifo = e->p_fifo;
   if (a.smp) {
     d.pcg = pcg_of(a.smp);
     d.pcg_window = a.pcg_window ? 1 : 0;

@@ -43,34 +43,150 @@ __device__ __forceinline__ int la_lead_find_or_add(const DevPool& p, int lead) {
   return -1;
 }
 
+// Bucket helpers for one warp; buckets are newest-first arrays of suffixes and
+// may exceed 32 entries in capacity mode, so every pass walks 32-entry chunks.
+// first index in [0, cnt) whose suffix equals `suf` (-1: none)
+static __device__ int la_bucket_find(const int* B, int cnt, int S, const int* suf, int lane) {
+  for (int base = 0; base < cnt; base += 32) {
+    bool match = false;
+    if (base + lane < cnt) {
+      match = true;
+      for (int s = 0; s < S; ++s) match &= (B[(base + lane) * S + s] == suf[s]);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, match);
+    if (m) return base + __ffs(m) - 1;
+  }
+  return -1;
+}
+
+// entries [0, upto) move down one slot (top chunk first: no overwrite before read)
+static __device__ void la_bucket_shift_down(int* B, int upto, int S, int lane) {
+  int tmp[LA_MAX_SUFFIX];
+  for (int base = ((upto - 1) >> 5) << 5; base >= 0 && upto > 0; base -= 32) {
+    const bool mv = base + lane < upto;
+    if (mv)
+      for (int s = 0; s < S; ++s) tmp[s] = B[(base + lane) * S + s];
+    __syncwarp();
+    if (mv)
+      for (int s = 0; s < S; ++s) B[(base + lane + 1) * S + s] = tmp[s];
+    __syncwarp();
+  }
+}
+
+// entries (v, cnt) move up one slot (bottom chunk first), dropping entry v
+static __device__ void la_bucket_remove(int* B, int cnt, int v, int S, int lane) {
+  int tmp[LA_MAX_SUFFIX];
+  for (int base = v + 1; base < cnt; base += 32) {
+    const bool mv = base + lane < cnt;
+    if (mv)
+      for (int s = 0; s < S; ++s) tmp[s] = B[(base + lane) * S + s];
+    __syncwarp();
+    if (mv)
+      for (int s = 0; s < S; ++s) B[(base + lane - 1) * S + s] = tmp[s];
+    __syncwarp();
+  }
+}
+
+// distinct-set probe in capacity mode: a live entry equal to g (returns its
+// slot, *free_slot untouched) or -1 with *free_slot = the first empty or
+// evicted slot on g's probe path
+static __device__ int la_set_find_live(const DevPool& p, const int* g, int N, int* free_slot) {
+  uint32_t h = la_gram_hash(g, N) & (uint32_t)p.st_mask;
+  *free_slot = -1;
+  for (int probe = 0; probe <= p.st_mask; ++probe) {
+    const int* key = p.set_keys + (size_t)h * N;
+    if (key[0] < 0) {
+      if (*free_slot < 0) *free_slot = (int)h;
+      return -1;
+    }
+    if (p.set_stamp[h] < 0) {
+      if (*free_slot < 0) *free_slot = (int)h;
+    } else {
+      bool eq = true;
+      for (int i = 0; i < N; ++i) eq &= (key[i] == g[i]);
+      if (eq) return (int)h;
+    }
+    h = (h + 1) & (uint32_t)p.st_mask;
+  }
+  return -1;
+}
+
 // One n-gram insert by one warp (reference pool.py:41-61): dedup on
-// (lead, suffix) with recency refresh, newest-first bucket, distinct count.
-// `g` may live in shared or global memory.
+// (lead, suffix) with recency refresh, newest-first bucket, distinct count,
+// and with a capacity the globally least-recently-touched entry is evicted
+// before a new one is added.  `g` may live in shared or global memory.
 static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int lane, int* overflow) {
   const int N = p.ngram, S = N - 1, C = p.C;
   int gl[LA_MAX_SUFFIX + 1];
 #pragma unroll
   for (int i = 0; i < LA_MAX_SUFFIX + 1; ++i) gl[i] = (i < N) ? g[i] : 0;
-  int slot = 0;
+  int slot = 0, victim = -1;
+  int vkey[LA_MAX_SUFFIX + 1];   // the victim's n-gram (its set slot may be reused below)
+#pragma unroll
+  for (int i = 0; i < LA_MAX_SUFFIX + 1; ++i) vkey[i] = 0;
   if (lane == 0) {
-    // distinct set (len(pool))
-    uint32_t h = la_gram_hash(gl, N) & (uint32_t)p.st_mask;
-    bool placed = false;
-    for (int probe = 0; probe <= p.st_mask; ++probe) {
-      int* key = p.set_keys + (size_t)h * N;
-      if (key[0] < 0) {
-        for (int i = 0; i < N; ++i) key[i] = gl[i];
-        p.counters[0] += 1;
-        placed = true;
-        break;
+    if (p.capacity == 0) {
+      // distinct set (len(pool))
+      uint32_t h = la_gram_hash(gl, N) & (uint32_t)p.st_mask;
+      bool placed = false;
+      for (int probe = 0; probe <= p.st_mask; ++probe) {
+        int* key = p.set_keys + (size_t)h * N;
+        if (key[0] < 0) {
+          for (int i = 0; i < N; ++i) key[i] = gl[i];
+          p.counters[0] += 1;
+          placed = true;
+          break;
+        }
+        bool eq = true;
+        for (int i = 0; i < N; ++i) eq &= (key[i] == gl[i]);
+        if (eq) { placed = true; break; }
+        h = (h + 1) & (uint32_t)p.st_mask;
       }
-      bool eq = true;
-      for (int i = 0; i < N; ++i) eq &= (key[i] == gl[i]);
-      if (eq) { placed = true; break; }
-      h = (h + 1) & (uint32_t)p.st_mask;
+      if (!placed) *overflow = 1;
+    } else {
+      int free_slot;
+      int h = la_set_find_live(p, gl, N, &free_slot);
+      if (h < 0) {
+        if (p.counters[0] >= p.capacity) {
+          // _entries.popitem(last=False): the oldest FIFO record still current
+          int head = p.counters[3];
+          while (head < p.counters[2]) {
+            const int v = p.fifo[head];
+            const int st = p.set_stamp[v];
+            ++head;
+            if (st == head - 1) { victim = v; break; }
+          }
+          p.counters[3] = head;
+          if (victim >= 0) {
+            for (int i = 0; i < N; ++i) vkey[i] = p.set_keys[(size_t)victim * N + i];
+            p.set_stamp[victim] = -1;
+            p.counters[0] -= 1;
+            // the victim's slot may be the first free one on our probe path
+            la_set_find_live(p, gl, N, &free_slot);
+          } else {
+            *overflow = 1;
+          }
+        }
+        h = free_slot;
+        if (h >= 0) {
+          int* key = p.set_keys + (size_t)h * N;
+          for (int i = 0; i < N; ++i) key[i] = gl[i];
+          p.counters[0] += 1;
+        } else {
+          *overflow = 1;
+        }
+      }
+      const int stamp = p.counters[2];
+      if (h >= 0 && stamp < p.log_cap) {
+        p.set_stamp[h] = stamp;
+        p.fifo[stamp] = h;
+        p.counters[2] = stamp + 1;
+      } else {
+        *overflow = 1;
+      }
     }
     slot = la_lead_find_or_add(p, gl[0]);
-    if (!placed || slot < 0) *overflow = 1;
+    if (slot < 0) *overflow = 1;
     int n = p.counters[1];
     if (n < p.log_cap) {
       for (int i = 0; i < N; ++i) p.log[(size_t)n * N + i] = gl[i];
@@ -80,24 +196,33 @@ static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int l
     }
   }
   slot = __shfl_sync(0xffffffffu, slot, 0);
-  if (slot < 0) return;
+  victim = __shfl_sync(0xffffffffu, victim, 0);
+#pragma unroll
+  for (int i = 0; i < LA_MAX_SUFFIX + 1; ++i) vkey[i] = __shfl_sync(0xffffffffu, vkey[i], 0);
   __syncwarp();
-  int cnt = p.bkt_cnt[slot];
-  int* B = p.bkt_suf + (size_t)slot * C * S;
-  bool match = false;
-  if (lane < cnt) {
-    match = true;
-    for (int s = 0; s < S; ++s) match &= (B[lane * S + s] == gl[1 + s]);
+  if (victim >= 0) {
+    // del old_bucket[old_suffix] (pool.py:54-58)
+    const int* vs = vkey + 1;
+    int vslot = 0;
+    if (lane == 0) vslot = la_lead_find(p, vkey[0]);
+    vslot = __shfl_sync(0xffffffffu, vslot, 0);
+    if (vslot >= 0) {
+      int* VB = p.bkt_suf + (size_t)vslot * C * S;
+      const int vcnt = p.bkt_cnt[vslot];
+      const int at = la_bucket_find(VB, vcnt, S, vs, lane);
+      if (at >= 0) {
+        la_bucket_remove(VB, vcnt, at, S, lane);
+        if (lane == 0) p.bkt_cnt[vslot] = vcnt - 1;
+      }
+    }
+    __syncwarp();
   }
-  unsigned m = __ballot_sync(0xffffffffu, match);
-  int pos = m ? (__ffs(m) - 1) : -1;
-  int upto = pos >= 0 ? pos : min(cnt, C - 1);   // entries [0, upto) move down one
-  int tmp[LA_MAX_SUFFIX];
-  if (lane < upto)
-    for (int s = 0; s < S; ++s) tmp[s] = B[lane * S + s];
-  __syncwarp();
-  if (lane < upto)
-    for (int s = 0; s < S; ++s) B[(lane + 1) * S + s] = tmp[s];
+  if (slot < 0) return;
+  const int cnt = p.bkt_cnt[slot];
+  int* B = p.bkt_suf + (size_t)slot * C * S;
+  const int pos = la_bucket_find(B, cnt, S, gl + 1, lane);
+  const int upto = pos >= 0 ? pos : min(cnt, C - 1);   // entries [0, upto) move down one
+  la_bucket_shift_down(B, upto, S, lane);
   if (lane == 0) {
     for (int s = 0; s < S; ++s) B[s] = gl[1 + s];
     if (pos < 0) p.bkt_cnt[slot] = min(cnt + 1, C);

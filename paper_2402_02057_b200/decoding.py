@@ -114,9 +114,6 @@ def _prepare_lookahead(model, prompt, config, sampler, pool):
     p = _prompt(prompt)
     if pool is not None and pool.ngram != config.ngram:
         raise ValueError("pool n-gram size does not match the generation config")
-    if pool is not None and pool.capacity is not None:
-        raise NotImplementedError("NGramPool(capacity=...) global LRU eviction is not "
-                                  "implemented on the device pool")
     init = None
     if pool is not None and len(pool):
         init = np.ascontiguousarray(np.asarray(pool.entries_oldest_first(), dtype=np.int32))
@@ -135,6 +132,7 @@ def _prepare_lookahead(model, prompt, config, sampler, pool):
     n_seed = max(0, len(p) - config.ngram + 1) if config.seed_pool_from_prompt else 0
     log_cap = n_seed + config.max_tokens * config.window + 1
     io = _IO(p, config.max_tokens, rng, init, config.ngram, log_cap)
+    io.io.pool_capacity = 0 if pool is None or pool.capacity is None else int(pool.capacity)
     io.sampler = dev_sampler
     return io
 
@@ -265,9 +263,6 @@ def start_session(model, prompt: Sequence[int], config: GenerationConfig, sample
         pool = NGramPool(config.ngram)
     elif pool.ngram != config.ngram:
         raise ValueError("pool n-gram size does not match the generation config")
-    if pool.capacity is not None:
-        raise NotImplementedError("NGramPool(capacity=...) global LRU eviction is not "
-                                  "implemented on the device pool")
     init = None
     if len(pool):
         init = np.ascontiguousarray(np.asarray(pool.entries_oldest_first(), dtype=np.int32))
@@ -277,6 +272,7 @@ def start_session(model, prompt: Sequence[int], config: GenerationConfig, sample
     stream = np.ascontiguousarray(cells if ncell else np.zeros(1, dtype=np.int32))
     n_seed = max(0, len(p) - config.ngram + 1) if config.seed_pool_from_prompt else 0
     io = _IO(p, 1, stream, init, config.ngram, 1)
+    io.io.pool_capacity = 0 if pool.capacity is None else int(pool.capacity)
     smp = _lib.make_sampler(sampler.temperature, sampler.top_k, sampler.top_p, rng)
     _lib.check(m.lib.la_session_start(m.engine(), C.byref(_gen_config(config)),
                                       1 if sampler.mode == "greedy" else 0, C.byref(smp),

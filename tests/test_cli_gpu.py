@@ -1,7 +1,7 @@
 """The CLI (cli.py, reference cli.py:1-333): every report file of the
 reference's own CLI runs (tests/golden/cli.json) reproduced byte for byte by
 the B200 engine on the same argv -- greedy and temperature lookahead,
-autoregressive, Jacobi, bench and LP simulate."""
+autoregressive, Jacobi, bench, LP simulate and an LRU-capped pool."""
 
 import os
 from pathlib import Path
@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 cli = pytest.importorskip("paper_2402_02057_b200.cli")
 
 
-@pytest.mark.parametrize("idx", range(6))
+@pytest.mark.parametrize("idx", range(7))
 def test_cli_reports_match_reference_byte_for_byte(idx, tmp_path, monkeypatch):
     g = load_golden("cli.json")
     case = g["cases"][idx]

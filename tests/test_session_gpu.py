@@ -115,3 +115,34 @@ def test_bf16_session_equals_whole_decode():
             assert len(steps) == met.steps
     finally:
         m.close()
+
+
+@pytest.mark.parametrize("cap", [1, 2, 5, 13, 40])
+def test_lru_capped_pool_matches_oracle(models, cap):
+    """NGramPool(capacity=...) global LRU eviction (pool.py:41-61) on the device
+    pool: per-step candidate counts and pool sizes, the decode, and the
+    caller pool afterwards equal the oracle's (itself pinned to the
+    reference's capped-pool golden streams)."""
+    from oracle import lookahead_oracle as lo
+    from oracle.model_oracle import TinyTransformerOracle
+    for (mseed, V), (W, N, G) in [((11, 12), (5, 3, 5)), ((3, 16), (7, 4, 7)), ((0, 256), (15, 5, 15))]:
+        m = models(mseed, V)
+        orc = TinyTransformerOracle(mseed, V)
+        prompt = [int(t) for t in np.random.default_rng(cap + V).integers(0, V, 12)]
+        cfg = la.GenerationConfig(window=W, ngram=N, max_candidates=G, max_tokens=40,
+                                  seed_pool_from_prompt=True)
+        opool = lo.OraclePool(N, capacity=cap)
+        run = lo.decode_lookahead(orc, prompt, W, N, G, 40, seed=cap, seed_pool=True, pool=opool)
+        pool = la.NGramPool(N, capacity=cap)
+        toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=cap), pool=pool)
+        assert toks == run.tokens
+        assert met.steps == len(run.steps)
+        assert met.total_queries == sum(s.query_count for s in run.steps)
+        assert len(pool) == len(opool) <= cap
+        for t in range(V):
+            assert pool.lookup(t, G) == opool.lookup(t, G), (mseed, t)
+        # per step, through a session
+        out, steps, state = _run_steps(m, prompt, cfg, la.SamplerSpec("greedy", seed=cap),
+                                       pool=la.NGramPool(N, capacity=cap))
+        assert [(s["c"], s["pool"], len(s["accepted"])) for s in steps] == \
+            [(s.candidate_count, s.pool_size, len(s.accepted)) for s in run.steps]
