@@ -45,4 +45,4 @@ struct LaAttnFusedArgs {
 };
 
 __global__ void la_attn_fused_kernel(LaAttnFusedArgs a);
-size_t la_attn_fused_smem();
+size_t la_attn_fused_smem(bool tc);

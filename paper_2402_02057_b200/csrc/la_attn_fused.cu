@@ -36,6 +36,7 @@ constexpr int kTcTiles = 6;
 constexpr int kTcQ = 0, kTcK = 32768, kTcV = kTcK + kTcTiles * 16384;
 constexpr int kTcSmem = kTcV + kTcTiles * 16384;                   // 224 KB
 constexpr int kMaskOff = kTcSmem > kStages * kTileBytes ? kTcSmem : kStages * kTileBytes;
+constexpr int kMaskOffMma = kStages * kTileBytes;   // mma.sync-only launches
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -115,7 +116,9 @@ __device__ __forceinline__ void wmark(const LaAttnFusedArgs& a, int v) {
 
 }  // namespace
 
-size_t la_attn_fused_smem() { return (size_t)kMaskOff + LA_MAX_ROWS * 4 * 4 + 64; }
+size_t la_attn_fused_smem(bool tc) {
+  return (size_t)(tc ? kMaskOff : kMaskOffMma) + LA_MAX_ROWS * 4 * 4 + 64;
+}
 
 // ---------------------------------------------------------------------------
 // Tensor-core chunk unit: S = Q K^T (tcgen05, M = 128 query rows, N = 64 keys
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sKV = smem;                                                   // [kStages][K | V]
-  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + kMaskOff);    // [128][4]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + (a.tc ? kMaskOff : kMaskOffMma));   // [128][4]
   int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
   uint64_t* sBars = reinterpret_cast<uint64_t*>(sFlag + 4);           // tensor-core path
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBars + 2);

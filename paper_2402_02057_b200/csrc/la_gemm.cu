@@ -139,16 +139,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     la_gemm_kernel(const LaGemmArgs args) {
+  const unsigned long long t_entry = args.trace ? globaltimer() : 0ull;   // trace: CTA start
   extern __shared__ uint8_t smem_raw[];
   const FwdPlan* P = args.plan;
   uint8_t* sm = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = sm;
   // one 192 KB ring: nst stages of (weights a_bytes | step rows 16 KB), the
   // weight and row halves in two contiguous regions (1024-B aligned)
-  const int nst = args.tpc == LA_TPC ? kStages : kMaxStages;
+  const int nst = args.nst > 0 ? args.nst : (args.tpc == LA_TPC ? kStages : kMaxStages);
   const uint32_t a_stage = (uint32_t)args.tpc * kTileBytes;
   uint8_t* sB = sA + nst * a_stage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sA + kStages * (kABytes + kBBytes));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + nst * (a_stage + kBBytes));
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
@@ -203,7 +204,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (long u = u_begin + n_pre; u < min(u_end, u_begin + n_pre + args.l2pf); ++u)
       ptx::bulk_prefetch_l2(a_src(u), a_bytes);
   }
-  const unsigned long long t_entry = args.trace ? globaltimer() : 0ull;
   la_pdl_wait();
   if (args.timing && threadIdx.x == 0) {
     if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();
@@ -450,7 +450,11 @@ static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), kSmemBytes, st, pdl, g.args);
+  // the ring (nst stages), barriers / TMEM slot, and the fused epilogue's staging
+  const int nst = g.args.nst > 0 ? g.args.nst : (g.args.tpc == LA_TPC ? kStages : kMaxStages);
+  const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + kBBytes) + 2 * kMaxStages * 8 +
+                      4 * 8 + 16 + (EPI == LA_EPI_PARTIAL ? 0 : 128 * kEpiLd * 4 + 128 * 4);
+  return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
 }
 
 int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {

@@ -48,6 +48,8 @@ struct LaGemmArgs {
   unsigned long long* trace;
   int debug;   // experiments: bit0 skip step-row loads, bit1 skip MMAs
   int l2pf;    // units beyond the smem ring prefetched to L2 before the dependency wait
+  int nst;     // smem ring stages (0: the default for tpc); fewer stages = a smaller CTA
+               // that fits beside the previous kernel's CTA and streams its weights early
   // ---- fused epilogue (LA_EPI_QKV / SWIGLU / LOGITS): stream-K fix-up in
   // the GEMM -- the CTA owning a tile's k = 0 piece adds the other pieces'
   // partials (in piece order) and applies the epilogue

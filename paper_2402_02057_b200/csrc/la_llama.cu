@@ -346,6 +346,16 @@ int llama_create(la_engine* e) {
     fin(p->qkv[l], 0, 0); fin(p->o[l], 1, 1); fin(p->gu[l], 2, 2); fin(p->down[l], 1, 4);
   }
   for (int l = 0; l < D.layers; ++l) { p->qkv[l].args.nrm = p->nrm; p->gu[l].args.nrm = p->nrm; }
+  {
+    // O projection ring depth (LA_O_STAGES; 0 = the default 4 stages).  A
+    // 3-stage ring fits beside an attention CTA register-wise only when the
+    // attention kernel is capped at <= 184 registers (per-SM-sub-partition
+    // register files: 2 warps x 32 x (attention + GEMM regs) <= 16384); that
+    // configuration co-resided on only part of the SMs and measured no gain.
+    const int ost = getenv("LA_O_STAGES") ? atoi(getenv("LA_O_STAGES")) : 0;
+    for (int l = 0; l < D.layers; ++l)
+      if (p->o[l].args.tpc == LA_TPC) p->o[l].args.nst = ost;
+  }
   p->head.args.nrm = p->nrm;
   fin(p->head, 3, 3);
   CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
@@ -400,7 +410,7 @@ int llama_create(la_engine* e) {
       }
     }
     ce = cudaFuncSetAttribute(la_attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)la_attn_fused_smem());
+                              (int)la_attn_fused_smem(true));
     if (ce != cudaSuccess) { la_set_error("fused attn smem attr: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
   }
   p->mega = getenv("LA_MEGA") && atoi(getenv("LA_MEGA")) == 1;
@@ -556,7 +566,7 @@ static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
                      p->rope_sin, p->H, p->KVH, p->nrm};
   }
   KT_BEGIN(st);
-  CK(la_launch(la_attn_fused_kernel, dim3(p->KVH * a.nrb_max * (a.S + 1)), dim3(256), la_attn_fused_smem(), st,
+  CK(la_launch(la_attn_fused_kernel, dim3(p->KVH * a.nrb_max * (a.S + 1)), dim3(256), la_attn_fused_smem(a.tc != 0), st,
                p->pdl, a));
   KT_END(st, "attn_fused");
   return LA_OK;
