@@ -672,8 +672,13 @@ extern "C" int32_t la_adjust_distributions(la_engine* e, const double* probs, in
   RET_IF(dgrow(e, &e->d_flag, &e->flag_cap, (size_t)n_rows));
   CK(cudaMemcpyAsync(e->d_adj, probs, (size_t)n_rows * V * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(e->d_flag, 0, (size_t)n_rows * 4, st));
-  la_adjust_probs_kernel<<<n_rows, 1024, 0, st>>>(e->d_adj, V, s->temperature, s->top_k, s->top_p,
-                                                  e->d_flag);
+  // LA_ADJ_HOOK_CLUSTER=1: the bf16 path's cluster-scope kernel instead of one CTA per row
+  if (getenv("LA_ADJ_HOOK_CLUSTER") && atoi(getenv("LA_ADJ_HOOK_CLUSTER")) == 1)
+    la_adjust_probs_cluster_kernel<<<n_rows * LA_ADJ_CLUSTER, LA_ADJ_THREADS, 0, st>>>(
+        e->d_adj, V, s->temperature, s->top_k, s->top_p, e->d_flag);
+  else
+    la_adjust_probs_kernel<<<n_rows, 1024, 0, st>>>(e->d_adj, V, s->temperature, s->top_k, s->top_p,
+                                                    e->d_flag);
   CK(cudaGetLastError());
   std::vector<int> flags(n_rows);
   CK(cudaMemcpyAsync(out, e->d_adj, (size_t)n_rows * V * 8, cudaMemcpyDeviceToHost, st));

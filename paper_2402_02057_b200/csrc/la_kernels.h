@@ -16,6 +16,11 @@ __global__ void la_kv_unpack_kernel(const DevDecode* dp, const uint8_t* gathered
                                     int row_bytes);
 __global__ void la_sample_adjust_kernel(DevDecode* dp);
 __global__ void la_sample_verify_kernel(DevDecode* dp);
+#define LA_ADJ_CLUSTER 8      // CTAs per adjusted row (bf16 path)
+#define LA_ADJ_THREADS 512
+__global__ void la_sample_adjust_cluster_kernel(DevDecode* dp);
+__global__ void la_adjust_probs_cluster_kernel(double* rows, int V, double temperature, int top_k,
+                                               double top_p, int* degenerate);
 __global__ void la_adjust_probs_kernel(double* rows, int V, double temperature, int top_k,
                                        double top_p, int* degenerate);
 __global__ void la_verify_hook_kernel(DevDecode* dp);

@@ -738,7 +738,8 @@ static int record_step(la_engine* e, cudaStream_t st, bool finish, int* nk) {
     const int rows = h.mode == LA_MODE_LOOKAHEAD ? 1 + h.G * (h.N - 1) : 1;
     {
       KT_BEGIN(st);
-      CK(la_launch(la_sample_adjust_kernel, dim3(rows), dim3(1024), 0, st, p->pdl, e->d_dec));
+      CK(la_launch(la_sample_adjust_cluster_kernel, dim3(rows * LA_ADJ_CLUSTER), dim3(LA_ADJ_THREADS), 0,
+                   st, p->pdl, e->d_dec));
       KT_END(st, "sample_adjust");
     }
     KT_BEGIN(st);

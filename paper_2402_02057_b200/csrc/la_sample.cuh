@@ -80,6 +80,9 @@ __host__ __device__ __forceinline__ int la_pcg_integers(LaPcg64& g, unsigned hig
 struct LaSampleSmem {
   unsigned long long hist[32][16];   // per-warp radix histograms (4-bit digits)
   unsigned long long tot[16];
+  unsigned long long gtot[16];       // cluster scope: histogram summed over the cluster
+  double xd;                         // cluster scope: this CTA's published partial
+  long long xl;
   double red[32];
   unsigned long long ured[32];
   int ired[32];
@@ -151,6 +154,85 @@ __device__ __forceinline__ int la_bscan_i(int v, LaSampleSmem& sm) {
   return base + inc - v;
 }
 
+// Reduction scopes of the row functions below.  A row is processed by one
+// CTA (LaBlockScope: the fp32 single-CTA decode, parity hooks) or by the CTAs
+// of a thread-block cluster, each owning a contiguous slice of the vocabulary
+// (LaClusterScope: the bf16 path's adjust kernel).  Cluster partials are
+// exchanged through distributed shared memory and combined in rank order, so
+// results are deterministic; every call is collective over the scope.
+struct LaBlockScope {
+  int lo, hi;   // [0, V)
+  __device__ double sum(double v, LaSampleSmem&) const { return v; }
+  __device__ float max(float v, LaSampleSmem&) const { return v; }
+  __device__ void combine16(LaSampleSmem&) const {}
+  __device__ long long prefix(long long, LaSampleSmem&) const { return 0; }
+};
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ void la_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <typename T>
+__device__ __forceinline__ T la_dsmem_ld(const T* local, unsigned rank) {
+  // address of `local`'s counterpart in CTA `rank` of the cluster
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(local), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  T v;
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long u;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(u) : "r"(r) : "memory");
+    memcpy(&v, &u, 8);
+  } else {
+    unsigned u;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(u) : "r"(r) : "memory");
+    memcpy(&v, &u, 4);
+  }
+  return v;
+}
+
+struct LaClusterScope {
+  int lo, hi;             // this CTA's slice
+  unsigned rank, size;
+  __device__ double sum(double v, LaSampleSmem& sm) const {
+    if (threadIdx.x == 0) sm.xd = v;
+    la_cluster_sync();
+    double t = 0.0;
+    for (unsigned r = 0; r < size; ++r) t += la_dsmem_ld(&sm.xd, r);
+    la_cluster_sync();
+    return t;
+  }
+  __device__ float max(float v, LaSampleSmem& sm) const {
+    if (threadIdx.x == 0) sm.xd = (double)v;
+    la_cluster_sync();
+    float t = -INFINITY;
+    for (unsigned r = 0; r < size; ++r) t = fmaxf(t, (float)la_dsmem_ld(&sm.xd, r));
+    la_cluster_sync();
+    return t;
+  }
+  // sm.tot[16] (this CTA) -> sm.tot[16] (whole cluster)
+  __device__ void combine16(LaSampleSmem& sm) const {
+    la_cluster_sync();
+    if (threadIdx.x < 16) {
+      unsigned long long t = 0ull;
+      for (unsigned r = 0; r < size; ++r) t += la_dsmem_ld(&sm.tot[threadIdx.x], r);
+      sm.gtot[threadIdx.x] = t;
+    }
+    la_cluster_sync();
+    if (threadIdx.x < 16) sm.tot[threadIdx.x] = sm.gtot[threadIdx.x];
+    __syncthreads();
+  }
+  // exclusive prefix over the cluster's ranks of a per-CTA value
+  __device__ long long prefix(long long v, LaSampleSmem& sm) const {
+    if (threadIdx.x == 0) sm.xl = v;
+    la_cluster_sync();
+    long long t = 0;
+    for (unsigned r = 0; r < rank; ++r) t += la_dsmem_ld(&sm.xl, r);
+    la_cluster_sync();
+    return t;
+  }
+};
+#endif
+
 __device__ __forceinline__ unsigned long long la_pbits(double p) {
   return (unsigned long long)__double_as_longlong(p);   // p >= 0: order preserving
 }
@@ -162,17 +244,19 @@ __device__ __forceinline__ unsigned long long la_pbits(double p) {
 // counted in per-thread registers and reduced by warp shuffles: near-uniform
 // distributions put almost every element in the same top digits, where
 // shared-memory atomics would serialise the CTA on one address.
-static __device__ bool la_radix_select(const double* p, int V, bool mass, double scale,
+template <typename Scope>
+static __device__ bool la_radix_select(const double* p, const Scope& sc, bool mass, double scale,
                                 unsigned long long need, LaSampleSmem& sm,
                                 unsigned long long* T, unsigned long long* above) {
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
+  const int V = sc.hi;
   const int nw = nth >> 5;
   unsigned long long prefix = 0ull, mask = 0ull, acc_above = 0ull;
   for (int shift = 60; shift >= 0; shift -= 4) {
     unsigned long long loc[16];
 #pragma unroll
     for (int d = 0; d < 16; ++d) loc[d] = 0ull;
-    for (int i0 = tid; i0 < V; i0 += 8 * nth) {
+    for (int i0 = sc.lo + tid; i0 < V; i0 += 8 * nth) {
       double vb[8];   // 8 loads in flight per thread (the pass is L2-latency bound)
 #pragma unroll
       for (int u = 0; u < 8; ++u) vb[u] = (i0 + u * nth < V) ? p[i0 + u * nth] : -1.0;
@@ -206,6 +290,7 @@ static __device__ bool la_radix_select(const double* p, int V, bool mass, double
       sm.tot[tid] = t;
     }
     __syncthreads();
+    sc.combine16(sm);
     if (tid == 0) {
       unsigned long long acc = acc_above;
       int sel = -1;
@@ -230,13 +315,16 @@ static __device__ bool la_radix_select(const double* p, int V, bool mass, double
 
 // keep p[i] with value key > T, and the first `m` (lowest ids) with key == T;
 // zero the rest (the (-p, id) order prefix of lexsort, sampling.py:43)
-static __device__ void la_keep_prefix(double* p, int V, unsigned long long T, long long m,
+template <typename Scope>
+static __device__ void la_keep_prefix(double* p, const Scope& sc, unsigned long long T, long long m,
                                LaSampleSmem& sm) {
-  const int chunk = (V + blockDim.x - 1) / blockDim.x;
-  const int lo = min(V, (int)threadIdx.x * chunk), hi = min(V, lo + chunk);
+  const int n = sc.hi - sc.lo;
+  const int chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = sc.lo + min(n, (int)threadIdx.x * chunk), hi = min(sc.hi, lo + chunk);
   int ties = 0;
   for (int i = lo; i < hi; ++i) ties += la_pbits(p[i]) == T;
   long long r = la_bscan_i(ties, sm);
+  r += sc.prefix((long long)la_bsum_d((double)ties, sm), sm);   // ties in lower-ranked slices
   for (int i = lo; i < hi; ++i) {
     const unsigned long long b = la_pbits(p[i]);
     bool keep = b > T;
@@ -250,25 +338,27 @@ static __device__ void la_keep_prefix(double* p, int V, unsigned long long T, lo
 // the model's probabilities are exp(l - max) / sum, models.py:268-271).
 // lg == nullptr: out[] already holds the probabilities.  Returns false
 // (DegenerateDistributionError) when all mass is truncated.
-static __device__ bool la_adjust_row(const float* lg, int V, double temperature, int top_k, double top_p,
-                              double* out, LaSampleSmem& sm) {
+template <typename Scope>
+static __device__ bool la_adjust_row_s(const float* lg, const Scope& sc, int V, double temperature,
+                                       int top_k, double top_p, double* out, LaSampleSmem& sm) {
   const int tid = threadIdx.x, nth = blockDim.x;
+  const int lo = sc.lo, hi = sc.hi;
   double Z = 1.0;
   if (lg) {
     float mx = -INFINITY;
-    for (int i = tid; i < V; i += nth) mx = fmaxf(mx, lg[i]);
-    mx = la_bmax_f(mx, sm);
+    for (int i = lo + tid; i < hi; i += nth) mx = fmaxf(mx, lg[i]);
+    mx = sc.max(la_bmax_f(mx, sm), sm);
     double s = 0.0;
-    for (int i = tid; i < V; i += nth) {
+    for (int i = lo + tid; i < hi; i += nth) {
       const double e = exp((double)lg[i] - (double)mx);
       out[i] = e;
       s += e;
     }
-    Z = la_bsum_d(s, sm);
+    Z = sc.sum(la_bsum_d(s, sm), sm);
   }
   const bool powr = temperature != 1.0;
   const double inv = 1.0 / temperature;
-  for (int i = tid; i < V; i += nth) {
+  for (int i = lo + tid; i < hi; i += nth) {
     double p = lg ? out[i] / Z : out[i];
     if (powr) p = pow(p, inv);
     out[i] = p;
@@ -276,30 +366,35 @@ static __device__ bool la_adjust_row(const float* lg, int V, double temperature,
   __syncthreads();
   unsigned long long T, above;
   if (top_k > 0 && top_k < V) {
-    if (la_radix_select(out, V, false, 0.0, (unsigned long long)top_k, sm, &T, &above))
-      la_keep_prefix(out, V, T, (long long)top_k - (long long)above, sm);
+    if (la_radix_select(out, sc, false, 0.0, (unsigned long long)top_k, sm, &T, &above))
+      la_keep_prefix(out, sc, T, (long long)top_k - (long long)above, sm);
   }
   if (top_p < 1.0) {
     double t = 0.0;
-    for (int i = tid; i < V; i += nth) t += out[i];
-    t = la_bsum_d(t, sm);
+    for (int i = lo + tid; i < hi; i += nth) t += out[i];
+    t = sc.sum(la_bsum_d(t, sm), sm);
     if (!(t > 0.0)) return false;
     const double one = 1152921504606846976.0;   // 2^60: the total's fixed-point weight
     const double scale = one / t;
     const unsigned long long need = (unsigned long long)ceil(top_p * one);
-    if (need > 0 && la_radix_select(out, V, true, scale, need, sm, &T, &above)) {
+    if (need > 0 && la_radix_select(out, sc, true, scale, need, sm, &T, &above)) {
       const unsigned long long f = (unsigned long long)(__longlong_as_double((long long)T) * scale);
       long long m = f ? (long long)((need - above + f - 1) / f) : 1;
-      la_keep_prefix(out, V, T, m < 1 ? 1 : m, sm);
+      la_keep_prefix(out, sc, T, m < 1 ? 1 : m, sm);
     }
   }
   double t = 0.0;
-  for (int i = tid; i < V; i += nth) t += out[i];
-  t = la_bsum_d(t, sm);
+  for (int i = lo + tid; i < hi; i += nth) t += out[i];
+  t = sc.sum(la_bsum_d(t, sm), sm);
   if (!(t > 0.0)) return false;
-  for (int i = tid; i < V; i += nth) out[i] = out[i] / t;
+  for (int i = lo + tid; i < hi; i += nth) out[i] = out[i] / t;
   __syncthreads();
   return true;
+}
+
+static __device__ bool la_adjust_row(const float* lg, int V, double temperature, int top_k, double top_p,
+                                     double* out, LaSampleSmem& sm) {
+  return la_adjust_row_s(lg, LaBlockScope{0, V}, V, temperature, top_k, top_p, out, sm);
 }
 
 // draw(p, rng): u = random(); first i with cumsum(p)[i] > u * cumsum(p)[-1]

@@ -27,8 +27,11 @@ def _spec(c, seed=None):
                           seed=c["seed"] if seed is None else seed)
 
 
-def test_adjusted_distribution_on_device(tiny):
-    """fp64 on both sides: same support, values within a few ulps (pow / sum order)."""
+@pytest.mark.parametrize("cluster", ["0", "1"])
+def test_adjusted_distribution_on_device(tiny, cluster, monkeypatch):
+    """fp64 on both sides: same support, values within a few ulps (pow / sum
+    order); one CTA per row (fp32 path) and the cluster-split row (bf16 path)."""
+    monkeypatch.setenv("LA_ADJ_HOOK_CLUSTER", cluster)
     for c in load_golden("sampling.json")["adjust"]:
         p = np.ascontiguousarray(np.array(c["probs"], dtype=np.float64)[None])
         out = np.zeros_like(p)
@@ -189,3 +192,23 @@ def test_verify_sample_edge_cases_on_device(tiny):
     dead = np.zeros(2)
     with pytest.raises(la.DegenerateDistributionError):
         _verify(tiny, dead, [((1,), [dead])], 0)
+
+
+@pytest.mark.parametrize("cluster", ["0", "1"])
+def test_adjusted_distribution_wide_vocab(tiny, cluster, monkeypatch):
+    """V = 32000 rows (slices of 4000 per cluster CTA) incl. ties, vs the oracle."""
+    from oracle.sampling_oracle import adjusted_distribution
+    monkeypatch.setenv("LA_ADJ_HOOK_CLUSTER", cluster)
+    rng = np.random.default_rng(9)
+    for T, k, tp in [(1.0, 50, None), (0.7, None, 0.9), (1.3, 1000, 0.5), (0.5, 7, 0.99)]:
+        p = rng.random(32000) ** 4
+        p[::97] = p[5]                       # a block of exact ties
+        p /= p.sum()
+        x = np.ascontiguousarray(p[None])
+        out = np.zeros_like(x)
+        smp = _lib.make_sampler(T, k, tp, np.random.default_rng(0))
+        _lib.check(tiny.lib.la_adjust_distributions(tiny.engine(), x.ctypes.data, 1, 32000,
+                                                    C.byref(smp), out.ctypes.data, tiny.stream()))
+        ref = adjusted_distribution(p, T, k, tp)
+        assert ((out[0] > 0) == (ref > 0)).all(), (T, k, tp)
+        np.testing.assert_allclose(out[0], ref, rtol=1e-11, atol=1e-300)
