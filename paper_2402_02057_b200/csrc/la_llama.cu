@@ -106,7 +106,7 @@ __global__ void la_set_cond_kernel(cudaGraphConditionalHandle h, const DevDecode
 // L2 traffic of the activations); one tile halves the split-K partial volume
 // of the narrow projections (O, down: only d/128 tiles for 148 SMs).
 static int build_gemm(LaGemm& g, const void* a_packed, int n_tiles, const void* b, int K, int tpc,
-                      int epi = LA_EPI_PARTIAL) {
+                      int epi = LA_EPI_PARTIAL, int max_grid = 0) {
   memset(&g, 0, sizeof(g));
   g.epi = epi;
   n_tiles = (n_tiles + LA_TPC - 1) / LA_TPC * LA_TPC;   // packed buffers carry zero tiles
@@ -116,7 +116,7 @@ static int build_gemm(LaGemm& g, const void* a_packed, int n_tiles, const void* 
   g.args.tpc = tpc;
   g.args.kb = K / 64;
   long U = (long)(n_tiles / tpc) * g.args.kb;
-  g.grid = (int)std::min<long>(la_sm_count(), U);
+  g.grid = (int)std::min<long>(max_grid > 0 ? std::min(max_grid, la_sm_count()) : la_sm_count(), U);
   g.args.max_segs = la_gemm_workspace_segs(n_tiles, g.args.kb, g.grid, tpc);
   return LA_OK;
 }
@@ -314,12 +314,15 @@ int llama_create(la_engine* e) {
       q.H = H; q.KVH = KVH;
     }
     track(p->qkv[l]);
-    RET_IF(build_gemm(p->o[l], w.wo, d / 128, p->attn, H * 128, narrow_tpc));
+    // LA_O_GRID / LA_DOWN_GRID: fewer CTAs = fewer split-K pieces per tile (experiment)
+    static const int o_grid = getenv("LA_O_GRID") ? atoi(getenv("LA_O_GRID")) : 0;
+    RET_IF(build_gemm(p->o[l], w.wo, d / 128, p->attn, H * 128, narrow_tpc, LA_EPI_PARTIAL, o_grid));
     track(p->o[l]);
     RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d, LA_TPC, fused ? LA_EPI_SWIGLU : LA_EPI_PARTIAL));
     p->gu[l].args.act = p->act;
     track(p->gu[l]);
-    RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn, narrow_tpc));
+    static const int down_grid = getenv("LA_DOWN_GRID") ? atoi(getenv("LA_DOWN_GRID")) : 0;
+    RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn, narrow_tpc, LA_EPI_PARTIAL, down_grid));
     track(p->down[l]);
   }
   p->head_tiles = (D.vocab + 127) / 128;

@@ -111,6 +111,24 @@ static __device__ int la_set_find_live(const DevPool& p, const int* g, int N, in
   return -1;
 }
 
+// newest-first bucket update of one suffix (move to front / push front)
+static __device__ void la_bucket_insert_warp(const DevPool& p, int slot, const int* suf, int lane) {
+  const int S = p.ngram - 1, C = p.C;
+  const int cnt = p.bkt_cnt[slot];
+  int* B = p.bkt_suf + (size_t)slot * C * S;
+  int sl[LA_MAX_SUFFIX];
+  for (int s = 0; s < S; ++s) sl[s] = suf[s];
+  const int pos = la_bucket_find(B, cnt, S, sl, lane);
+  const int upto = pos >= 0 ? pos : min(cnt, C - 1);   // entries [0, upto) move down one
+  la_bucket_shift_down(B, upto, S, lane);
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) B[s] = sl[s];
+    if (pos < 0) p.bkt_cnt[slot] = min(cnt + 1, C);
+  }
+  __threadfence_block();
+  __syncwarp();
+}
+
 // One n-gram insert by one warp (reference pool.py:41-61): dedup on
 // (lead, suffix) with recency refresh, newest-first bucket, distinct count,
 // and with a capacity the globally least-recently-touched entry is evicted
@@ -218,17 +236,92 @@ static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int l
     __syncwarp();
   }
   if (slot < 0) return;
-  const int cnt = p.bkt_cnt[slot];
-  int* B = p.bkt_suf + (size_t)slot * C * S;
-  const int pos = la_bucket_find(B, cnt, S, gl + 1, lane);
-  const int upto = pos >= 0 ? pos : min(cnt, C - 1);   // entries [0, upto) move down one
-  la_bucket_shift_down(B, upto, S, lane);
-  if (lane == 0) {
-    for (int s = 0; s < S; ++s) B[s] = gl[1 + s];
-    if (pos < 0) p.bkt_cnt[slot] = min(cnt + 1, C);
+  la_bucket_insert_warp(p, slot, gl + 1, lane);
+}
+
+// Ordered insert of one step's W harvested n-grams (insert_all, pool.py:63-67)
+// by the whole block, for the unbounded pool: the result equals W serial
+// la_pool_insert_warp calls.  In-batch repeats are refreshes of their first
+// occurrence; the distinct set and lead table take the remaining (distinct)
+// n-grams concurrently (CAS-claimed slots; a half-written key never equals a
+// different n-gram); log entries go to fixed positions; bucket updates --
+// the only order-dependent part -- run one warp per distinct lead, in column
+// order (different leads' buckets commute).
+static __device__ void la_pool_insert_batch(const DevPool& p, const int* grams, int W, int* overflow) {
+  __shared__ int s_new[64], s_slot[64], s_lfirst[64], s_gfirst[64];
+  const int N = p.ngram, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int n0 = p.counters[1];
+  if (tid < W) {
+    const int j = tid;
+    const int* g = grams + j * N;
+    int gf = j, lf = j;
+    for (int q = j - 1; q >= 0; --q) {
+      const int* h = grams + q * N;
+      bool eq = true;
+      for (int i = 0; i < N; ++i) eq &= (h[i] == g[i]);
+      if (eq) gf = q;
+      if (h[0] == g[0]) lf = q;
+    }
+    s_gfirst[j] = gf;
+    s_lfirst[j] = lf;
+    int is_new = 0;
+    if (gf == j) {
+      // distinct set (len(pool)): claim an empty slot with CAS on key[0]
+      uint32_t h = la_gram_hash(g, N) & (uint32_t)p.st_mask;
+      bool placed = false;
+      for (int probe = 0; probe <= p.st_mask && !placed; ++probe) {
+        int* key = p.set_keys + (size_t)h * N;
+        int k0 = atomicCAS(key, -1, g[0]);
+        if (k0 == -1) {
+          for (int i = 1; i < N; ++i) key[i] = g[i];
+          is_new = 1;
+          placed = true;
+        } else {
+          bool eq = (k0 == g[0]);
+          for (int i = 1; i < N && eq; ++i) eq &= (((volatile int*)key)[i] == g[i]);
+          if (eq) placed = true;
+          else h = (h + 1) & (uint32_t)p.st_mask;
+        }
+      }
+      if (!placed) *overflow = 1;
+    }
+    s_new[j] = is_new;
+    // lead table: claim or find with CAS (bucket counts start at 0)
+    int slot = -1;
+    if (lf == j) {
+      uint32_t h = la_mix32((uint32_t)g[0]) & (uint32_t)p.lt_mask;
+      for (int probe = 0; probe <= p.lt_mask; ++probe) {
+        const int k = atomicCAS(p.lead_keys + h, -1, g[0]);
+        if (k == -1 || k == g[0]) { slot = (int)h; break; }
+        h = (h + 1) & (uint32_t)p.lt_mask;
+      }
+      if (slot < 0) *overflow = 1;
+    }
+    s_slot[j] = slot;
+    if (n0 + j < p.log_cap) {
+      for (int i = 0; i < N; ++i) p.log[(size_t)(n0 + j) * N + i] = g[i];
+    } else {
+      *overflow = 1;
+    }
   }
-  __threadfence_block();
-  __syncwarp();
+  __syncthreads();
+  if (tid == 0) {
+    int added = 0;
+    for (int j = 0; j < W; ++j) added += s_new[j];
+    p.counters[0] += added;
+    p.counters[1] = min(n0 + W, p.log_cap);
+  }
+  // bucket updates: warp w serves the distinct leads w, w + nw, ... (first-occurrence order)
+  int q = 0;
+  for (int j = 0; j < W; ++j) {
+    if (s_lfirst[j] != j) continue;
+    if (q++ % nw != warp) continue;
+    const int slot = s_slot[j];
+    if (slot < 0) continue;
+    for (int jj = j; jj < W; ++jj)
+      if (s_lfirst[jj] == j) la_bucket_insert_warp(p, slot, grams + jj * N + 1, lane);
+  }
+  __syncthreads();
 }
 
 // ================================================= window geometry (A.1)
@@ -453,9 +546,13 @@ static __device__ void la_step_finish(DevDecode& d) {
     gr[N - 1] = s_newtop[j];
   }
   __syncthreads();
-  // ordered pool insert (pool.py:63-67), one warp, column order
-  if (tid < 32)
+  // ordered pool insert (pool.py:63-67), column order: block-parallel for the
+  // unbounded pool, one warp serially under an LRU cap (evictions are global)
+  if (d.pool.capacity == 0) {
+    la_pool_insert_batch(d.pool, s_grams, W, &d.overflow);
+  } else if (tid < 32) {
     for (int j = 0; j < W; ++j) la_pool_insert_warp(d.pool, s_grams + j * N, tid, &d.overflow);
+  }
   // window update (layout.py:219-252) with refills from the RNG stream
   const int sft = s_k - 1;
   const int v0 = min(sft, W - 1), v1 = min(sft, W);
