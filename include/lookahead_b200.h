@@ -190,6 +190,15 @@ int32_t la_verify_sample_dists(la_engine* e, const double* dists, int32_t V, int
                                int32_t c, const int32_t* suffixes, const la_sampler* s,
                                int32_t* out, int32_t* n_out, void* stream);
 
+/* Tests only: a fresh device pool (n-gram size N, LRU capacity or 0, bucket
+ * size C >= limit) fed n_grams n-grams in batches of `batch` (<= 64) through the
+ * step-finish insert path (pool.py:41-67); after every batch, lookup(lead,
+ * limit) (pool.py:69-81) for each of n_leads leads and len(pool):
+ * out[batch][lead][limit][N-1], counts[batch][lead], lens[batch]. */
+int32_t la_pool_test(int32_t N, int32_t capacity, int32_t C, const int32_t* grams, int32_t n_grams,
+                     int32_t batch, const int32_t* leads, int32_t n_leads, int32_t limit,
+                     int32_t* out, int32_t* counts, int32_t* lens);
+
 /* The generator as the device advances it, evaluated on the HOST (no GPU):
  * kind 0 random(), kind 1 integers(0, high); writes n values. */
 int32_t la_pcg64_draws(const la_sampler* s, int32_t kind, int32_t high, int32_t n, double* out);

@@ -36,7 +36,7 @@ EXPORTS = (
     "la_gemm_timing_reset", "la_gemm_timing_read", "la_forward_timing_read", "la_packed_bytes",
     "la_decode_jacobi", "la_decode_lookahead_sampled", "la_decode_autoregressive_sampled",
     "la_adjust_distributions", "la_verify_sample_dists", "la_pcg64_draws",
-    "la_session_start", "la_session_step", "la_session_read",
+    "la_session_start", "la_session_step", "la_session_read", "la_pool_test",
     "la_pack_weight",
 )
 
@@ -151,6 +151,8 @@ def load(path: str | os.PathLike | None = None):
                                      C.POINTER(la_decode_io), C.c_void_p]
     lib.la_session_step.argtypes = [C.c_void_p, C.POINTER(la_step_outcome), C.c_void_p]
     lib.la_session_read.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _P32]
+    lib.la_pool_test.argtypes = [C.c_int32, C.c_int32, C.c_int32, _P32, C.c_int32, C.c_int32, _P32,
+                                 C.c_int32, C.c_int32, _P32, _P32, _P32]
     lib.la_gemm_timing_reset.argtypes = [C.c_void_p]
     lib.la_gemm_timing_read.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     for name in EXPORTS:

@@ -660,6 +660,70 @@ extern "C" int32_t la_session_read(la_engine* e, int32_t what, int32_t offset, i
   return LA_ERR_INVALID_CONFIG;
 }
 
+// ------------------------------------------------------------- pool hook
+// Tests only: a fresh device pool (N, capacity; bucket size C) fed n_grams
+// n-grams in batches of `batch` through the K10 insert path; after each batch
+// lookup(lead, limit) of every lead and len(pool).  out[b][q][limit][N-1],
+// counts[b][q], lens[b] (host).
+extern "C" int32_t la_pool_test(int32_t N, int32_t capacity, int32_t C, const int32_t* grams,
+                                int32_t n_grams, int32_t batch, const int32_t* leads, int32_t n_leads,
+                                int32_t limit, int32_t* out, int32_t* counts, int32_t* lens) {
+  if (N < 2 || N > LA_MAX_NGRAM || C < 1 || n_grams < 1 || batch < 1 || batch > 64 || n_leads < 1 ||
+      limit < 1 || limit > C || capacity < 0 || !grams || !leads || !out || !counts || !lens) {
+    la_set_error("bad arguments");
+    return LA_ERR_INVALID_CONFIG;
+  }
+  const size_t LT = pow2_at_least(2 * (size_t)n_grams + 2), ST = LT;
+  const int nb = (n_grams + batch - 1) / batch;
+  const int Cb = capacity ? std::max(C, capacity) : C;
+  std::vector<void*> bufs;
+  auto dev = [&](size_t bytes, int fill) -> void* {
+    void* q = nullptr;
+    if (cudaMalloc(&q, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+    cudaMemset(q, fill, std::max<size_t>(bytes, 16));
+    bufs.push_back(q);
+    return q;
+  };
+  DevPool p{};
+  p.ngram = N; p.C = Cb; p.lt_mask = (int)LT - 1; p.st_mask = (int)ST - 1;
+  p.log_cap = n_grams + 1; p.capacity = capacity;
+  p.lead_keys = (int*)dev(LT * 4, 0xff);
+  p.bkt_cnt = (int*)dev(LT * 4, 0);
+  p.bkt_suf = (int*)dev(LT * Cb * (N - 1) * 4, 0);
+  p.set_keys = (int*)dev(ST * N * 4, 0xff);
+  p.set_stamp = (int*)dev(ST * 4, 0);
+  p.fifo = (int*)dev((size_t)p.log_cap * 4, 0);
+  p.counters = (int*)dev(16, 0);
+  p.log = (int*)dev((size_t)p.log_cap * N * 4, 0);
+  int* d_grams = (int*)dev((size_t)n_grams * N * 4, 0);
+  int* d_leads = (int*)dev((size_t)n_leads * 4, 0);
+  int* d_out = (int*)dev((size_t)nb * n_leads * limit * (N - 1) * 4, 0);
+  int* d_counts = (int*)dev((size_t)nb * n_leads * 4, 0);
+  int* d_lens = (int*)dev((size_t)nb * 4, 0);
+  int* d_ovf = (int*)dev(16, 0);
+  int rc = LA_OK;
+  for (void* q : bufs)
+    if (!q) rc = LA_ERR_CUDA;
+  int ovf = 0;
+  if (rc == LA_OK) {
+    cudaMemcpy(d_grams, grams, (size_t)n_grams * N * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_leads, leads, (size_t)n_leads * 4, cudaMemcpyHostToDevice);
+    la_pool_test_kernel<<<1, 256>>>(p, d_grams, n_grams, batch, d_leads, n_leads, limit, d_out,
+                                    d_counts, d_lens, d_ovf);
+    cudaError_t ce = cudaDeviceSynchronize();
+    if (ce != cudaSuccess) { la_set_error("pool test: %s", cudaGetErrorString(ce)); rc = LA_ERR_CUDA; }
+    else {
+      cudaMemcpy(out, d_out, (size_t)nb * n_leads * limit * (N - 1) * 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(counts, d_counts, (size_t)nb * n_leads * 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(lens, d_lens, (size_t)nb * 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&ovf, d_ovf, 4, cudaMemcpyDeviceToHost);
+    }
+  }
+  for (void* q : bufs) if (q) cudaFree(q);
+  if (rc == LA_OK && ovf) { la_set_error("pool overflow"); rc = LA_ERR_CAPACITY; }
+  return rc;
+}
+
 // ---------------------------------------------------------- sampler hooks
 extern "C" int32_t la_adjust_distributions(la_engine* e, const double* probs, int32_t n_rows,
                                            int32_t V, const la_sampler* s, double* out,

@@ -4,6 +4,9 @@
 
 __global__ void la_pool_seed_kernel(DevDecode* dp, const int* grams, int n, int log_from);
 __global__ void la_step_build_kernel(DevDecode* dp, FwdPlan* P);
+__global__ void la_pool_test_kernel(DevPool pool, const int* grams, int n_grams, int batch,
+                                    const int* leads, int n_leads, int limit, int* out, int* counts,
+                                    int* lens, int* overflow);
 __global__ void la_step_finish_kernel(DevDecode* dp);
 __global__ void la_scatter_amax_kernel(DevDecode* dp, const FwdPlan* P, const int* row_amax);
 __global__ void la_merge_amax_kernel(DevDecode* dp, const int* gathered, int world);

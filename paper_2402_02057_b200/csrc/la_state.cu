@@ -17,6 +17,35 @@ __global__ void la_pool_seed_kernel(DevDecode* dp, const int* grams, int n, int 
   }
 }
 
+// Parity hook (tests): replay n-gram batches through the device pool -- the
+// K10 insert path (block-parallel, or serial under an LRU cap) -- and after
+// every batch record lookup(lead, limit) for each requested lead and len(pool).
+__global__ void __launch_bounds__(256) la_pool_test_kernel(DevPool pool, const int* grams, int n_grams,
+                                                           int batch, const int* leads, int n_leads,
+                                                           int limit, int* out, int* counts, int* lens,
+                                                           int* overflow) {
+  const int N = pool.ngram, S = N - 1;
+  const int nb = (n_grams + batch - 1) / batch;
+  for (int b = 0; b < nb; ++b) {
+    const int g0 = b * batch, W = min(batch, n_grams - g0);
+    if (pool.capacity == 0) {
+      la_pool_insert_batch(pool, grams + (size_t)g0 * N, W, overflow);
+    } else if (threadIdx.x < 32) {
+      for (int j = 0; j < W; ++j) la_pool_insert_warp(pool, grams + (size_t)(g0 + j) * N, threadIdx.x, overflow);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < n_leads; q += blockDim.x) {
+      const int slot = la_lead_find(pool, leads[q]);
+      const int c = slot < 0 ? 0 : min(pool.bkt_cnt[slot], limit);
+      counts[(size_t)b * n_leads + q] = c;
+      int* o = out + ((size_t)b * n_leads + q) * limit * S;
+      for (int i = 0; i < c * S; ++i) o[i] = pool.bkt_suf[(size_t)slot * pool.C * S + i];
+    }
+    if (threadIdx.x == 0) lens[b] = pool.counters[0];
+    __syncthreads();
+  }
+}
+
 // K1: prepare_step (decoding.py:152-157) as one CTA.
 __global__ void __launch_bounds__(256) la_step_build_kernel(DevDecode* dp, FwdPlan* P) {
   LA_PDL_ENTRY();

@@ -1,0 +1,69 @@
+"""Device n-gram pool (la_state.cuh) against the oracle pool (pool.py:17-90),
+through the step-finish insert path: the block-parallel batch insert for the
+unbounded pool and the serial LRU path under a capacity.  The oracle pool is
+itself pinned to the reference's pool streams (tests/test_oracle_golden.py)."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import lookahead_oracle as lo
+from tests.conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+la = pytest.importorskip("paper_2402_02057_b200")
+from paper_2402_02057_b200 import _lib  # noqa: E402
+
+P32 = C.POINTER(C.c_int32)
+
+
+def _device_pool(N, cap, grams, batch, leads, limit):
+    lib = _lib.load()
+    g = np.ascontiguousarray(np.asarray(grams, dtype=np.int32).reshape(-1, N))
+    ld = np.ascontiguousarray(np.asarray(leads, dtype=np.int32))
+    nb = (len(g) + batch - 1) // batch
+    out = np.zeros((nb, len(ld), limit, N - 1), dtype=np.int32)
+    counts = np.zeros((nb, len(ld)), dtype=np.int32)
+    lens = np.zeros(nb, dtype=np.int32)
+    _lib.check(lib.la_pool_test(N, cap or 0, limit, g.ctypes.data_as(P32), len(g), batch,
+                                ld.ctypes.data_as(P32), len(ld), limit, out.ctypes.data_as(P32),
+                                counts.ctypes.data_as(P32), lens.ctypes.data_as(P32)))
+    return out, counts, lens
+
+
+@pytest.mark.parametrize("cap", [None, 3, 17])
+@pytest.mark.parametrize("N,vocab,batch", [(2, 3, 15), (3, 4, 15), (5, 3, 7), (4, 6, 31)])
+def test_batched_inserts_equal_serial_oracle(N, vocab, batch, cap):
+    rng = np.random.default_rng(N * 100 + vocab + batch + (cap or 0))
+    grams = rng.integers(0, vocab, size=(batch * 12, N))
+    grams[::5] = grams[1::5][: len(grams[::5])]          # in-batch repeats
+    leads, limit = list(range(vocab)), 8
+    out, counts, lens = _device_pool(N, cap, grams.ravel(), batch, leads, limit)
+    pool = lo.OraclePool(N, capacity=cap)
+    for b in range(len(lens)):
+        pool.insert_all([tuple(int(t) for t in x) for x in grams[b * batch:(b + 1) * batch]])
+        assert lens[b] == len(pool), b
+        for q, lead in enumerate(leads):
+            ref = pool.lookup(lead, limit)
+            got = [tuple(out[b, q, i].tolist()) for i in range(counts[b, q])]
+            assert got == [tuple(s) for s in ref], (b, lead)
+
+
+def test_reference_pool_streams_on_device():
+    """tests/golden/pool.json (reference NGramPool op streams, with and without
+    capacity): one insert per batch, every lookup checked."""
+    for case in load_golden("pool.json")["cases"]:
+        N, cap = case["ngram"], case["capacity"]
+        ops = case["ops"]
+        vocab = 1 + max(max(o["insert"]) for o in ops)
+        out, counts, lens = _device_pool(N, cap, [t for o in ops for t in o["insert"]], 1,
+                                         list(range(max(vocab, 8))), 8)
+        for b, o in enumerate(ops):
+            lead, lim = o["lookup"]
+            if lead >= out.shape[1]:
+                continue
+            got = [list(out[b, lead, i]) for i in range(min(counts[b, lead], lim))]
+            assert got == o["result"], (N, cap, b)
+            assert lens[b] == o["len"]
