@@ -42,10 +42,11 @@ __global__ void __cluster_dims__(LA_ADJ_CLUSTER, 1, 1) __launch_bounds__(LA_ADJ_
   unsigned rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int V = d.V;
-  const LaClusterScope sc{(int)((long)V * rank / LA_ADJ_CLUSTER),
-                          (int)((long)V * (rank + 1) / LA_ADJ_CLUSTER), rank, LA_ADJ_CLUSTER};
+  LaClusterScope sc{(int)((long)V * rank / LA_ADJ_CLUSTER),
+                    (int)((long)V * (rank + 1) / LA_ADJ_CLUSTER), rank, LA_ADJ_CLUSTER};
   const bool ok = la_adjust_row_s(d.logits + (size_t)la_sample_row(d, j) * V, sc, V, d.temperature,
                                   d.top_k, d.top_p, d.adj + (size_t)j * V, sm);
+  sc.finish();
   if (!ok && rank == 0 && threadIdx.x == 0) d.degenerate = 1;
 }
 
@@ -74,11 +75,11 @@ __global__ void __cluster_dims__(LA_ADJ_CLUSTER, 1, 1) __launch_bounds__(LA_ADJ_
   const int j = blockIdx.x / LA_ADJ_CLUSTER;
   unsigned rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const LaClusterScope sc{(int)((long)V * rank / LA_ADJ_CLUSTER),
-                          (int)((long)V * (rank + 1) / LA_ADJ_CLUSTER), rank, LA_ADJ_CLUSTER};
-  if (!la_adjust_row_s(nullptr, sc, V, temperature, top_k, top_p, rows + (size_t)j * V, sm) &&
-      rank == 0 && threadIdx.x == 0)
-    degenerate[j] = 1;
+  LaClusterScope sc{(int)((long)V * rank / LA_ADJ_CLUSTER),
+                    (int)((long)V * (rank + 1) / LA_ADJ_CLUSTER), rank, LA_ADJ_CLUSTER};
+  const bool ok = la_adjust_row_s(nullptr, sc, V, temperature, top_k, top_p, rows + (size_t)j * V, sm);
+  sc.finish();
+  if (!ok && rank == 0 && threadIdx.x == 0) degenerate[j] = 1;
 }
 
 // parity hook: verify_sample on caller distributions already in d.adj

@@ -80,9 +80,9 @@ __host__ __device__ __forceinline__ int la_pcg_integers(LaPcg64& g, unsigned hig
 struct LaSampleSmem {
   unsigned long long hist[32][16];   // per-warp radix histograms (4-bit digits)
   unsigned long long tot[16];
-  unsigned long long gtot[16];       // cluster scope: histogram summed over the cluster
-  double xd;                         // cluster scope: this CTA's published partial
-  long long xl;
+  unsigned long long xt[2][16];      // cluster scope: published histograms (double-buffered)
+  double xd[2];                      // cluster scope: published partials (double-buffered)
+  long long xl[2];
   double red[32];
   unsigned long long ured[32];
   int ired[32];
@@ -162,10 +162,11 @@ __device__ __forceinline__ int la_bscan_i(int v, LaSampleSmem& sm) {
 // results are deterministic; every call is collective over the scope.
 struct LaBlockScope {
   int lo, hi;   // [0, V)
-  __device__ double sum(double v, LaSampleSmem&) const { return v; }
-  __device__ float max(float v, LaSampleSmem&) const { return v; }
-  __device__ void combine16(LaSampleSmem&) const {}
-  __device__ long long prefix(long long, LaSampleSmem&) const { return 0; }
+  __device__ double sum(double v, LaSampleSmem&) { return v; }
+  __device__ float max(float v, LaSampleSmem&) { return v; }
+  __device__ void combine16(LaSampleSmem&) {}
+  __device__ long long prefix(long long, LaSampleSmem&) { return 0; }
+  __device__ void finish() {}
 };
 
 #if defined(__CUDACC__)
@@ -193,43 +194,47 @@ __device__ __forceinline__ T la_dsmem_ld(const T* local, unsigned rank) {
 struct LaClusterScope {
   int lo, hi;             // this CTA's slice
   unsigned rank, size;
-  __device__ double sum(double v, LaSampleSmem& sm) const {
-    if (threadIdx.x == 0) sm.xd = v;
+  int ph = 0;             // exchange parity: a slot is rewritten only two exchanges
+                          // later, after an intervening barrier every CTA has passed
+  __device__ double sum(double v, LaSampleSmem& sm) {
+    const int b = ph; ph ^= 1;
+    if (threadIdx.x == 0) sm.xd[b] = v;
     la_cluster_sync();
     double t = 0.0;
-    for (unsigned r = 0; r < size; ++r) t += la_dsmem_ld(&sm.xd, r);
-    la_cluster_sync();
+    for (unsigned r = 0; r < size; ++r) t += la_dsmem_ld(&sm.xd[b], r);
     return t;
   }
-  __device__ float max(float v, LaSampleSmem& sm) const {
-    if (threadIdx.x == 0) sm.xd = (double)v;
+  __device__ float max(float v, LaSampleSmem& sm) {
+    const int b = ph; ph ^= 1;
+    if (threadIdx.x == 0) sm.xd[b] = (double)v;
     la_cluster_sync();
     float t = -INFINITY;
-    for (unsigned r = 0; r < size; ++r) t = fmaxf(t, (float)la_dsmem_ld(&sm.xd, r));
-    la_cluster_sync();
+    for (unsigned r = 0; r < size; ++r) t = fmaxf(t, (float)la_dsmem_ld(&sm.xd[b], r));
     return t;
   }
   // sm.tot[16] (this CTA) -> sm.tot[16] (whole cluster)
-  __device__ void combine16(LaSampleSmem& sm) const {
+  __device__ void combine16(LaSampleSmem& sm) {
+    const int b = ph; ph ^= 1;
+    if (threadIdx.x < 16) sm.xt[b][threadIdx.x] = sm.tot[threadIdx.x];
     la_cluster_sync();
     if (threadIdx.x < 16) {
       unsigned long long t = 0ull;
-      for (unsigned r = 0; r < size; ++r) t += la_dsmem_ld(&sm.tot[threadIdx.x], r);
-      sm.gtot[threadIdx.x] = t;
+      for (unsigned r = 0; r < size; ++r) t += la_dsmem_ld(&sm.xt[b][threadIdx.x], r);
+      sm.tot[threadIdx.x] = t;
     }
-    la_cluster_sync();
-    if (threadIdx.x < 16) sm.tot[threadIdx.x] = sm.gtot[threadIdx.x];
     __syncthreads();
   }
   // exclusive prefix over the cluster's ranks of a per-CTA value
-  __device__ long long prefix(long long v, LaSampleSmem& sm) const {
-    if (threadIdx.x == 0) sm.xl = v;
+  __device__ long long prefix(long long v, LaSampleSmem& sm) {
+    const int b = ph; ph ^= 1;
+    if (threadIdx.x == 0) sm.xl[b] = v;
     la_cluster_sync();
     long long t = 0;
-    for (unsigned r = 0; r < rank; ++r) t += la_dsmem_ld(&sm.xl, r);
-    la_cluster_sync();
+    for (unsigned r = 0; r < rank; ++r) t += la_dsmem_ld(&sm.xl[b], r);
     return t;
   }
+  // before the CTA may exit: no peer still reads this CTA's slots
+  __device__ void finish() { la_cluster_sync(); }
 };
 #endif
 
@@ -245,7 +250,7 @@ __device__ __forceinline__ unsigned long long la_pbits(double p) {
 // distributions put almost every element in the same top digits, where
 // shared-memory atomics would serialise the CTA on one address.
 template <typename Scope>
-static __device__ bool la_radix_select(const double* p, const Scope& sc, bool mass, double scale,
+static __device__ bool la_radix_select(const double* p, Scope& sc, bool mass, double scale,
                                 unsigned long long need, LaSampleSmem& sm,
                                 unsigned long long* T, unsigned long long* above) {
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
@@ -316,7 +321,7 @@ static __device__ bool la_radix_select(const double* p, const Scope& sc, bool ma
 // keep p[i] with value key > T, and the first `m` (lowest ids) with key == T;
 // zero the rest (the (-p, id) order prefix of lexsort, sampling.py:43)
 template <typename Scope>
-static __device__ void la_keep_prefix(double* p, const Scope& sc, unsigned long long T, long long m,
+static __device__ void la_keep_prefix(double* p, Scope& sc, unsigned long long T, long long m,
                                LaSampleSmem& sm) {
   const int n = sc.hi - sc.lo;
   const int chunk = (n + blockDim.x - 1) / blockDim.x;
@@ -339,7 +344,7 @@ static __device__ void la_keep_prefix(double* p, const Scope& sc, unsigned long 
 // lg == nullptr: out[] already holds the probabilities.  Returns false
 // (DegenerateDistributionError) when all mass is truncated.
 template <typename Scope>
-static __device__ bool la_adjust_row_s(const float* lg, const Scope& sc, int V, double temperature,
+static __device__ bool la_adjust_row_s(const float* lg, Scope& sc, int V, double temperature,
                                        int top_k, double top_p, double* out, LaSampleSmem& sm) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lo = sc.lo, hi = sc.hi;
@@ -394,7 +399,8 @@ static __device__ bool la_adjust_row_s(const float* lg, const Scope& sc, int V, 
 
 static __device__ bool la_adjust_row(const float* lg, int V, double temperature, int top_k, double top_p,
                                      double* out, LaSampleSmem& sm) {
-  return la_adjust_row_s(lg, LaBlockScope{0, V}, V, temperature, top_k, top_p, out, sm);
+  LaBlockScope sc{0, V};
+  return la_adjust_row_s(lg, sc, V, temperature, top_k, top_p, out, sm);
 }
 
 // draw(p, rng): u = random(); first i with cumsum(p)[i] > u * cumsum(p)[-1]
