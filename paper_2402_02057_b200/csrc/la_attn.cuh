@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 
 #include "la_common.cuh"
+#include "la_gemm.cuh"
 #include "la_reduce.cuh"
 
 struct LaAttnArgs {
@@ -46,3 +47,20 @@ struct LaAttnFusedArgs {
 
 __global__ void la_attn_fused_kernel(LaAttnFusedArgs a);
 size_t la_attn_fused_smem(bool tc);
+
+// Attention + O projection in ONE persistent launch (LA_ATTN_O=1, experimental):
+// every CTA streams its first O-weight units into its smem ring at launch, runs
+// its attention unit (if any), publishes per-KV-head completion, then runs its
+// O stream-K units -- each waiting only for the heads its k-range reads.  The
+// O pieces land exactly where the standalone O GEMM puts them.
+struct LaAttnOArgs {
+  LaAttnFusedArgs at;     // attention (mma.sync path)
+  LaGemmArgs g;           // the O projection (split-K pieces, tpc = LA_TPC)
+  unsigned* head_done;    // [KVH] attention units finished this launch (reset by the last CTA)
+  unsigned* exit_cnt;     // CTAs finished this launch
+  unsigned* err;          // spin timeout (dependency never satisfied)
+  int nst;                // O-weight ring stages
+};
+size_t la_attn_o_smem(int nst);
+cudaError_t la_attn_o_launch(const LaAttnOArgs& x, int grid, cudaStream_t st, bool pdl);
+

@@ -293,41 +293,39 @@ __device__ void attn_tc_unit(const LaAttnFusedArgs& a, const FwdPlan* P, uint8_t
   wmark(a, 12);
 }
 
-// grid = KVH * nrb_max * (S + 1) units, block = 256 (8 warps x 16 query rows)
-__global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a) {
-  stamp(a, 0);
-  la_pdl_trigger();
-  la_l2_prefetch_gemm(a.pf);
+// Before the dependency wait: pull unit e's prefix K/V rows into L2.  Only a
+// cache hint -- if the plan or cache is not final yet the lines are merely
+// refetched after the wait -- so it is always safe.
+__device__ __forceinline__ void attn_prefetch_kv(const LaAttnFusedArgs& a, int e) {
   const FwdPlan* P = a.plan;
-  {
-    // before the dependency wait: pull this unit's prefix K/V rows into L2.
-    // Only a cache hint -- if the plan or cache is not final yet the lines
-    // are merely refetched after the wait -- so it is always safe.
-    const int S = a.S;
-    const int e = blockIdx.x;
-    const int split = e % (S + 1);
-    const int ctx = P->n_prefix;
-    if (split < S && P->n_rows > 0 && ctx > 0) {
-      const int kvh = e / (a.nrb_max * (S + 1));
-      const int CH = chunk_keys(ctx, S);
-      const int k0 = min(ctx, split * CH), k1 = min(ctx, (split + 1) * CH);
-      const size_t kv_ld = (size_t)a.KVH * 128;
-      for (int i = threadIdx.x; i < 2 * (k1 - k0); i += blockDim.x) {
-        const int key = k0 + (i >> 1);
-        const __nv_bfloat16* src = ((i & 1) ? a.vc : a.kc) + (size_t)key * kv_ld + kvh * 128;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(reinterpret_cast<uint64_t>(src)) : "memory");
-      }
+  const int S = a.S;
+  const int split = e % (S + 1);
+  const int ctx = P->n_prefix;
+  if (split < S && P->n_rows > 0 && ctx > 0) {
+    const int kvh = e / (a.nrb_max * (S + 1));
+    const int CH = chunk_keys(ctx, S);
+    const int k0 = min(ctx, split * CH), k1 = min(ctx, (split + 1) * CH);
+    const size_t kv_ld = (size_t)a.KVH * 128;
+    for (int i = threadIdx.x; i < 2 * (k1 - k0); i += blockDim.x) {
+      const int key = k0 + (i >> 1);
+      const __nv_bfloat16* src = ((i & 1) ? a.vc : a.kc) + (size_t)key * kv_ld + kvh * 128;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(reinterpret_cast<uint64_t>(src)) : "memory");
     }
   }
-  la_pdl_wait();
+}
+
+// One attention unit e = (KV head, row block, key chunk) after the dependency
+// wait, on a K/V ring of STAGES tiles at smem (plus the mask at mask_off).
+template <int STAGES>
+__device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
   stamp(a, 1);
+  const FwdPlan* P = a.plan;
   const int n_rows = P->n_rows, ctx = P->n_prefix;
   if (n_rows == 0) return;
   const int g = a.H / a.KVH;
   const int nq = n_rows * g;
   const int n_rb = (nq + 127) >> 7;
   const int S = a.S;
-  const int e = blockIdx.x;
   const int kvh = e / (a.nrb_max * (S + 1));
   const int rb = (e / (S + 1)) % a.nrb_max;
   const int split = e % (S + 1);
@@ -343,9 +341,8 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
     k_end = min(ctx, (split + 1) * CH);
   }
 
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* sKV = smem;                                                   // [kStages][K | V]
-  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + (a.tc ? kMaskOff : kMaskOffMma));   // [128][4]
+  uint8_t* sKV = smem;                                                   // [STAGES][K | V]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + (a.tc ? kMaskOff : STAGES * kTileBytes));   // [128][4]
   int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
   uint64_t* sBars = reinterpret_cast<uint64_t*>(sFlag + 4);           // tensor-core path
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBars + 2);
@@ -358,7 +355,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   const bool tc = a.tc && n_tiles <= kTcTiles && (smem_u32(smem) & 1023u) == 0u;
 
   auto load_kv = [&](int t) {
-    uint8_t* kb = sKV + (t % kStages) * kTileBytes;
+    uint8_t* kb = sKV + (t % STAGES) * kTileBytes;
     const int t0 = k_begin + t * kKeyTile;
     for (int i = tid; i < kKeyTile * 16; i += 256) {
       const int row = i >> 4, ch = i & 15, key = t0 + row;
@@ -372,7 +369,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   // (before the QKV epilogue), the step block's keys only after it
   auto issue_first = [&]() {
 #pragma unroll 1
-    for (int t = 0; t < kStages - 1; ++t) {
+    for (int t = 0; t < STAGES - 1; ++t) {
       if (t < n_tiles) load_kv(t);
       cp_commit();
     }
@@ -457,13 +454,13 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
     const bool warp_active = rb * 128 + warp * 16 < nq;
 
     for (int t = 0; t < n_tiles; ++t) {
-      if (t + kStages - 1 < n_tiles) load_kv(t + kStages - 1);
+      if (t + STAGES - 1 < n_tiles) load_kv(t + STAGES - 1);
       cp_commit();
-      cp_wait<kStages - 1>();
+      cp_wait<STAGES - 1>();
       __syncthreads();
       if (t == 0) stamp(a, 3);
       if (warp_active) {
-        const uint8_t* sK = sKV + (t % kStages) * kTileBytes;
+        const uint8_t* sK = sKV + (t % STAGES) * kTileBytes;
         const uint8_t* sV = sK + kKeyTile * 256;
         float s[8][4];
   #pragma unroll
@@ -655,6 +652,233 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
                      pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
   }
   stamp(a, 6);
+}
+
+// grid = KVH * nrb_max * (S + 1) units, block = 256 (8 warps x 16 query rows)
+__global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  stamp(a, 0);
+  la_pdl_trigger();
+  la_l2_prefetch_gemm(a.pf);
+  attn_prefetch_kv(a, blockIdx.x);
+  la_pdl_wait();
+  attn_unit<kStages>(a, smem, blockIdx.x);
+}
+
+// ---------------------------------------------------------------------------
+// Attention + O projection, one persistent launch (see la_attn.cuh).
+namespace {
+constexpr int kAoStages = 2;   // attention K/V ring in the fused kernel
+constexpr int kAoAttnBytes = kAoStages * kTileBytes + LA_MAX_ROWS * 4 * 4 + 64;
+constexpr int kAoGemmOff = (kAoAttnBytes + 1023) / 1024 * 1024;
+constexpr int kAoTile = 128 * 128;          // one 128 x 64 bf16 weight tile
+constexpr int kAoB = 128 * 128;             // <= 128 step rows x 64 bf16
+constexpr unsigned kAoSpin = 1u << 26;
+
+__device__ __forceinline__ unsigned ao_ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+}  // namespace
+
+size_t la_attn_o_smem(int nst) {
+  return 1024 + kAoGemmOff + (size_t)nst * (LA_TPC * kAoTile + kAoB) + 8 * (2 * nst + 4) + 16;
+}
+
+__global__ void __launch_bounds__(256, 1) la_attn_o_kernel(LaAttnOArgs x) {
+  extern __shared__ uint8_t ao_raw[];
+  uint8_t* smem = ao_raw + ((1024 - (smem_u32(ao_raw) & 1023)) & 1023);
+  const LaGemmArgs& g = x.g;
+  const LaAttnFusedArgs& a = x.at;
+  const int nst = x.nst;
+  constexpr uint32_t a_bytes = LA_TPC * kAoTile;
+  uint8_t* sA = smem + kAoGemmOff;
+  uint8_t* sB = sA + nst * a_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + nst * kAoB);
+  uint64_t* empty = full + nst;
+  uint64_t* tfull = empty + nst;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // O stream-K range of this CTA (identical to the standalone O GEMM's)
+  const int kb = g.kb;
+  const long U = (long)(g.n_tiles / LA_TPC) * kb;
+  const long Pn = gridDim.x;
+  const long u_begin = (long)blockIdx.x * U / Pn, u_end = (long)(blockIdx.x + 1) * U / Pn;
+  const int n_pre = (int)min((long)nst, u_end - u_begin);
+  la_pdl_trigger();
+  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 0] = t_; }
+  uint64_t pol_w = 0;
+  if (threadIdx.x == 0) {
+    pol_w = ptx::policy_evict_first();
+    for (int i = 0; i < n_pre; ++i) {
+      ptx::mbar_expect_tx_noarrive(&full[i], a_bytes);
+      ptx::bulk_load(sA + i * a_bytes, g.a + (size_t)(u_begin + i) * (a_bytes / 2), a_bytes, &full[i], pol_w);
+    }
+    // the units beyond the ring go to L2 meanwhile (read right after attention)
+    if (g.l2pf)
+      for (long u = u_begin + n_pre; u < u_end; ++u)
+        ptx::bulk_prefetch_l2(g.a + (size_t)u * (a_bytes / 2), a_bytes);
+  }
+  const int n_att = a.KVH * a.nrb_max * (a.S + 1);
+  if ((int)blockIdx.x < n_att) attn_prefetch_kv(a, blockIdx.x);
+  la_pdl_wait();
+  const FwdPlan* P = g.plan;
+  const int n_rows = P->n_rows, n_pad = P->n_pad;
+
+  // ---- attention phase: this CTA's unit, then publish its KV head
+  if ((int)blockIdx.x < n_att) {
+    attn_unit<kAoStages>(a, smem, blockIdx.x);
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // the O bulk copies read a.out
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(x.head_done + blockIdx.x / (a.nrb_max * (a.S + 1)), 1u);
+    }
+  }
+  __syncthreads();
+
+  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 1] = t_; }
+  // ---- O projection phase (split-K pieces, as la_gemm_kernel<LA_EPI_PARTIAL>)
+  const unsigned target = (unsigned)(a.nrb_max * (a.S + 1));
+  const int feats_per_kvh = (a.H / a.KVH) * 128;
+  if (n_rows == 0) {
+    if (threadIdx.x == 0)
+      for (int i = 0; i < n_pre; ++i) {
+        ptx::mbar_arrive(&full[i]);
+        ptx::mbar_wait(&full[i], 0);
+      }
+  } else if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_x = ptx::policy_evict_last();
+      const uint32_t bbytes = (uint32_t)n_pad * 128;
+      int ready = -1;
+      long it = 0;
+      for (long u = u_begin; u < u_end; ++u, ++it) {
+        const int k = (int)(u % kb);
+        const int s = (int)(it % nst);
+        const uint32_t r = (uint32_t)(it / nst);
+        const int kvh = k * 64 / feats_per_kvh;
+        if (kvh != ready) {
+          unsigned n = 0;
+          while ((int)(ao_ld_acquire(x.head_done + kvh) - target) < 0) {
+            if (++n > kAoSpin) { atomicExch(x.err, 1u); break; }
+            __nanosleep(64);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          if (ready < 0 && x.g.trace) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 2] = t_; }
+          ready = kvh;
+        }
+        if (it < n_pre) {
+          ptx::mbar_expect_tx(&full[s], bbytes);
+        } else {
+          ptx::mbar_wait(&empty[s], (r - 1) & 1);
+          ptx::mbar_expect_tx(&full[s], a_bytes + bbytes);
+          ptx::bulk_load(sA + s * a_bytes, g.a + (size_t)u * (a_bytes / 2), a_bytes, &full[s], pol_w);
+        }
+        ptx::bulk_load(sB + s * kAoB, g.b + (size_t)k * (kAoB / 2), bbytes, &full[s], pol_x);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = ptx::umma_idesc_bf16(128, (uint32_t)n_pad);
+      long it = 0, u = u_begin;
+      int use[2] = {0, 0}, buf = 0;
+      while (u < u_end) {
+        const int tile = (int)(u / kb);
+        const long seg_start = u, seg_end = min(u_end, (long)(tile + 1) * kb);
+        if (use[buf] > 0) {
+          ptx::mbar_wait(&tempty[buf], (use[buf] - 1) & 1);
+          ptx::tc_fence_after();
+        }
+        const uint32_t d_tmem = tmem + buf * (LA_TPC * 128);
+        for (; u < seg_end; ++u, ++it) {
+          const int s = (int)(it % nst);
+          ptx::mbar_wait(&full[s], (uint32_t)(it / nst) & 1);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * a_bytes), b_addr = smem_u32(sB + s * kAoB);
+          for (int tt = 0; tt < LA_TPC; ++tt)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kAoTile + kk * 32),
+                             ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
+                             (u > seg_start || kk > 0) ? 1u : 0u);
+          ptx::umma_commit(&empty[s]);
+        }
+        ptx::umma_commit(&tfull[buf]);
+        use[buf]++;
+        buf ^= 1;
+      }
+    }
+  } else if (warp < 6) {
+    const int row_base = 32 * (warp & 3);
+    const int f = row_base + lane;
+    int use[2] = {0, 0}, buf = 0;
+    long u = u_begin;
+    while (u < u_end) {
+      const int tile = (int)(u / kb);
+      const long seg_end = min(u_end, (long)(tile + 1) * kb);
+      const long c_first = la_cta_of((long)tile * kb, U, Pn);
+      const int seg = (int)(blockIdx.x - c_first);
+      ptx::mbar_wait(&tfull[buf], use[buf] & 1);
+      ptx::tc_fence_after();
+      for (int tt = 0; tt < LA_TPC; ++tt) {
+        const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
+        float* wsp = g.ws + ((size_t)(tile * LA_TPC + tt) * g.max_segs + seg) * 128 * 128 + f;
+        for (int c0 = 0; c0 < n_pad; c0 += 32) {
+          float v[32];
+          ptx::tmem_ld32(t_base + c0, v);
+          const int nj = min(32, n_rows - c0);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[buf]);
+      use[buf]++;
+      buf ^= 1;
+      u = seg_end;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 3] = t_; }
+  if (threadIdx.x == 0) {
+    // the last CTA out resets the per-head counters for the next launch
+    __threadfence();
+    if (atomicAdd(x.exit_cnt, 1u) == gridDim.x - 1) {
+      for (int h = 0; h < a.KVH; ++h) x.head_done[h] = 0u;
+      *x.exit_cnt = 0u;
+      __threadfence();
+    }
+  }
+}
+
+cudaError_t la_attn_o_launch(const LaAttnOArgs& x, int grid, cudaStream_t st, bool pdl) {
+  static bool attr = false;
+  const size_t smem = la_attn_o_smem(x.nst);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(la_attn_o_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return la_launch(la_attn_o_kernel, dim3(grid), dim3(256), smem, st, pdl, x);
 }
 
 LA_TL_DEFINE_SETTER(attnf)

@@ -64,6 +64,8 @@ struct LlamaPath {
   int attn_min_chunk = 128;               // LA_ATTN_MIN_CHUNK
   bool attn_fused = true;                 // fused QKV fix-up + attention + merge (LA_ATTN_FUSED=0: 3 kernels)
   LaAttnFusedArgs af{};                   // its static arguments
+  bool attn_o = false;                    // attention + O projection in one launch (LA_ATTN_O=1)
+  unsigned *ao_head = nullptr, *ao_exit = nullptr, *ao_err = nullptr;
   int skip = 0;                           // LA_SKIP: debug mask of per-layer launches to omit (timing only)
   bool mega = false;                      // persistent whole-forward kernel (LA_MEGA=1; experimental)
   LaMegaArgs ma{};
@@ -400,6 +402,15 @@ int llama_create(la_engine* e) {
     RET_IF(lalloc(e, &af.part_o, groups * units * 128 * 128));
     RET_IF(lalloc(e, &af.part_ml, groups * units * 128));
     RET_IF(lalloc(e, &af.cnt, groups));
+    // attention + O in one persistent launch: needs every attention unit and
+    // every O CTA co-resident (one CTA per SM) and the O GEMM on all SMs
+    p->attn_o = getenv("LA_ATTN_O") && atoi(getenv("LA_ATTN_O")) == 1 && af.spread_merge && !af.tc &&
+                !af.fuse_qkv && !p->fused && !p->mega;
+    if (p->attn_o) {
+      RET_IF(lalloc(e, &p->ao_head, (size_t)p->KVH));
+      RET_IF(lalloc(e, &p->ao_exit, 1));
+      RET_IF(lalloc(e, &p->ao_err, 1));
+    }
     if (getenv("LA_ATTN_TRACE")) {
       if (atoi(getenv("LA_ATTN_TRACE")) == 2) {
         // mapped host memory: readable by a host watchdog while a kernel hangs
@@ -615,8 +626,25 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       KT_END(st, "qkv_epi");
       ++n;
     }
+    if (p->attn_o && p->o[l].grid == la_sm_count() && p->o[l].args.tpc == LA_TPC) {
+      LaAttnOArgs x;
+      x.at = p->af;
+      x.at.plan = e->d_plan;
+      x.at.kc = kc + l * lstride;
+      x.at.vc = vc + l * lstride;
+      x.at.pf = LaPrefetch{};
+      x.at.trace = nullptr;
+      x.g = p->o[l].args;   // trace (LA_GEMM_TRACE): entry, attention done, first head ready, end
+      x.g.timing = nullptr;
+      x.head_done = p->ao_head; x.exit_cnt = p->ao_exit; x.err = p->ao_err;
+      x.nst = 3;
+      x.g.l2pf = getenv("LA_ATTN_O_L2") ? atoi(getenv("LA_ATTN_O_L2")) : 0;   // measured slower when on
+      KT_BEGIN(st);
+      CK(la_attn_o_launch(x, la_sm_count(), st, p->pdl));
+      KT_END(st, "attn+o");
+      --n;
+    } else {
       if (!(p->skip & 2)) RET_IF(p->attn_fused ? launch_attn_fused(e, l, st) : launch_attn(e, l, st));
-    {
       KT_BEGIN(st);
       if (!(p->skip & 128)) RET_IF(la_gemm_launch(p->o[l], st, p->pdl));
       KT_END(st, "gemm_o");
@@ -925,6 +953,10 @@ cudaError_t llama_copy_argmax(la_engine* e, int32_t* host, int n, cudaStream_t s
 // spin-timeout flag of the persistent kernel (a dependency never satisfied)
 int llama_mega_error(la_engine* e) {
   LlamaPath* p = e->llama;
+  if (p && p->attn_o) {
+    unsigned v = 0;
+    if (cudaMemcpy(&v, p->ao_err, sizeof(v), cudaMemcpyDeviceToHost) == cudaSuccess && v) return 1;
+  }
   if (!p || !p->mega) return 0;
   unsigned v = 0;
   if (cudaMemcpy(&v, p->ma.sync + p->ma.sm.err, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
