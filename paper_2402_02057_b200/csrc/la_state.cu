@@ -46,16 +46,39 @@ __global__ void __launch_bounds__(256) la_pool_test_kernel(DevPool pool, const i
   }
 }
 
+// The step kernels run on a shared-memory copy of the decode state (one
+// coalesced load, one store back): the state machine reads its scalar fields
+// after every barrier, and from global memory each read is an L2 round trip.
+__device__ __forceinline__ void la_dec_load(DevDecode& sd, const DevDecode* dp) {
+  static_assert(sizeof(DevDecode) % 4 == 0, "DevDecode copy granularity");
+  const int* src = reinterpret_cast<const int*>(dp);
+  int* dst = reinterpret_cast<int*>(&sd);
+  for (int i = threadIdx.x; i < (int)(sizeof(DevDecode) / 4); i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+}
+__device__ __forceinline__ void la_dec_store(DevDecode* dp, const DevDecode& sd) {
+  __syncthreads();
+  const int* src = reinterpret_cast<const int*>(&sd);
+  int* dst = reinterpret_cast<int*>(dp);
+  for (int i = threadIdx.x; i < (int)(sizeof(DevDecode) / 4); i += blockDim.x) dst[i] = src[i];
+}
+
 // K1: prepare_step (decoding.py:152-157) as one CTA.
 __global__ void __launch_bounds__(256) la_step_build_kernel(DevDecode* dp, FwdPlan* P) {
+  __shared__ __align__(16) DevDecode sd;
   LA_PDL_ENTRY();
-  la_step_build(*dp, *P);
+  la_dec_load(sd, dp);
+  la_step_build(sd, *P);
+  la_dec_store(dp, sd);
 }
 
 // K10: finish_step (decoding.py:160-204) as one CTA.
 __global__ void __launch_bounds__(256) la_step_finish_kernel(DevDecode* dp) {
+  __shared__ __align__(16) DevDecode sd;
   LA_PDL_ENTRY();
-  la_step_finish(*dp);
+  la_dec_load(sd, dp);
+  la_step_finish(sd);
+  la_dec_store(dp, sd);
 }
 
 // Per-row argmax merge into the global-row array (owned rows only).
