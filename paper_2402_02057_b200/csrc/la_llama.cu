@@ -65,6 +65,7 @@ struct LlamaPath {
   bool attn_fused = true;                 // fused QKV fix-up + attention + merge (LA_ATTN_FUSED=0: 3 kernels)
   LaAttnFusedArgs af{};                   // its static arguments
   bool attn_o = false;                    // attention + O projection in one launch (LA_ATTN_O=1)
+  bool head_fused = false;                // LM head epilogue inside its GEMM (LA_HEAD_FUSED=1)
   unsigned *ao_head = nullptr, *ao_exit = nullptr, *ao_err = nullptr;
   int skip = 0;                           // LA_SKIP: debug mask of per-layer launches to omit (timing only)
   bool mega = false;                      // persistent whole-forward kernel (LA_MEGA=1; experimental)
@@ -328,7 +329,11 @@ int llama_create(la_engine* e) {
     track(p->down[l]);
   }
   p->head_tiles = (D.vocab + 127) / 128;
-  RET_IF(build_gemm(p->head, p->lm_head, p->head_tiles, p->h, d, LA_TPC, fused ? LA_EPI_LOGITS : LA_EPI_PARTIAL));
+  // LA_HEAD_FUSED=1: the LM head's logits / argmax epilogue inside its GEMM
+  // (most tile pairs are owned whole by one CTA: ~54 units per CTA)
+  p->head_fused = fused || (getenv("LA_HEAD_FUSED") && atoi(getenv("LA_HEAD_FUSED")) == 1);
+  RET_IF(build_gemm(p->head, p->lm_head, p->head_tiles, p->h, d, LA_TPC,
+                    p->head_fused ? LA_EPI_LOGITS : LA_EPI_PARTIAL));
   track(p->head);
   RET_IF(lalloc(e, &p->keys, LA_MAX_ROWS));
   p->head.args.keys = p->keys;
@@ -690,7 +695,7 @@ static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
     KT_END(st, "gemm_head");
   }
   KT_BEGIN(st);
-  if (!p->fused) {
+  if (!p->head_fused) {
     LaLogitsEpi lg{e->d_plan, p->ws, split_of(p->head), p->keys, p->logits, p->V, p->nrm};
     CK(la_launch(la_logits_epi_kernel, dim3(p->head_tiles, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, lg));
     *nk += 1;
