@@ -39,6 +39,8 @@ struct LaAttnFusedArgs {
   int spread_merge;              // grid <= SMs: every chunk CTA merges a share of the rows
   int fuse_qkv;                  // grid <= SMs: the QKV epilogue runs here first (grid barrier)
   int tc;                        // tcgen05 QK^T / PV for chunks of <= 6 key tiles
+  int cluster;                   // launched as clusters of S+1 CTAs = one (KV head, row block):
+                                 // chunk partials stay in smem and merge over DSMEM
   int dbg;                       // LA_ATTN_DBG experiments: 1 skip PV MMAs, 2 skip QK^T MMAs
   LaQkvEpi qkv;                  // its arguments
   unsigned* gbar;                // grid-barrier counter (monotonic; + grid per launch)
@@ -46,7 +48,8 @@ struct LaAttnFusedArgs {
 };
 
 __global__ void la_attn_fused_kernel(LaAttnFusedArgs a);
-size_t la_attn_fused_smem(bool tc);
+cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_t st, bool pdl);
+size_t la_attn_fused_smem(bool tc, bool cluster = false);
 
 // Attention + O projection in ONE persistent launch (LA_ATTN_O=1, experimental):
 // every CTA streams its first O-weight units into its smem ring at launch, runs

@@ -37,6 +37,13 @@ constexpr int kTcQ = 0, kTcK = 32768, kTcV = kTcK + kTcTiles * 16384;
 constexpr int kTcSmem = kTcV + kTcTiles * 16384;                   // 224 KB
 constexpr int kMaskOff = kTcSmem > kStages * kTileBytes ? kTcSmem : kStages * kTileBytes;
 constexpr int kMaskOffMma = kStages * kTileBytes;   // mma.sync-only launches
+// cluster mode: 4-tile ring | pushed partials [(S+1) * rows_per <= 136][128] fp32 |
+// their (m, l) | mask
+constexpr int kClStages = 4;
+constexpr int kClPush = kClStages * kTileBytes;
+constexpr int kClPushRows = 136;
+constexpr int kClPushML = kClPush + kClPushRows * 128 * 4;
+constexpr int kClMaskOff = kClPushML + kClPushRows * 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -116,8 +123,8 @@ __device__ __forceinline__ void wmark(const LaAttnFusedArgs& a, int v) {
 
 }  // namespace
 
-size_t la_attn_fused_smem(bool tc) {
-  return (size_t)(tc ? kMaskOff : kMaskOffMma) + LA_MAX_ROWS * 4 * 4 + 64;
+size_t la_attn_fused_smem(bool tc, bool cluster) {
+  return (size_t)(tc ? kMaskOff : cluster ? kClMaskOff : kMaskOffMma) + LA_MAX_ROWS * 4 * 4 + 64;
 }
 
 // ---------------------------------------------------------------------------
@@ -314,6 +321,57 @@ __device__ __forceinline__ void attn_prefetch_kv(const LaAttnFusedArgs& a, int e
   }
 }
 
+// Cluster-mode merge: rows [r0, r1) of this CTA's share, combining the S+1
+// chunk partials held in the cluster's shared memories (rank = chunk) in chunk
+// order -- the same arithmetic as the global-memory merge.
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ void attn_merge_cluster(const LaAttnFusedArgs& a, uint8_t* smem, int rb, int g, int nq, int kvh,
+                                   int S, int split) {
+  const int tid = threadIdx.x;
+  const float* sP = reinterpret_cast<const float*>(smem + kClPush);
+  const float2* sM = reinterpret_cast<const float2*>(smem + kClPushML);
+  const int nqb = min(128, nq - rb * 128);
+  const int rows_per = (nqb + S) / (S + 1);
+  const int r0 = split * rows_per, r1 = min(nqb, r0 + rows_per);
+  for (int row = r0 + (tid >> 3); row < r1; row += 32) {
+    const int lr = row - r0;
+    const int qr = rb * 128 + row;
+    const int hd = (tid & 7) * 16;
+    float m = -INFINITY, ll = 0.f;
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    for (int sp = 0; sp <= S; ++sp) {
+      const int slot = sp * rows_per + lr;
+      const float2 ml = sM[slot];
+      if (ml.x == -INFINITY) continue;
+      const float4* po = reinterpret_cast<const float4*>(sP + (size_t)slot * 128 + hd);
+      const float4 v0 = po[0], v1 = po[1], v2 = po[2], v3 = po[3];
+      const float vv[16] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w,
+                            v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};
+      const float mn = fmaxf(m, ml.x);
+      const float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = acc[i] * s0 + vv[i] * s1;
+      ll = ll * s0 + ml.y * s1;
+      m = mn;
+    }
+    const float inv = 1.0f / ll;
+    const int r = qr / g, head = kvh * g + qr % g;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      *reinterpret_cast<uint4*>(a.out + la_act_off(r, head * 128 + hd + 8 * c)) =
+          make_uint4(pack_bf16(acc[8 * c] * inv, acc[8 * c + 1] * inv),
+                     pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
+                     pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
+                     pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
+  }
+}
+
 // One attention unit e = (KV head, row block, key chunk) after the dependency
 // wait, on a K/V ring of STAGES tiles at smem (plus the mask at mask_off).
 template <int STAGES>
@@ -342,7 +400,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
   }
 
   uint8_t* sKV = smem;                                                   // [STAGES][K | V]
-  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + (a.tc ? kMaskOff : STAGES * kTileBytes));   // [128][4]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + (a.tc ? kMaskOff : a.cluster ? kClMaskOff : STAGES * kTileBytes));   // [128][4]
   int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
   uint64_t* sBars = reinterpret_cast<uint64_t*>(sFlag + 4);           // tensor-core path
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBars + 2);
@@ -555,10 +613,31 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
       l0 += __shfl_xor_sync(0xffffffffu, l0, off);
       l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
+    // cluster mode: push each row's partial straight into the smem of the
+    // chunk CTA that merges it (rank row / rows_per), slot [chunk][local row]
+    const int nqb_ = min(128, nq - rb * 128);
+    const int rows_per_ = (nqb_ + S) / (S + 1);
   #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int row = qrow0 + half * 8;
       if (rb * 128 + row >= nq) continue;
+      if (a.cluster) {
+        const unsigned owner = (unsigned)(row / rows_per_);
+        const int slot = split * rows_per_ + (row - (int)owner * rows_per_);
+        const uint32_t dst = dsmem_addr(smem + kClPush + (size_t)slot * 512, owner);
+  #pragma unroll
+        for (int dd = 0; dd < 16; ++dd) {
+          const int col = dd * 8 + (lane & 3) * 2;
+          asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};"
+                       :: "r"(dst + col * 4), "f"(o[dd][half * 2]), "f"(o[dd][half * 2 + 1]) : "memory");
+        }
+        if ((lane & 3) == 0) {
+          const float2 ml = make_float2(half ? m1 : m0, half ? l1 : l0);
+          asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};"
+                       :: "r"(dsmem_addr(smem + kClPushML + slot * 8, owner)), "f"(ml.x), "f"(ml.y) : "memory");
+        }
+        continue;
+      }
       float* dst = a.part_o + ((grp * (S + 1) + split) * 128 + row) * 128;
   #pragma unroll
       for (int dd = 0; dd < 16; ++dd) {
@@ -568,6 +647,15 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
       if ((lane & 3) == 0)
         __stcg(a.part_ml + (grp * (S + 1) + split) * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
     }
+  }
+  if (a.cluster) {
+    // every chunk CTA of the group is in this cluster: one barrier makes the
+    // pushed partials visible; each CTA then merges its rows from local smem
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    stamp(a, 5);
+    attn_merge_cluster(a, smem, rb, g, nq, kvh, S, split);
+    stamp(a, 6);
+    return;
   }
   __syncthreads();
   // arrival of this chunk.  Counters only grow: an active group gains exactly
@@ -662,7 +750,38 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   la_l2_prefetch_gemm(a.pf);
   attn_prefetch_kv(a, blockIdx.x);
   la_pdl_wait();
-  attn_unit<kStages>(a, smem, blockIdx.x);
+  if (a.cluster) attn_unit<kClStages>(a, smem, blockIdx.x);
+  else attn_unit<kStages>(a, smem, blockIdx.x);
+  if (a.dbg & 8) {   // timing experiment: 5 us of extra attention time per CTA
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    do { asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); } while (t - t0 < 5000ull);
+  }
+}
+
+cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_t st, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = la_attn_fused_smem(a.tc != 0, a.cluster != 0);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (a.cluster) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = a.S + 1;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, la_attn_fused_kernel, a);
 }
 
 // ---------------------------------------------------------------------------

@@ -399,6 +399,12 @@ int llama_create(la_engine* e) {
     // mma.sync path on the parity tests) but measured slower on cfg2 -- its
     // S -> softmax -> PV phases serialise (no cross-tile pipelining yet)
     af.tc = getenv("LA_ATTN_TC") && atoi(getenv("LA_ATTN_TC")) == 1;
+    // LA_ATTN_CLUSTER=1: the S+1 chunk CTAs of each (KV head, row block) form
+    // a cluster; partials are pushed into the merging CTA's smem (remote
+    // stores) and merged after one cluster barrier.  Measured equal to the
+    // global partials + counter path (the barrier costs what the atomics did).
+    af.cluster = af.spread_merge && !af.tc && !af.fuse_qkv && units <= 8 &&
+                 getenv("LA_ATTN_CLUSTER") && atoi(getenv("LA_ATTN_CLUSTER")) == 1;
     af.dbg = getenv("LA_ATTN_DBG") ? atoi(getenv("LA_ATTN_DBG")) : 0;
     af.scale = 1.0f / sqrtf(128.0f);
     af.q = p->q;
@@ -585,8 +591,7 @@ static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
                      p->rope_sin, p->H, p->KVH, p->nrm};
   }
   KT_BEGIN(st);
-  CK(la_launch(la_attn_fused_kernel, dim3(p->KVH * a.nrb_max * (a.S + 1)), dim3(256), la_attn_fused_smem(a.tc != 0), st,
-               p->pdl, a));
+  CK(la_attn_fused_launch(a, p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
   KT_END(st, "attn_fused");
   return LA_OK;
 }
@@ -639,6 +644,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       x.at.vc = vc + l * lstride;
       x.at.pf = LaPrefetch{};
       x.at.trace = nullptr;
+      x.at.cluster = 0;
       x.g = p->o[l].args;   // trace (LA_GEMM_TRACE): entry, attention done, first head ready, end
       x.g.timing = nullptr;
       x.head_done = p->ao_head; x.exit_cnt = p->ao_exit; x.err = p->ao_err;
