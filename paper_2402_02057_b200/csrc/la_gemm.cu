@@ -146,10 +146,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = sm;
   // one 192 KB ring: nst stages of (weights a_bytes | step rows 16 KB), the
   // weight and row halves in two contiguous regions (1024-B aligned)
-  const int nst = args.nst > 0 ? args.nst : (args.tpc == LA_TPC ? kStages : kMaxStages);
+  const bool dual = args.b2 != nullptr;   // prefill: two row blocks per weight stage
+  const int nst = args.nst > 0 ? args.nst : (args.tpc == LA_TPC || dual ? kStages : kMaxStages);
   const uint32_t a_stage = (uint32_t)args.tpc * kTileBytes;
+  const uint32_t b_stage = dual ? 2 * kBBytes : kBBytes;
   uint8_t* sB = sA + nst * a_stage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sA + nst * (a_stage + kBBytes));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + nst * (a_stage + b_stage));
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
@@ -212,6 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 0] = t_entry;
   const int n_rows = P->n_rows;
   const int n_pad = P->n_pad;
+  const int n_rows2 = dual ? args.plan2->n_rows : 0;
+  const int n_pad2 = dual ? args.plan2->n_pad : 0;
   if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
 
   if (n_rows == 0) {
@@ -225,28 +229,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol_x = ptx::policy_evict_last();    // step rows: re-read by every CTA
-      const uint32_t bbytes = (uint32_t)n_pad * 128;
+      const uint32_t bbytes = (uint32_t)n_pad * 128, bbytes2 = (uint32_t)n_pad2 * 128;
       long it = 0;
       for (long u = u_begin; u < u_end; ++u, ++it) {
         const int k = (int)(u % kb);
         const int s = (int)(it % nst);
         const uint32_t r = (uint32_t)(it / nst);
         const bool load_b = !(args.debug & 1);
+        const uint32_t bb = load_b ? bbytes + bbytes2 : 0;
         if (it < n_pre) {
-          ptx::mbar_expect_tx(&full[s], load_b ? bbytes : 0);   // weights already in flight
+          ptx::mbar_expect_tx(&full[s], bb);   // weights already in flight
         } else {
           ptx::mbar_wait(&empty[s], (r - 1) & 1);
-          ptx::mbar_expect_tx(&full[s], a_bytes + (load_b ? bbytes : 0));
+          ptx::mbar_expect_tx(&full[s], a_bytes + bb);
           ptx::bulk_load(sA + s * a_stage, a_src(u), a_bytes, &full[s], pol_w);
         }
-        if (load_b)
-          ptx::bulk_load(sB + s * kBBytes, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
+        if (load_b) {
+          ptx::bulk_load(sB + s * b_stage, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
+          if (dual && bbytes2)
+            ptx::bulk_load(sB + s * b_stage + kBBytes, args.b2 + (size_t)k * (kBBytes / 2), bbytes2,
+                           &full[s], pol_x);
+        }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = ptx::umma_idesc_bf16(128, (uint32_t)n_pad);
+      const uint32_t idesc2 = ptx::umma_idesc_bf16(128, (uint32_t)(n_pad2 > 0 ? n_pad2 : 16));
       long it = 0, u = u_begin;
       int use[2] = {0, 0}, buf = 0;
       while (u < u_end) {
@@ -262,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&full[s], (uint32_t)(it / nst) & 1);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sA + s * a_stage);
-          const uint32_t b_addr = ptx::smem_u32(sB + s * kBBytes);
+          const uint32_t b_addr = ptx::smem_u32(sB + s * b_stage);
           if (args.debug & 2) {
             ptx::mbar_arrive(&empty[s]);
             continue;
@@ -272,6 +282,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < 4; ++kk)
               ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kTileBytes + kk * 32),
                              ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
+                             (u > seg_start || kk > 0) ? 1u : 0u);
+          if (dual && n_pad2 > 0)   // second row block into the buffer's upper 128 columns
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              ptx::umma_bf16(d_tmem + 128, ptx::umma_desc_sw128(a_addr + kk * 32),
+                             ptx::umma_desc_sw128(b_addr + kBBytes + kk * 32), idesc2,
                              (u > seg_start || kk > 0) ? 1u : 0u);
           ptx::umma_commit(&empty[s]);
         }
@@ -296,15 +312,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&tfull[buf], use[buf] & 1);
       ptx::tc_fence_after();
       if (EPI == LA_EPI_PARTIAL || seg != 0) {
-        // write this piece's fp32 partial
-        for (int tt = 0; tt < tpc; ++tt) {
+        // write this piece's fp32 partial (dual mode: both row blocks)
+        const int nblk = dual ? 2 : tpc;
+        for (int tt = 0; tt < nblk; ++tt) {
           const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
-          const int ftile = tile * tpc + tt;
-          float* wsp = args.ws + ((size_t)ftile * args.max_segs + seg) * 128 * 128 + f;
-          for (int c0 = 0; c0 < n_pad; c0 += 32) {
+          const int ftile = dual ? tile : tile * tpc + tt;
+          float* wsp = (dual && tt ? args.ws2 : args.ws) + ((size_t)ftile * args.max_segs + seg) * 128 * 128 + f;
+          const int nr = dual && tt ? n_rows2 : n_rows, np = dual && tt ? n_pad2 : n_pad;
+          for (int c0 = 0; c0 < np; c0 += 32) {
             float v[32];
             ptx::tmem_ld32(t_base + c0, v);
-            const int nj = min(32, n_rows - c0);
+            const int nj = min(32, nr - c0);
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj)
               if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
@@ -451,8 +469,9 @@ static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
     attr = true;
   }
   // the ring (nst stages), barriers / TMEM slot, and the fused epilogue's staging
-  const int nst = g.args.nst > 0 ? g.args.nst : (g.args.tpc == LA_TPC ? kStages : kMaxStages);
-  const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + kBBytes) + 2 * kMaxStages * 8 +
+  const bool dual = g.args.b2 != nullptr;
+  const int nst = g.args.nst > 0 ? g.args.nst : (g.args.tpc == LA_TPC || dual ? kStages : kMaxStages);
+  const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + (dual ? 2 : 1) * kBBytes) + 2 * kMaxStages * 8 +
                       4 * 8 + 16 + (EPI == LA_EPI_PARTIAL ? 0 : 128 * kEpiLd * 4 + 128 * 4);
   return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
 }

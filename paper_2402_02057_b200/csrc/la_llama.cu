@@ -54,6 +54,14 @@ struct LlamaPath {
   unsigned long long* trace = nullptr;    // [4 GEMM kinds][256 CTAs][4] (LA_GEMM_TRACE=1)
   float* logits = nullptr;                // device dump target (parity hook), else null
   std::vector<LaGemm> qkv, o, gu, down;
+  // dual-chunk prefill (LA_PREFILL_PAIR, default on): one-tile-per-unit configs
+  // of the four projections (B = two 128-row prompt chunks per weight stage)
+  // and the second chunk's activations
+  bool prefill_pair = false;
+  std::vector<LaGemm> qkv1, o1, gu1, down1;
+  FwdPlan* plan2 = nullptr;
+  float *x2 = nullptr, *ss2 = nullptr, *ws2 = nullptr;
+  __nv_bfloat16 *h2 = nullptr, *q2 = nullptr, *attn2 = nullptr, *act2 = nullptr;
   LaGemm head{};
   int head_tiles = 0;
   int kernels_per_step = 0;
@@ -328,6 +336,18 @@ int llama_create(la_engine* e) {
     RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn, narrow_tpc, LA_EPI_PARTIAL, down_grid));
     track(p->down[l]);
   }
+  p->prefill_pair = !fused && !(getenv("LA_PREFILL_PAIR") && atoi(getenv("LA_PREFILL_PAIR")) == 0);
+  if (p->prefill_pair) {
+    p->qkv1.resize(D.layers); p->o1.resize(D.layers); p->gu1.resize(D.layers); p->down1.resize(D.layers);
+    for (int l = 0; l < D.layers; ++l) {
+      const LlamaLayerW& w = p->lw[l];
+      RET_IF(build_gemm(p->qkv1[l], w.wqkv, H + 2 * KVH, p->h, d, 1));
+      RET_IF(build_gemm(p->o1[l], w.wo, d / 128, p->attn, H * 128, 1));
+      RET_IF(build_gemm(p->gu1[l], w.wgu, D.ffn / 64, p->h, d, 1));
+      RET_IF(build_gemm(p->down1[l], w.wd, d / 128, p->act, D.ffn, 1));
+      track(p->qkv1[l]); track(p->o1[l]); track(p->gu1[l]); track(p->down1[l]);
+    }
+  }
   p->head_tiles = (D.vocab + 127) / 128;
   // LA_HEAD_FUSED=1: the LM head's logits / argmax epilogue inside its GEMM
   // (most tile pairs are owned whole by one CTA: ~54 units per CTA)
@@ -341,6 +361,17 @@ int llama_create(la_engine* e) {
   int* counters = nullptr;
   RET_IF(lalloc(e, &counters, 4096));
   RET_IF(lalloc(e, &p->ws, ws_need));
+  if (p->prefill_pair) {
+    const size_t R = LA_MAX_ROWS, qd = (size_t)H * 128;
+    RET_IF(lalloc(e, &p->ws2, ws_need));
+    RET_IF(lalloc(e, &p->plan2, 1));
+    RET_IF(lalloc(e, &p->x2, R * d));
+    RET_IF(lalloc(e, &p->ss2, (size_t)d));
+    RET_IF(lalloc(e, &p->h2, R * d));
+    RET_IF(lalloc(e, &p->q2, R * qd));
+    RET_IF(lalloc(e, &p->attn2, R * qd));
+    RET_IF(lalloc(e, &p->act2, R * (size_t)D.ffn));
+  }
   RET_IF(lalloc(e, &p->timing, 48));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
   if (trace) RET_IF(lalloc(e, &p->trace, 5 * 256 * 4));   // qkv, o, gu, head, down
@@ -355,6 +386,10 @@ int llama_create(la_engine* e) {
   for (int l = 0; l < D.layers; ++l) {
     fin(p->qkv[l], 0, 0); fin(p->o[l], 1, 1); fin(p->gu[l], 2, 2); fin(p->down[l], 1, 4);
   }
+  for (size_t l = 0; l < p->qkv1.size(); ++l)
+    for (LaGemm* g : {&p->qkv1[l], &p->o1[l], &p->gu1[l], &p->down1[l]}) {
+      g->args.plan = e->d_plan; g->args.ws = p->ws; g->args.counters = counters;
+    }
   for (int l = 0; l < D.layers; ++l) { p->qkv[l].args.nrm = p->nrm; p->gu[l].args.nrm = p->nrm; }
   {
     // O projection ring depth (LA_O_STAGES; 0 = the default 4 stages).  A
@@ -729,8 +764,81 @@ static int mega_forward(la_engine* e, cudaStream_t st, bool head, bool scatter, 
   return LA_OK;
 }
 
+// Two 128-row prompt chunks through all layers, layer-major: every projection
+// streams its weights ONCE for both (dual-chunk GEMM, tpc = 1); the epilogues
+// and attention run per chunk with the chunk's own plan and activations, chunk
+// 0 first (chunk 1's attention reads chunk 0's keys of the same layer).
+static int prefill_pair(la_engine* e, const int* d_tokens, int s0, int R0, int s1, int R1,
+                        cudaStream_t st) {
+  LlamaPath* p = e->llama;
+  struct Chunk {
+    FwdPlan* plan; float *x, *ss, *ws; __nv_bfloat16 *h, *q, *attn, *act;
+  } c[2] = {{e->d_plan, p->x, p->ss, p->ws, p->h, p->q, p->attn, p->act},
+            {p->plan2, p->x2, p->ss2, p->ws2, p->h2, p->q2, p->attn2, p->act2}};
+  la_plan_chain_kernel<<<1, 128, 0, st>>>(c[0].plan, d_tokens, s0, R0);
+  la_plan_chain_kernel<<<1, 128, 0, st>>>(c[1].plan, d_tokens, s1, R1);
+  CK(cudaGetLastError());
+  auto nrm = [&](int i) { LaRowNorm r = p->nrm; r.ss = c[i].ss; return r; };
+  auto resid = [&](int i, const LaGemm* from, const float* g, bool embed) -> int {
+    LaResidNorm r;
+    r.pf = LaPrefetch{};
+    r.plan = c[i].plan;
+    r.ws = from ? c[i].ws : nullptr;
+    r.sp = from ? split_of(*from) : LaSplit{2, 1, 1, 1, 1};
+    r.embed = embed ? p->embed : nullptr;
+    r.x = c[i].x; r.g = g; r.h = c[i].h; r.d = p->d; r.eps = p->eps; r.ss = c[i].ss;
+    CK(la_launch(la_resid_norm_kernel, dim3(p->d / 128, LA_MAX_ROWS / 8), dim3(256), 0, st, p->pdl, r));
+    return LA_OK;
+  };
+  auto dual = [&](const LaGemm& g0, const __nv_bfloat16* b0, const __nv_bfloat16* b1) -> int {
+    LaGemm g = g0;
+    g.args.b = b0; g.args.b2 = b1;
+    g.args.ws = c[0].ws; g.args.ws2 = c[1].ws;
+    g.args.plan = c[0].plan; g.args.plan2 = c[1].plan;
+    return la_gemm_launch(g, st, p->pdl);
+  };
+  __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc);
+  __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc);
+  const size_t lstride = (size_t)e->slots * p->KVH * 128;
+  for (int i = 0; i < 2; ++i) RET_IF(resid(i, nullptr, p->lw[0].attn_norm, true));
+  for (int l = 0; l < p->L; ++l) {
+    RET_IF(dual(p->qkv1[l], c[0].h, c[1].h));
+    for (int i = 0; i < 2; ++i) {
+      LaQkvEpi q{LaPrefetch{}, c[i].plan, c[i].ws, split_of(p->qkv1[l]), c[i].q, kc + l * lstride,
+                 vc + l * lstride, p->rope_cos, p->rope_sin, p->H, p->KVH, nrm(i)};
+      CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
+    }
+    for (int i = 0; i < 2; ++i) {
+      LaAttnFusedArgs a = p->af;
+      a.plan = c[i].plan; a.q = c[i].q; a.out = c[i].attn;
+      a.kc = kc + l * lstride; a.vc = vc + l * lstride;
+      a.pf = LaPrefetch{};
+      CK(la_attn_fused_launch(a, p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
+    }
+    RET_IF(dual(p->o1[l], c[0].attn, c[1].attn));
+    for (int i = 0; i < 2; ++i) RET_IF(resid(i, &p->o1[l], p->lw[l].mlp_norm, false));
+    RET_IF(dual(p->gu1[l], c[0].h, c[1].h));
+    for (int i = 0; i < 2; ++i) {
+      LaSwigluEpi sw{LaPrefetch{}, c[i].plan, c[i].ws, split_of(p->gu1[l]), c[i].act, p->ffn, nrm(i)};
+      CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 16), dim3(128), 0, st, p->pdl, sw));
+    }
+    RET_IF(dual(p->down1[l], c[0].act, c[1].act));
+    const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
+    for (int i = 0; i < 2; ++i) RET_IF(resid(i, &p->down1[l], next, false));
+    CK(cudaGetLastError());
+  }
+  return LA_OK;
+}
+
 int llama_prefill(la_engine* e, const int* d_tokens, int n, cudaStream_t st) {
-  for (int start = 0; start < n; start += LA_MAX_ROWS) {
+  LlamaPath* p = e->llama;
+  int start = 0;
+  // pairs of full 128-row chunks share every weight pass
+  if (p->prefill_pair && !p->mega && !p->af.fuse_qkv)
+    for (; start + LA_MAX_ROWS < n; start += 2 * LA_MAX_ROWS)
+      RET_IF(prefill_pair(e, d_tokens, start, LA_MAX_ROWS, start + LA_MAX_ROWS,
+                          std::min(LA_MAX_ROWS, n - start - LA_MAX_ROWS), st));
+  for (; start < n; start += LA_MAX_ROWS) {
     int R = std::min(LA_MAX_ROWS, n - start);
     la_plan_chain_kernel<<<1, 128, 0, st>>>(e->d_plan, d_tokens, start, R);
     CK(cudaGetLastError());
