@@ -146,10 +146,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = sm;
   // one 192 KB ring: nst stages of (weights a_bytes | step rows 16 KB), the
   // weight and row halves in two contiguous regions (1024-B aligned)
-  const bool dual = args.b2 != nullptr;   // prefill: two row blocks per weight stage
-  const int nst = args.nst > 0 ? args.nst : (args.tpc == LA_TPC || dual ? kStages : kMaxStages);
+  const int nblk = args.nblk > 1 ? args.nblk : 1;   // prefill: row blocks per weight stage
+  const bool multi = nblk > 1;
+  const int nbuf = nblk > 2 ? 1 : 2;                 // TMEM accumulator buffers
+  const int nst = args.nst > 0 ? args.nst : multi ? (nblk > 2 ? 2 : kStages)
+                                                  : (args.tpc == LA_TPC ? kStages : kMaxStages);
   const uint32_t a_stage = (uint32_t)args.tpc * kTileBytes;
-  const uint32_t b_stage = dual ? 2 * kBBytes : kBBytes;
+  const uint32_t b_stage = (uint32_t)nblk * kBBytes;
   uint8_t* sB = sA + nst * a_stage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sA + nst * (a_stage + b_stage));
   uint64_t* empty = full + kMaxStages;
@@ -214,8 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 0] = t_entry;
   const int n_rows = P->n_rows;
   const int n_pad = P->n_pad;
-  const int n_rows2 = dual ? args.plan2->n_rows : 0;
-  const int n_pad2 = dual ? args.plan2->n_pad : 0;
+  int n_rows_x[3] = {0, 0, 0}, n_pad_x[3] = {0, 0, 0};
+  for (int j = 1; j < nblk; ++j) { n_rows_x[j - 1] = args.planx[j - 1]->n_rows; n_pad_x[j - 1] = args.planx[j - 1]->n_pad; }
   if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
 
   if (n_rows == 0) {
@@ -229,14 +232,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol_x = ptx::policy_evict_last();    // step rows: re-read by every CTA
-      const uint32_t bbytes = (uint32_t)n_pad * 128, bbytes2 = (uint32_t)n_pad2 * 128;
+      uint32_t bbytes_all = (uint32_t)n_pad * 128;
+      for (int j = 1; j < nblk; ++j) bbytes_all += (uint32_t)n_pad_x[j - 1] * 128;
+      const uint32_t bbytes = (uint32_t)n_pad * 128;
       long it = 0;
       for (long u = u_begin; u < u_end; ++u, ++it) {
         const int k = (int)(u % kb);
         const int s = (int)(it % nst);
         const uint32_t r = (uint32_t)(it / nst);
         const bool load_b = !(args.debug & 1);
-        const uint32_t bb = load_b ? bbytes + bbytes2 : 0;
+        const uint32_t bb = load_b ? bbytes_all : 0;
         if (it < n_pre) {
           ptx::mbar_expect_tx(&full[s], bb);   // weights already in flight
         } else {
@@ -246,9 +251,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (load_b) {
           ptx::bulk_load(sB + s * b_stage, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
-          if (dual && bbytes2)
-            ptx::bulk_load(sB + s * b_stage + kBBytes, args.b2 + (size_t)k * (kBBytes / 2), bbytes2,
-                           &full[s], pol_x);
+          for (int j = 1; j < nblk; ++j)
+            ptx::bulk_load(sB + s * b_stage + j * kBBytes, args.bx[j - 1] + (size_t)k * (kBBytes / 2),
+                           (uint32_t)n_pad_x[j - 1] * 128, &full[s], pol_x);
         }
       }
     }
@@ -256,7 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = ptx::umma_idesc_bf16(128, (uint32_t)n_pad);
-      const uint32_t idesc2 = ptx::umma_idesc_bf16(128, (uint32_t)(n_pad2 > 0 ? n_pad2 : 16));
+      uint32_t idesc_x[3];
+      for (int j = 0; j < 3; ++j) idesc_x[j] = ptx::umma_idesc_bf16(128, (uint32_t)(n_pad_x[j] > 0 ? n_pad_x[j] : 16));
       long it = 0, u = u_begin;
       int use[2] = {0, 0}, buf = 0;
       while (u < u_end) {
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&tempty[buf], (use[buf] - 1) & 1);
           ptx::tc_fence_after();
         }
-        const uint32_t d_tmem = tmem + buf * (LA_TPC * 128);   // TMEM sized for LA_TPC
+        const uint32_t d_tmem = tmem + buf * (LA_TPC * 128);   // TMEM sized for LA_TPC (single buffer: buf = 0)
         for (; u < seg_end; ++u, ++it) {
           const int s = (int)(it % nst);
           ptx::mbar_wait(&full[s], (uint32_t)(it / nst) & 1);
@@ -283,17 +289,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kTileBytes + kk * 32),
                              ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
                              (u > seg_start || kk > 0) ? 1u : 0u);
-          if (dual && n_pad2 > 0)   // second row block into the buffer's upper 128 columns
+          for (int j = 1; j < nblk; ++j)   // row block j into columns [128 j, 128 j + 128)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              ptx::umma_bf16(d_tmem + 128, ptx::umma_desc_sw128(a_addr + kk * 32),
-                             ptx::umma_desc_sw128(b_addr + kBBytes + kk * 32), idesc2,
+              ptx::umma_bf16(d_tmem + 128 * j, ptx::umma_desc_sw128(a_addr + kk * 32),
+                             ptx::umma_desc_sw128(b_addr + j * kBBytes + kk * 32), idesc_x[j - 1],
                              (u > seg_start || kk > 0) ? 1u : 0u);
           ptx::umma_commit(&empty[s]);
         }
         ptx::umma_commit(&tfull[buf]);
         use[buf]++;
-        buf ^= 1;
+        buf = nbuf == 2 ? buf ^ 1 : 0;
       }
       if (args.trace) args.trace[blockIdx.x * 4 + 2] = globaltimer();
     }
@@ -312,13 +318,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&tfull[buf], use[buf] & 1);
       ptx::tc_fence_after();
       if (EPI == LA_EPI_PARTIAL || seg != 0) {
-        // write this piece's fp32 partial (dual mode: both row blocks)
-        const int nblk = dual ? 2 : tpc;
-        for (int tt = 0; tt < nblk; ++tt) {
+        // write this piece's fp32 partial (multi-chunk mode: every row block)
+        const int nout = multi ? nblk : tpc;
+        for (int tt = 0; tt < nout; ++tt) {
           const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
-          const int ftile = dual ? tile : tile * tpc + tt;
-          float* wsp = (dual && tt ? args.ws2 : args.ws) + ((size_t)ftile * args.max_segs + seg) * 128 * 128 + f;
-          const int nr = dual && tt ? n_rows2 : n_rows, np = dual && tt ? n_pad2 : n_pad;
+          const int ftile = multi ? tile : tile * tpc + tt;
+          float* wsp = (multi && tt ? args.wsx[tt - 1] : args.ws) + ((size_t)ftile * args.max_segs + seg) * 128 * 128 + f;
+          const int nr = multi && tt ? n_rows_x[tt - 1] : n_rows, np = multi && tt ? n_pad_x[tt - 1] : n_pad;
           for (int c0 = 0; c0 < np; c0 += 32) {
             float v[32];
             ptx::tmem_ld32(t_base + c0, v);
@@ -380,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive(&tempty[buf]);
       }
       use[buf]++;
-      buf ^= 1;
+      buf = nbuf == 2 ? buf ^ 1 : 0;
       u = seg_end;
     }
   }
@@ -469,9 +475,10 @@ static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
     attr = true;
   }
   // the ring (nst stages), barriers / TMEM slot, and the fused epilogue's staging
-  const bool dual = g.args.b2 != nullptr;
-  const int nst = g.args.nst > 0 ? g.args.nst : (g.args.tpc == LA_TPC || dual ? kStages : kMaxStages);
-  const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + (dual ? 2 : 1) * kBBytes) + 2 * kMaxStages * 8 +
+  const int nblk = g.args.nblk > 1 ? g.args.nblk : 1;
+  const int nst = g.args.nst > 0 ? g.args.nst : nblk > 1 ? (nblk > 2 ? 2 : kStages)
+                                                         : (g.args.tpc == LA_TPC ? kStages : kMaxStages);
+  const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + nblk * kBBytes) + 2 * kMaxStages * 8 +
                       4 * 8 + 16 + (EPI == LA_EPI_PARTIAL ? 0 : 128 * kEpiLd * 4 + 128 * 4);
   return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
 }

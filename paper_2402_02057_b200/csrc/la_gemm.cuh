@@ -50,12 +50,14 @@ struct LaGemmArgs {
   int l2pf;    // units beyond the smem ring prefetched to L2 before the dependency wait
   int nst;     // smem ring stages (0: the default for tpc); fewer stages = a smaller CTA
                // that fits beside the previous kernel's CTA and streams its weights early
-  // ---- dual-chunk mode (prefill, b2 != null, tpc == 1, split-K pieces only):
-  // every weight stage multiplies TWO row blocks -- b (rows of `plan`) into ws
-  // and b2 (rows of plan2) into ws2 -- so one weight pass serves 256 rows
-  const __nv_bfloat16* b2;
-  float* ws2;
-  const FwdPlan* plan2;
+  // ---- multi-chunk mode (prefill, nblk > 1, tpc == 1, split-K pieces only):
+  // every weight stage multiplies nblk <= 4 row blocks -- block 0 = b / ws /
+  // plan, block j = bx[j-1] / wsx[j-1] / planx[j-1] -- so one weight pass
+  // serves up to 512 rows (TMEM: double-buffered for <= 2 blocks, single above)
+  int nblk;
+  const __nv_bfloat16* bx[3];
+  float* wsx[3];
+  const FwdPlan* planx[3];
   // ---- fused epilogue (LA_EPI_QKV / SWIGLU / LOGITS): stream-K fix-up in
   // the GEMM -- the CTA owning a tile's k = 0 piece adds the other pieces'
   // partials (in piece order) and applies the epilogue

@@ -57,11 +57,13 @@ struct LlamaPath {
   // dual-chunk prefill (LA_PREFILL_PAIR, default on): one-tile-per-unit configs
   // of the four projections (B = two 128-row prompt chunks per weight stage)
   // and the second chunk's activations
-  bool prefill_pair = false;
+  int prefill_group = 1;                  // prompt chunks per weight pass (LA_PREFILL_GROUP, <= 4)
   std::vector<LaGemm> qkv1, o1, gu1, down1;
-  FwdPlan* plan2 = nullptr;
-  float *x2 = nullptr, *ss2 = nullptr, *ws2 = nullptr;
-  __nv_bfloat16 *h2 = nullptr, *q2 = nullptr, *attn2 = nullptr, *act2 = nullptr;
+  struct ChunkBufs {                      // chunks 1..3 of a group (chunk 0 uses the step buffers)
+    FwdPlan* plan = nullptr;
+    float *x = nullptr, *ss = nullptr, *ws = nullptr;
+    __nv_bfloat16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
+  } cx[3];
   LaGemm head{};
   int head_tiles = 0;
   int kernels_per_step = 0;
@@ -336,8 +338,8 @@ int llama_create(la_engine* e) {
     RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn, narrow_tpc, LA_EPI_PARTIAL, down_grid));
     track(p->down[l]);
   }
-  p->prefill_pair = !fused && !(getenv("LA_PREFILL_PAIR") && atoi(getenv("LA_PREFILL_PAIR")) == 0);
-  if (p->prefill_pair) {
+  p->prefill_group = fused ? 1 : std::max(1, std::min(4, getenv("LA_PREFILL_GROUP") ? atoi(getenv("LA_PREFILL_GROUP")) : 4));
+  if (p->prefill_group > 1) {
     p->qkv1.resize(D.layers); p->o1.resize(D.layers); p->gu1.resize(D.layers); p->down1.resize(D.layers);
     for (int l = 0; l < D.layers; ++l) {
       const LlamaLayerW& w = p->lw[l];
@@ -361,16 +363,17 @@ int llama_create(la_engine* e) {
   int* counters = nullptr;
   RET_IF(lalloc(e, &counters, 4096));
   RET_IF(lalloc(e, &p->ws, ws_need));
-  if (p->prefill_pair) {
+  for (int j = 0; j + 1 < p->prefill_group; ++j) {
     const size_t R = LA_MAX_ROWS, qd = (size_t)H * 128;
-    RET_IF(lalloc(e, &p->ws2, ws_need));
-    RET_IF(lalloc(e, &p->plan2, 1));
-    RET_IF(lalloc(e, &p->x2, R * d));
-    RET_IF(lalloc(e, &p->ss2, (size_t)d));
-    RET_IF(lalloc(e, &p->h2, R * d));
-    RET_IF(lalloc(e, &p->q2, R * qd));
-    RET_IF(lalloc(e, &p->attn2, R * qd));
-    RET_IF(lalloc(e, &p->act2, R * (size_t)D.ffn));
+    LlamaPath::ChunkBufs& c = p->cx[j];
+    RET_IF(lalloc(e, &c.ws, ws_need));
+    RET_IF(lalloc(e, &c.plan, 1));
+    RET_IF(lalloc(e, &c.x, R * d));
+    RET_IF(lalloc(e, &c.ss, (size_t)d));
+    RET_IF(lalloc(e, &c.h, R * d));
+    RET_IF(lalloc(e, &c.q, R * qd));
+    RET_IF(lalloc(e, &c.attn, R * qd));
+    RET_IF(lalloc(e, &c.act, R * (size_t)D.ffn));
   }
   RET_IF(lalloc(e, &p->timing, 48));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
@@ -764,19 +767,26 @@ static int mega_forward(la_engine* e, cudaStream_t st, bool head, bool scatter, 
   return LA_OK;
 }
 
-// Two 128-row prompt chunks through all layers, layer-major: every projection
-// streams its weights ONCE for both (dual-chunk GEMM, tpc = 1); the epilogues
-// and attention run per chunk with the chunk's own plan and activations, chunk
-// 0 first (chunk 1's attention reads chunk 0's keys of the same layer).
-static int prefill_pair(la_engine* e, const int* d_tokens, int s0, int R0, int s1, int R1,
-                        cudaStream_t st) {
+// Up to four 128-row prompt chunks through all layers, layer-major: every
+// projection streams its weights ONCE for the group (multi-chunk GEMM,
+// tpc = 1); the epilogues and attention run per chunk with the chunk's own plan
+// and activations, in chunk order (chunk i's attention reads the keys of
+// chunks < i of the same layer).
+static int prefill_chunks(la_engine* e, const int* d_tokens, int start, int n_chunks, int n_tok,
+                          cudaStream_t st) {
   LlamaPath* p = e->llama;
   struct Chunk {
     FwdPlan* plan; float *x, *ss, *ws; __nv_bfloat16 *h, *q, *attn, *act;
-  } c[2] = {{e->d_plan, p->x, p->ss, p->ws, p->h, p->q, p->attn, p->act},
-            {p->plan2, p->x2, p->ss2, p->ws2, p->h2, p->q2, p->attn2, p->act2}};
-  la_plan_chain_kernel<<<1, 128, 0, st>>>(c[0].plan, d_tokens, s0, R0);
-  la_plan_chain_kernel<<<1, 128, 0, st>>>(c[1].plan, d_tokens, s1, R1);
+  } c[4];
+  c[0] = {e->d_plan, p->x, p->ss, p->ws, p->h, p->q, p->attn, p->act};
+  for (int j = 1; j < n_chunks; ++j) {
+    const LlamaPath::ChunkBufs& b = p->cx[j - 1];
+    c[j] = {b.plan, b.x, b.ss, b.ws, b.h, b.q, b.attn, b.act};
+  }
+  for (int i = 0; i < n_chunks; ++i) {
+    const int s0 = start + i * LA_MAX_ROWS;
+    la_plan_chain_kernel<<<1, 128, 0, st>>>(c[i].plan, d_tokens, s0, std::min(LA_MAX_ROWS, start + n_tok - s0));
+  }
   CK(cudaGetLastError());
   auto nrm = [&](int i) { LaRowNorm r = p->nrm; r.ss = c[i].ss; return r; };
   auto resid = [&](int i, const LaGemm* from, const float* g, bool embed) -> int {
@@ -790,41 +800,43 @@ static int prefill_pair(la_engine* e, const int* d_tokens, int s0, int R0, int s
     CK(la_launch(la_resid_norm_kernel, dim3(p->d / 128, LA_MAX_ROWS / 8), dim3(256), 0, st, p->pdl, r));
     return LA_OK;
   };
-  auto dual = [&](const LaGemm& g0, const __nv_bfloat16* b0, const __nv_bfloat16* b1) -> int {
+  auto multi = [&](const LaGemm& g0, __nv_bfloat16* Chunk::*b) -> int {
     LaGemm g = g0;
-    g.args.b = b0; g.args.b2 = b1;
-    g.args.ws = c[0].ws; g.args.ws2 = c[1].ws;
-    g.args.plan = c[0].plan; g.args.plan2 = c[1].plan;
+    g.args.nblk = n_chunks;
+    g.args.b = c[0].*b; g.args.ws = c[0].ws; g.args.plan = c[0].plan;
+    for (int j = 1; j < n_chunks; ++j) {
+      g.args.bx[j - 1] = c[j].*b; g.args.wsx[j - 1] = c[j].ws; g.args.planx[j - 1] = c[j].plan;
+    }
     return la_gemm_launch(g, st, p->pdl);
   };
   __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc);
   __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc);
   const size_t lstride = (size_t)e->slots * p->KVH * 128;
-  for (int i = 0; i < 2; ++i) RET_IF(resid(i, nullptr, p->lw[0].attn_norm, true));
+  for (int i = 0; i < n_chunks; ++i) RET_IF(resid(i, nullptr, p->lw[0].attn_norm, true));
   for (int l = 0; l < p->L; ++l) {
-    RET_IF(dual(p->qkv1[l], c[0].h, c[1].h));
-    for (int i = 0; i < 2; ++i) {
+    RET_IF(multi(p->qkv1[l], &Chunk::h));
+    for (int i = 0; i < n_chunks; ++i) {
       LaQkvEpi q{LaPrefetch{}, c[i].plan, c[i].ws, split_of(p->qkv1[l]), c[i].q, kc + l * lstride,
                  vc + l * lstride, p->rope_cos, p->rope_sin, p->H, p->KVH, nrm(i)};
       CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < n_chunks; ++i) {
       LaAttnFusedArgs a = p->af;
       a.plan = c[i].plan; a.q = c[i].q; a.out = c[i].attn;
       a.kc = kc + l * lstride; a.vc = vc + l * lstride;
       a.pf = LaPrefetch{};
       CK(la_attn_fused_launch(a, p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
     }
-    RET_IF(dual(p->o1[l], c[0].attn, c[1].attn));
-    for (int i = 0; i < 2; ++i) RET_IF(resid(i, &p->o1[l], p->lw[l].mlp_norm, false));
-    RET_IF(dual(p->gu1[l], c[0].h, c[1].h));
-    for (int i = 0; i < 2; ++i) {
+    RET_IF(multi(p->o1[l], &Chunk::attn));
+    for (int i = 0; i < n_chunks; ++i) RET_IF(resid(i, &p->o1[l], p->lw[l].mlp_norm, false));
+    RET_IF(multi(p->gu1[l], &Chunk::h));
+    for (int i = 0; i < n_chunks; ++i) {
       LaSwigluEpi sw{LaPrefetch{}, c[i].plan, c[i].ws, split_of(p->gu1[l]), c[i].act, p->ffn, nrm(i)};
       CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 16), dim3(128), 0, st, p->pdl, sw));
     }
-    RET_IF(dual(p->down1[l], c[0].act, c[1].act));
+    RET_IF(multi(p->down1[l], &Chunk::act));
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
-    for (int i = 0; i < 2; ++i) RET_IF(resid(i, &p->down1[l], next, false));
+    for (int i = 0; i < n_chunks; ++i) RET_IF(resid(i, &p->down1[l], next, false));
     CK(cudaGetLastError());
   }
   return LA_OK;
@@ -833,11 +845,14 @@ static int prefill_pair(la_engine* e, const int* d_tokens, int s0, int R0, int s
 int llama_prefill(la_engine* e, const int* d_tokens, int n, cudaStream_t st) {
   LlamaPath* p = e->llama;
   int start = 0;
-  // pairs of full 128-row chunks share every weight pass
-  if (p->prefill_pair && !p->mega && !p->af.fuse_qkv)
-    for (; start + LA_MAX_ROWS < n; start += 2 * LA_MAX_ROWS)
-      RET_IF(prefill_pair(e, d_tokens, start, LA_MAX_ROWS, start + LA_MAX_ROWS,
-                          std::min(LA_MAX_ROWS, n - start - LA_MAX_ROWS), st));
+  // groups of up to prefill_group 128-row chunks share every weight pass
+  if (p->prefill_group > 1 && !p->mega && !p->af.fuse_qkv)
+    while (start + LA_MAX_ROWS < n) {
+      const int chunks = std::min(p->prefill_group, (n - start + LA_MAX_ROWS - 1) / LA_MAX_ROWS);
+      const int tok = std::min(n - start, chunks * LA_MAX_ROWS);
+      RET_IF(prefill_chunks(e, d_tokens, start, chunks, tok, st));
+      start += tok;
+    }
   for (; start < n; start += LA_MAX_ROWS) {
     int R = std::min(LA_MAX_ROWS, n - start);
     la_plan_chain_kernel<<<1, 128, 0, st>>>(e->d_plan, d_tokens, start, R);
