@@ -374,7 +374,7 @@ __device__ void attn_merge_cluster(const LaAttnFusedArgs& a, uint8_t* smem, int 
 
 // One attention unit e = (KV head, row block, key chunk) after the dependency
 // wait, on a K/V ring of STAGES tiles at smem (plus the mask at mask_off).
-template <int STAGES>
+template <int STAGES, bool CLUSTER = false>
 __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
   stamp(a, 1);
   const FwdPlan* P = a.plan;
@@ -400,7 +400,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
   }
 
   uint8_t* sKV = smem;                                                   // [STAGES][K | V]
-  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + (a.tc ? kMaskOff : a.cluster ? kClMaskOff : STAGES * kTileBytes));   // [128][4]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + (a.tc ? kMaskOff : CLUSTER ? kClMaskOff : STAGES * kTileBytes));   // [128][4]
   int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
   uint64_t* sBars = reinterpret_cast<uint64_t*>(sFlag + 4);           // tensor-core path
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBars + 2);
@@ -621,7 +621,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
     for (int half = 0; half < 2; ++half) {
       const int row = qrow0 + half * 8;
       if (rb * 128 + row >= nq) continue;
-      if (a.cluster) {
+      if constexpr (CLUSTER) {
         const unsigned owner = (unsigned)(row / rows_per_);
         const int slot = split * rows_per_ + (row - (int)owner * rows_per_);
         const uint32_t dst = dsmem_addr(smem + kClPush + (size_t)slot * 512, owner);
@@ -648,7 +648,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
         __stcg(a.part_ml + (grp * (S + 1) + split) * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
     }
   }
-  if (a.cluster) {
+  if constexpr (CLUSTER) {
     // every chunk CTA of the group is in this cluster: one barrier makes the
     // pushed partials visible; each CTA then merges its rows from local smem
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -750,13 +750,22 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   la_l2_prefetch_gemm(a.pf);
   attn_prefetch_kv(a, blockIdx.x);
   la_pdl_wait();
-  if (a.cluster) attn_unit<kClStages>(a, smem, blockIdx.x);
-  else attn_unit<kStages>(a, smem, blockIdx.x);
+  attn_unit<kStages>(a, smem, blockIdx.x);
   if (a.dbg & 8) {   // timing experiment: 5 us of extra attention time per CTA
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
     do { asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); } while (t - t0 < 5000ull);
   }
+}
+
+// LA_ATTN_CLUSTER=1 variant: launched as clusters of S+1 CTAs (one per
+// (KV head, row block)), partials pushed into the merging CTA's smem
+__global__ void __launch_bounds__(256, 1) la_attn_cluster_kernel(LaAttnFusedArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  la_pdl_trigger();
+  attn_prefetch_kv(a, blockIdx.x);
+  la_pdl_wait();
+  attn_unit<kClStages, true>(a, smem, blockIdx.x);
 }
 
 cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_t st, bool pdl) {
@@ -781,6 +790,16 @@ cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_
   }
   cfg.attrs = at;
   cfg.numAttrs = n;
+  if (a.cluster) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(la_attn_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)la_attn_fused_smem(false, true));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    return cudaLaunchKernelEx(&cfg, la_attn_cluster_kernel, a);
+  }
   return cudaLaunchKernelEx(&cfg, la_attn_fused_kernel, a);
 }
 

@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = sm;
   // one 192 KB ring: nst stages of (weights a_bytes | step rows 16 KB), the
   // weight and row halves in two contiguous regions (1024-B aligned)
-  const int nblk = args.nblk > 1 ? args.nblk : 1;   // prefill: row blocks per weight stage
-  const bool multi = nblk > 1;
+  constexpr bool multi = EPI == LA_EPI_MULTI;        // prefill: row blocks per weight stage
+  const int nblk = multi ? args.nblk : 1;
   const int nbuf = nblk > 2 ? 1 : 2;                 // TMEM accumulator buffers
   const int nst = args.nst > 0 ? args.nst : multi ? (nblk > 2 ? 2 : kStages)
                                                   : (args.tpc == LA_TPC ? kStages : kMaxStages);
@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_rows = P->n_rows;
   const int n_pad = P->n_pad;
   int n_rows_x[3] = {0, 0, 0}, n_pad_x[3] = {0, 0, 0};
-  for (int j = 1; j < nblk; ++j) { n_rows_x[j - 1] = args.planx[j - 1]->n_rows; n_pad_x[j - 1] = args.planx[j - 1]->n_pad; }
+  if constexpr (multi)
+    for (int j = 1; j < nblk; ++j) { n_rows_x[j - 1] = args.planx[j - 1]->n_rows; n_pad_x[j - 1] = args.planx[j - 1]->n_pad; }
   if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
 
   if (n_rows == 0) {
@@ -233,7 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint64_t pol_x = ptx::policy_evict_last();    // step rows: re-read by every CTA
       uint32_t bbytes_all = (uint32_t)n_pad * 128;
-      for (int j = 1; j < nblk; ++j) bbytes_all += (uint32_t)n_pad_x[j - 1] * 128;
+      if constexpr (multi)
+        for (int j = 1; j < nblk; ++j) bbytes_all += (uint32_t)n_pad_x[j - 1] * 128;
       const uint32_t bbytes = (uint32_t)n_pad * 128;
       long it = 0;
       for (long u = u_begin; u < u_end; ++u, ++it) {
@@ -251,9 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (load_b) {
           ptx::bulk_load(sB + s * b_stage, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
-          for (int j = 1; j < nblk; ++j)
-            ptx::bulk_load(sB + s * b_stage + j * kBBytes, args.bx[j - 1] + (size_t)k * (kBBytes / 2),
-                           (uint32_t)n_pad_x[j - 1] * 128, &full[s], pol_x);
+          if constexpr (multi)
+            for (int j = 1; j < nblk; ++j)
+              ptx::bulk_load(sB + s * b_stage + j * kBBytes, args.bx[j - 1] + (size_t)k * (kBBytes / 2),
+                             (uint32_t)n_pad_x[j - 1] * 128, &full[s], pol_x);
         }
       }
     }
@@ -261,8 +264,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = ptx::umma_idesc_bf16(128, (uint32_t)n_pad);
-      uint32_t idesc_x[3];
-      for (int j = 0; j < 3; ++j) idesc_x[j] = ptx::umma_idesc_bf16(128, (uint32_t)(n_pad_x[j] > 0 ? n_pad_x[j] : 16));
+      uint32_t idesc_x[3] = {0u, 0u, 0u};
+      if constexpr (multi)
+        for (int j = 0; j < 3; ++j) idesc_x[j] = ptx::umma_idesc_bf16(128, (uint32_t)(n_pad_x[j] > 0 ? n_pad_x[j] : 16));
       long it = 0, u = u_begin;
       int use[2] = {0, 0}, buf = 0;
       while (u < u_end) {
@@ -289,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kTileBytes + kk * 32),
                              ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
                              (u > seg_start || kk > 0) ? 1u : 0u);
+          if constexpr (multi)
           for (int j = 1; j < nblk; ++j)   // row block j into columns [128 j, 128 j + 128)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg = (int)(blockIdx.x - c_first);
       ptx::mbar_wait(&tfull[buf], use[buf] & 1);
       ptx::tc_fence_after();
-      if (EPI == LA_EPI_PARTIAL || seg != 0) {
+      if (EPI == LA_EPI_PARTIAL || multi || seg != 0) {
         // write this piece's fp32 partial (multi-chunk mode: every row block)
         const int nout = multi ? nblk : tpc;
         for (int tt = 0; tt < nout; ++tt) {
@@ -336,12 +341,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[buf]);
-        if (EPI != LA_EPI_PARTIAL) {
+        if (EPI != LA_EPI_PARTIAL && !multi) {
           __threadfence();
           ptx::named_bar_sync(1, 128);
           if (et == 0) atomicAdd(args.counters + tile, 1);
         }
-      } else if constexpr (EPI != LA_EPI_PARTIAL) {
+      } else if constexpr (EPI != LA_EPI_PARTIAL && EPI != LA_EPI_MULTI) {
         // owner of the tile's k = 0 piece: wait for the other pieces, sum them
         // in piece order onto the accumulator, apply the fused epilogue
         const int nseg = (int)(la_cta_of((long)(tile + 1) * kb - 1, U, Pn) - c_first + 1);
@@ -479,7 +484,7 @@ static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
   const int nst = g.args.nst > 0 ? g.args.nst : nblk > 1 ? (nblk > 2 ? 2 : kStages)
                                                          : (g.args.tpc == LA_TPC ? kStages : kMaxStages);
   const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + nblk * kBBytes) + 2 * kMaxStages * 8 +
-                      4 * 8 + 16 + (EPI == LA_EPI_PARTIAL ? 0 : 128 * kEpiLd * 4 + 128 * 4);
+                      4 * 8 + 16 + (EPI == LA_EPI_PARTIAL || EPI == LA_EPI_MULTI ? 0 : 128 * kEpiLd * 4 + 128 * 4);
   return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
 }
 
@@ -489,7 +494,7 @@ int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {
     case LA_EPI_QKV: e = launch_epi<LA_EPI_QKV>(g, st, pdl); break;
     case LA_EPI_SWIGLU: e = launch_epi<LA_EPI_SWIGLU>(g, st, pdl); break;
     case LA_EPI_LOGITS: e = launch_epi<LA_EPI_LOGITS>(g, st, pdl); break;
-    default: e = launch_epi<LA_EPI_PARTIAL>(g, st, pdl); break;
+    default: e = g.args.nblk > 1 ? launch_epi<LA_EPI_MULTI>(g, st, pdl) : launch_epi<LA_EPI_PARTIAL>(g, st, pdl); break;
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { la_set_error("gemm launch: %s", cudaGetErrorString(e)); return LA_ERR_CUDA; }

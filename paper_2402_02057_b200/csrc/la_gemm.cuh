@@ -73,7 +73,8 @@ struct LaGemmArgs {
   LaRowNorm nrm;                     // fused epilogues: deferred RMSNorm of the input rows
 };
 
-enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_LOGITS = 3 };
+enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_LOGITS = 3,
+                 LA_EPI_MULTI = 4 };   // split-K pieces, nblk row blocks (prefill; chosen by nblk > 1)
 
 struct LaGemm {
   LaGemmArgs args;
