@@ -248,6 +248,7 @@ int32_t la_decode_lookahead_group(la_engine* const* engines, int32_t n, const la
  * every launch since the last reset.  out16[4*k + 0] = summed ns,
  * out16[4*k + 1] = launches, for k = 0 QKV, 1 O/down (residual), 2 gate/up,
  * 3 LM head. */
+int32_t la_gemm_timing_enable(la_engine* e, int32_t on);   /* off by default (costs ~4 % of a step) */
 int32_t la_gemm_timing_reset(la_engine* e);
 int32_t la_gemm_timing_read(la_engine* e, double* out16);
 /* Device time of the persistent forward kernel (bf16 path): out2 = {summed ns,

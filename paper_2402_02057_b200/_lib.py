@@ -33,7 +33,7 @@ EXPORTS = (
     "la_last_error", "la_abi_version", "la_weight_count", "la_weight_name", "la_create",
     "la_destroy", "la_decode_lookahead", "la_decode_autoregressive", "la_forward_layout",
     "la_lp_unique_id", "la_lp_init", "la_decode_lookahead_group", "la_debug_read",
-    "la_gemm_timing_reset", "la_gemm_timing_read", "la_forward_timing_read", "la_packed_bytes",
+    "la_gemm_timing_enable", "la_gemm_timing_reset", "la_gemm_timing_read", "la_forward_timing_read", "la_packed_bytes",
     "la_decode_jacobi", "la_decode_lookahead_sampled", "la_decode_autoregressive_sampled",
     "la_adjust_distributions", "la_verify_sample_dists", "la_pcg64_draws",
     "la_session_start", "la_session_step", "la_session_read", "la_pool_test",
@@ -153,6 +153,7 @@ def load(path: str | os.PathLike | None = None):
     lib.la_session_read.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _P32]
     lib.la_pool_test.argtypes = [C.c_int32, C.c_int32, C.c_int32, _P32, C.c_int32, C.c_int32, _P32,
                                  C.c_int32, C.c_int32, _P32, _P32, _P32]
+    lib.la_gemm_timing_enable.argtypes = [C.c_void_p, C.c_int32]
     lib.la_gemm_timing_reset.argtypes = [C.c_void_p]
     lib.la_gemm_timing_read.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     for name in EXPORTS:

@@ -383,7 +383,10 @@ int llama_create(la_engine* e) {
   auto fin = [&](LaGemm& gg, int kind, int tkind) {
     gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.debug = dbg; gg.args.counters = counters;
     gg.args.l2pf = l2pf;
-    gg.args.timing = p->timing + 8 * kind;
+    // in-kernel launch timing is opt-in (la_gemm_timing_enable / LA_GEMM_TIMING=1):
+    // its atomics sit on the producer thread's path and cost ~4 % of a step
+    static const int timing_on = getenv("LA_GEMM_TIMING") ? atoi(getenv("LA_GEMM_TIMING")) : 0;
+    gg.args.timing = timing_on ? p->timing + 8 * kind : nullptr;
     gg.args.trace = trace ? p->trace + 256 * 4 * tkind : nullptr;
   };
   for (int l = 0; l < D.layers; ++l) {
@@ -1059,6 +1062,23 @@ int llama_read_trace(la_engine* e, void* host, size_t bytes) {
 }
 
 // ------------------------------------------------------- GEMM timing ABI
+// switch the in-kernel launch timing of the GEMMs on / off (the cached step
+// graphs bake the kernel arguments: they are rebuilt on next use)
+extern "C" int32_t la_gemm_timing_enable(la_engine* e, int32_t on) {
+  if (!e || !e->llama) { la_set_error("no bf16 path on this engine"); return LA_ERR_INVALID_CONFIG; }
+  LlamaPath* p = e->llama;
+  CK(cudaSetDevice(e->device));
+  CK(cudaDeviceSynchronize());
+  auto set = [&](LaGemm& g, int kind) { g.args.timing = on ? p->timing + 8 * kind : nullptr; };
+  for (int l = 0; l < p->L; ++l) { set(p->qkv[l], 0); set(p->o[l], 1); set(p->gu[l], 2); set(p->down[l], 1); }
+  set(p->head, 3);
+  if (p->loop_exec) { cudaGraphExecDestroy(p->loop_exec); p->loop_exec = nullptr; }
+  if (p->loop_graph) { cudaGraphDestroy(p->loop_graph); p->loop_graph = nullptr; }
+  if (p->fwd_exec) { cudaGraphExecDestroy(p->fwd_exec); p->fwd_exec = nullptr; }
+  if (p->fwd_graph) { cudaGraphDestroy(p->fwd_graph); p->fwd_graph = nullptr; }
+  return LA_OK;
+}
+
 extern "C" int32_t la_gemm_timing_reset(la_engine* e) {
   if (!e || !e->llama) { la_set_error("no bf16 path on this engine"); return LA_ERR_INVALID_CONFIG; }
   CK(cudaSetDevice(e->device));
