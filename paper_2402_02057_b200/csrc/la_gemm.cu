@@ -164,17 +164,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sRstd = sEpi + 128 * kEpiLd;   // fused epilogues: per-row deferred-norm scale
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < nst; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
-    ptx::fence_barrier_init();
-  }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
   const int kb = args.kb;
   const int tpc = args.tpc;
   const int n_units_t = args.n_tiles / tpc;      // unit tiles (pairs when tpc == 2)
@@ -183,10 +172,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long u_begin = (long)blockIdx.x * U / Pn;
   const long u_end = (long)(blockIdx.x + 1) * U / Pn;
   const int n_pre = (int)min((long)nst, u_end - u_begin);
-
-  // PDL: the weights do not depend on the previous kernel, so the first
-  // stages' weight tiles stream in while the previous kernel drains.
-  la_pdl_trigger();
   // weight block of unit u: packed tiles are pair-interleaved per k-block, so
   // a 2-tile unit is one 32 KB copy and a 1-tile unit one 16 KB copy
   const uint32_t a_bytes = (uint32_t)tpc * kTileBytes;
@@ -195,14 +180,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long t = u / kb, k = u % kb;
     return args.a + ((size_t)((t / LA_TPC) * kb + k) * LA_TPC + (t % LA_TPC)) * (kTileBytes / 2);
   };
+  // PDL: the weights do not depend on the previous kernel, so the first
+  // stages' weight tiles stream in while the previous kernel drains -- issued
+  // right after the barrier init, overlapping warp 1's TMEM allocation
+  la_pdl_trigger();
   uint64_t pol_w = 0;
-  if (warp == 0 && lane == 0) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
+    ptx::fence_barrier_init();
     pol_w = ptx::policy_evict_first();   // weights: streamed once
     for (int i = 0; i < n_pre; ++i) {
       ptx::mbar_expect_tx_noarrive(&full[i], a_bytes);
       ptx::bulk_load(sA + i * a_stage, a_src(u_begin + i), a_bytes, &full[i], pol_w);
     }
   }
+  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
   if (warp == 0 && lane == 0 && args.l2pf > 0) {
     // keep HBM streaming while the previous kernel finishes: the units just
     // beyond the smem ring go to L2 (a cache hint, always safe)
