@@ -37,6 +37,8 @@ struct LaAttnFusedArgs {
   int H, KVH, S, nrb_max;
   float scale;
   int spread_merge;              // grid <= SMs: every chunk CTA merges a share of the rows
+  int sms;                       // > 0: also spread-merge any launch whose ACTIVE units (row
+                                 // blocks in use x KVH x (S+1)) fit on this many SMs
   int fuse_qkv;                  // grid <= SMs: the QKV epilogue runs here first (grid barrier)
   int tc;                        // tcgen05 QK^T / PV for chunks of <= 6 key tiles
   int cluster;                   // launched as clusters of S+1 CTAs = one (KV head, row block):

@@ -388,6 +388,9 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
   const int rb = (e / (S + 1)) % a.nrb_max;
   const int split = e % (S + 1);
   const bool active = rb < n_rb;
+  // co-residency of a group's chunk CTAs: guaranteed when the whole grid fits
+  // the SMs, or when the active units do (inactive CTAs exit at once)
+  const bool spread = a.spread_merge || (a.sms > 0 && a.KVH * n_rb * (S + 1) <= a.sms);
   const bool step_unit = split == S;
   int k_begin, k_end;
   if (step_unit) {
@@ -664,7 +667,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
     __threadfence();
     const unsigned old = atomicAdd(a.cnt + grp, 1u);
     const unsigned target = (old / (unsigned)(S + 1) + 1) * (unsigned)(S + 1);
-    if (a.spread_merge) {
+    if (spread) {
       // every chunk CTA of the group is resident (grid <= SMs, 1 CTA / SM):
       // wait for the others, then merge this chunk's share of the rows
       unsigned v;
@@ -685,8 +688,8 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
   // ---- merge the S+1 chunk partials of this group in chunk order: rows
   // [r0, r1) of the group's valid rows, 8 threads per row x 16 dims
   const int nqb = min(128, nq - rb * 128);
-  const int rows_per = a.spread_merge ? (nqb + S) / (S + 1) : nqb;
-  const int r0 = a.spread_merge ? split * rows_per : 0;
+  const int rows_per = spread ? (nqb + S) / (S + 1) : nqb;
+  const int r0 = spread ? split * rows_per : 0;
   const int r1 = min(nqb, r0 + rows_per);
   for (int row = r0 + (tid >> 3); row < r1; row += 32) {
     const int qr = rb * 128 + row;

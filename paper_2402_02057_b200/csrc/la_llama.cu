@@ -425,11 +425,18 @@ int llama_create(la_engine* e) {
     LaAttnFusedArgs& af = p->af;
     af.H = p->H; af.KVH = p->KVH;
     af.nrb_max = (LA_MAX_ROWS * g + 127) / 128;
-    int units = std::max(2, std::min(9, la_sm_count() / (p->KVH * af.nrb_max)));
+    // key splits per (KV head, row block): sized for the row blocks of a
+    // typical step (<= 64 query tokens: ceil(64 g / 128) blocks) rather than
+    // the 128-row maximum, so GQA models keep several chunks per KV head; a
+    // launch whose active units exceed the SMs falls back to the last-arriver
+    // merge in-kernel (same chunk-order combine: identical results)
+    const int nrb_typ = std::max(1, std::min(af.nrb_max, (64 * g + 127) / 128));
+    int units = std::max(2, std::min(9, la_sm_count() / (p->KVH * nrb_typ)));
     if (getenv("LA_ATTN_SPLITS")) units = std::max(2, std::min(16, atoi(getenv("LA_ATTN_SPLITS")) + 1));
     af.S = units - 1;
     // co-residency (1 CTA per SM, grid <= SMs) makes the spread merge's wait safe
     af.spread_merge = (p->KVH * af.nrb_max * units <= la_sm_count()) && !getenv("LA_ATTN_LAST_MERGE");
+    af.sms = getenv("LA_ATTN_LAST_MERGE") ? 0 : la_sm_count();
     // optional (LA_ATTN_FUSE_QKV=1): the QKV epilogue inside the attention
     // kernel behind a grid barrier (needs every CTA co-resident).  Measured
     // slower: 32K threads reduce the partials ~3x slower than the separate
