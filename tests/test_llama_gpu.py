@@ -45,7 +45,7 @@ def _make(name, max_context=1024):
 # tcgen05 attention, attention + O projection in one persistent launch
 PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "mega": {"LA_MEGA": "1"},
          "tc_attn": {"LA_ATTN_TC": "1"}, "attn_o": {"LA_ATTN_O": "1"},
-         "cluster_attn": {"LA_ATTN_CLUSTER": "1"}}
+         "cluster_attn": {"LA_ATTN_CLUSTER": "1"}, "last_merge": {"LA_ATTN_LAST_MERGE": "1"}}
 
 
 @pytest.fixture(scope="module", params=[(c, p) for p in PATHS for c in CONFIGS],
@@ -53,7 +53,7 @@ PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "mega": {"LA_MEGA": 
 def pair(request):
     name, path = request.param
     saved = {k: os.environ.get(k) for k in ("LA_FUSED_EPI", "LA_MEGA", "LA_ATTN_TC", "LA_ATTN_O",
-                                            "LA_ATTN_CLUSTER")}
+                                            "LA_ATTN_CLUSTER", "LA_ATTN_LAST_MERGE")}
     for k in saved:
         os.environ.pop(k, None)
     os.environ.update(PATHS[path])
