@@ -175,3 +175,19 @@ def test_jacobi_fixed_point_equals_greedy(pair):
             agree = next((i for i, (a, b) in enumerate(zip(it, toks)) if a != b), len(toks))
             assert agree >= prev
             prev = agree
+
+
+def test_lookahead_equals_greedy_with_many_candidates(pair):
+    """A repetitive prompt fills the n-gram pool, so steps carry up to G
+    candidate branches (M up to (N-1)(W+G) = 120 rows, every attention warp
+    active, several row blocks for GQA); tokens must still equal greedy."""
+    name, m, orc = pair
+    V = orc.vocab_size
+    motif = [int(t) for t in np.random.default_rng(21).integers(0, V, 7)]
+    prompt = (motif * 12)[:80]
+    ar = la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), 40)
+    cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=40,
+                              seed_pool_from_prompt=True)
+    toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=3))
+    assert toks == ar, name
+    assert met.total_queries > met.steps * 60, "expected candidate branches in some steps"
