@@ -36,7 +36,7 @@ extern "C" {
 
 /* Thread-local description of the last error on this thread. */
 const char* la_last_error(void);
-/* ABI version (bumped on any signature change). */
+/* ABI version (bumped on any signature or struct-layout change; 2: la_decode_io.pool_capacity). */
 int32_t la_abi_version(void);
 
 /* ------------------------------------------------------------------ model */

@@ -15,6 +15,8 @@ from .types import DegenerateDistributionError, LayoutError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "liblookahead_b200.so"
 
+ABI_VERSION = 2   # la_abi_version() of the library this binding matches
+
 LA_OK = 0
 LA_ERR_INVALID_CONFIG = -1
 LA_ERR_LAYOUT = -2
@@ -114,6 +116,9 @@ def load(path: str | os.PathLike | None = None):
     lib = C.CDLL(str(p))
     lib.la_last_error.restype = C.c_char_p
     lib.la_abi_version.restype = C.c_int32
+    if lib.la_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{p}: ABI version {lib.la_abi_version()}, this binding needs {ABI_VERSION} "
+                           "(rebuild with `python -m paper_2402_02057_b200._build`)")
     lib.la_weight_count.argtypes = [C.POINTER(la_model_desc)]
     lib.la_weight_count.restype = C.c_int32
     lib.la_weight_name.argtypes = [C.POINTER(la_model_desc), C.c_int32]

@@ -23,7 +23,7 @@ void la_set_error(const char* fmt, ...) {
 }
 
 extern "C" const char* la_last_error(void) { return g_err; }
-extern "C" int32_t la_abi_version(void) { return 1; }
+extern "C" int32_t la_abi_version(void) { return 2; }   // 2: la_decode_io.pool_capacity
 
 #define CK(x) LA_CUDA_CHECK(x)
 #define RET_IF(x)              \

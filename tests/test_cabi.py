@@ -36,7 +36,7 @@ def test_python_binding_covers_header(lib):
 def test_weight_names_and_abi(lib):
     import ctypes as C
     from paper_2402_02057_b200 import _lib
-    assert lib.la_abi_version() == 1
+    assert lib.la_abi_version() == _lib.ABI_VERSION == 2
     d = _lib.la_model_desc(_lib.ARCH_LLAMA_BF16, 32000, 4096, 32, 32, 32, 128, 11008, 1e4, 1e-5, 2048)
     n = lib.la_weight_count(C.byref(d))
     assert n == 3 + 6 * 32
