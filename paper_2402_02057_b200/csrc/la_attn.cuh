@@ -44,6 +44,13 @@ struct LaAttnFusedArgs {
   int cluster;                   // launched as clusters of S+1 CTAs = one (KV head, row block):
                                  // chunk partials stay in smem and merge over DSMEM
   int dbg;                       // LA_ATTN_DBG experiments: 1 skip PV MMAs, 2 skip QK^T MMAs
+  int ksplit;                    // key tiles split by parity over the two warp groups (LA_ATTN_KSPLIT;
+                                 // 2: K/V tiles by TMA through kmap / vmap)
+  const CUtensorMap* kmap;       // whole K / V cache as [layers * slots][KVH * 128], SW128 boxes
+  const CUtensorMap* vmap;       //   of [64 keys][64 dims] (device memory)
+  int kv_row0;                   // this layer's first row in the maps (layer * slots)
+  int kv_pf;                     // bulk-prefetch the unit's prefix K/V into L2 before the
+                                 // dependency wait (LA_ATTN_KV_PF=1; measured slower, off)
   LaQkvEpi qkv;                  // its arguments
   unsigned* gbar;                // grid-barrier counter (monotonic; + grid per launch)
   unsigned long long* trace;     // optional [grid][8] globaltimer stamps (LA_ATTN_TRACE=1)

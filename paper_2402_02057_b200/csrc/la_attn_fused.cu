@@ -302,13 +302,16 @@ __device__ void attn_tc_unit(const LaAttnFusedArgs& a, const FwdPlan* P, uint8_t
 
 // Before the dependency wait: pull unit e's prefix K/V rows into L2.  Only a
 // cache hint -- if the plan or cache is not final yet the lines are merely
-// refetched after the wait -- so it is always safe.
+// refetched after the wait -- so it is always safe.  Off by default
+// (LA_ATTN_KV_PF=1): one serialised bulk prefetch per 256-B row costs more
+// than it hides once chunks are long (13B, 3.5K keys: attention 60 -> 51 us
+// per layer without it; 7B 512-1K keys: no change).
 __device__ __forceinline__ void attn_prefetch_kv(const LaAttnFusedArgs& a, int e) {
   const FwdPlan* P = a.plan;
   const int S = a.S;
   const int split = e % (S + 1);
   const int ctx = P->n_prefix;
-  if (split < S && P->n_rows > 0 && ctx > 0) {
+  if (a.kv_pf && split < S && P->n_rows > 0 && ctx > 0) {
     const int kvh = e / (a.nrb_max * (S + 1));
     const int CH = chunk_keys(ctx, S);
     const int k0 = min(ctx, split * CH), k1 = min(ctx, (split + 1) * CH);
@@ -359,6 +362,96 @@ __device__ void attn_merge_cluster(const LaAttnFusedArgs& a, uint8_t* smem, int 
       for (int i = 0; i < 16; ++i) acc[i] = acc[i] * s0 + vv[i] * s1;
       ll = ll * s0 + ml.y * s1;
       m = mn;
+    }
+    const float inv = 1.0f / ll;
+    const int r = qr / g, head = kvh * g + qr % g;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      *reinterpret_cast<uint4*>(a.out + la_act_off(r, head * 128 + hd + 8 * c)) =
+          make_uint4(pack_bf16(acc[8 * c] * inv, acc[8 * c + 1] * inv),
+                     pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
+                     pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
+                     pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
+  }
+}
+
+// Chunk arrival + merge of a (KV head, row block) group after every chunk
+// CTA wrote its partial to global memory: spread (every chunk CTA merges a
+// share of the rows once all arrived) or last-arriver (one CTA merges all).
+__device__ __forceinline__ void attn_arrive_merge(const LaAttnFusedArgs& a, int* sFlag, size_t grp, int S, int split,
+                                  int rb, int g, int nq, int kvh, bool spread) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  // arrival of this chunk.  Counters only grow: an active group gains exactly
+  // S+1 per launch, so the group's target is the next multiple of S+1.
+  if (tid == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(a.cnt + grp, 1u);
+    const unsigned target = (old / (unsigned)(S + 1) + 1) * (unsigned)(S + 1);
+    if (spread) {
+      // every chunk CTA of the group is resident (grid <= SMs, 1 CTA / SM):
+      // wait for the others, then merge this chunk's share of the rows
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.cnt + grp) : "memory");
+        if ((int)(v - target) < 0) __nanosleep(64);
+      } while ((int)(v - target) < 0);
+      *sFlag = 1;
+    } else {
+      *sFlag = old + 1 == target;   // the last chunk merges every row
+      if (*sFlag) __threadfence();
+    }
+  }
+  __syncthreads();
+  stamp(a, 5);
+  if (!*sFlag) return;
+
+  // ---- merge the S+1 chunk partials of this group in chunk order: rows
+  // [r0, r1) of the group's valid rows, 8 threads per row x 16 dims
+  const int nqb = min(128, nq - rb * 128);
+  const int rows_per = spread ? (nqb + S) / (S + 1) : nqb;
+  const int r0 = spread ? split * rows_per : 0;
+  const int r1 = min(nqb, r0 + rows_per);
+  for (int row = r0 + (tid >> 3); row < r1; row += 32) {
+    const int qr = rb * 128 + row;
+    const int hd = (tid & 7) * 16;
+    float m = -INFINITY, ll = 0.f;
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    // partials in batches of 4 with every load of a batch in flight together
+    // (a dependent L2 round trip per partial otherwise); same combine order
+    for (int sp0 = 0; sp0 <= S; sp0 += 4) {
+      float2 mlv[4];
+      float4 pv[4][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int sp = sp0 + j;
+        if (sp <= S) {
+          const size_t us = grp * (S + 1) + sp;
+          mlv[j] = __ldcg(a.part_ml + us * 128 + row);
+          const float4* po = reinterpret_cast<const float4*>(a.part_o + (us * 128 + row) * 128 + hd);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pv[j][q] = __ldcg(po + q);
+        } else {
+          mlv[j] = make_float2(-INFINITY, 0.f);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 ml = mlv[j];
+        if (ml.x == -INFINITY) continue;
+        const float mn = fmaxf(m, ml.x);
+        const float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
+        const float vv[16] = {pv[j][0].x, pv[j][0].y, pv[j][0].z, pv[j][0].w,
+                              pv[j][1].x, pv[j][1].y, pv[j][1].z, pv[j][1].w,
+                              pv[j][2].x, pv[j][2].y, pv[j][2].z, pv[j][2].w,
+                              pv[j][3].x, pv[j][3].y, pv[j][3].z, pv[j][3].w};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = acc[i] * s0 + vv[i] * s1;
+        ll = ll * s0 + ml.y * s1;
+        m = mn;
+      }
     }
     const float inv = 1.0f / ll;
     const int r = qr / g, head = kvh * g + qr % g;
@@ -660,88 +753,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
     stamp(a, 6);
     return;
   }
-  __syncthreads();
-  // arrival of this chunk.  Counters only grow: an active group gains exactly
-  // S+1 per launch, so the group's target is the next multiple of S+1.
-  if (tid == 0) {
-    __threadfence();
-    const unsigned old = atomicAdd(a.cnt + grp, 1u);
-    const unsigned target = (old / (unsigned)(S + 1) + 1) * (unsigned)(S + 1);
-    if (spread) {
-      // every chunk CTA of the group is resident (grid <= SMs, 1 CTA / SM):
-      // wait for the others, then merge this chunk's share of the rows
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.cnt + grp) : "memory");
-        if ((int)(v - target) < 0) __nanosleep(64);
-      } while ((int)(v - target) < 0);
-      *sFlag = 1;
-    } else {
-      *sFlag = old + 1 == target;   // the last chunk merges every row
-      if (*sFlag) __threadfence();
-    }
-  }
-  __syncthreads();
-  stamp(a, 5);
-  if (!*sFlag) return;
-
-  // ---- merge the S+1 chunk partials of this group in chunk order: rows
-  // [r0, r1) of the group's valid rows, 8 threads per row x 16 dims
-  const int nqb = min(128, nq - rb * 128);
-  const int rows_per = spread ? (nqb + S) / (S + 1) : nqb;
-  const int r0 = spread ? split * rows_per : 0;
-  const int r1 = min(nqb, r0 + rows_per);
-  for (int row = r0 + (tid >> 3); row < r1; row += 32) {
-    const int qr = rb * 128 + row;
-    const int hd = (tid & 7) * 16;
-    float m = -INFINITY, ll = 0.f;
-    float acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-    // partials in batches of 4 with every load of a batch in flight together
-    // (a dependent L2 round trip per partial otherwise); same combine order
-    for (int sp0 = 0; sp0 <= S; sp0 += 4) {
-      float2 mlv[4];
-      float4 pv[4][4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int sp = sp0 + j;
-        if (sp <= S) {
-          const size_t us = grp * (S + 1) + sp;
-          mlv[j] = __ldcg(a.part_ml + us * 128 + row);
-          const float4* po = reinterpret_cast<const float4*>(a.part_o + (us * 128 + row) * 128 + hd);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) pv[j][q] = __ldcg(po + q);
-        } else {
-          mlv[j] = make_float2(-INFINITY, 0.f);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 ml = mlv[j];
-        if (ml.x == -INFINITY) continue;
-        const float mn = fmaxf(m, ml.x);
-        const float s0 = exp2f(m - mn), s1 = exp2f(ml.x - mn);
-        const float vv[16] = {pv[j][0].x, pv[j][0].y, pv[j][0].z, pv[j][0].w,
-                              pv[j][1].x, pv[j][1].y, pv[j][1].z, pv[j][1].w,
-                              pv[j][2].x, pv[j][2].y, pv[j][2].z, pv[j][2].w,
-                              pv[j][3].x, pv[j][3].y, pv[j][3].z, pv[j][3].w};
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = acc[i] * s0 + vv[i] * s1;
-        ll = ll * s0 + ml.y * s1;
-        m = mn;
-      }
-    }
-    const float inv = 1.0f / ll;
-    const int r = qr / g, head = kvh * g + qr % g;
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-      *reinterpret_cast<uint4*>(a.out + la_act_off(r, head * 128 + hd + 8 * c)) =
-          make_uint4(pack_bf16(acc[8 * c] * inv, acc[8 * c + 1] * inv),
-                     pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
-                     pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
-                     pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
-  }
+  attn_arrive_merge(a, sFlag, grp, S, split, rb, g, nq, kvh, spread);
   stamp(a, 6);
 }
 
@@ -771,11 +783,393 @@ __global__ void __launch_bounds__(256, 1) la_attn_cluster_kernel(LaAttnFusedArgs
   attn_unit<kClStages, true>(a, smem, blockIdx.x);
 }
 
+// ---------------------------------------------------------------------------
+// Key-split variant (LA_ATTN_KSPLIT=1).  A chunk's key tiles are split by
+// parity: every row's chunk partial is (online softmax over the even tiles)
+// combined with (online softmax over the odd tiles), in that order.  Row
+// blocks of <= 64 rows run the two parities at once on the two warp groups
+// (warps 0-3 even, 4-7 odd; 2 tiles per ring slot) -- twice the warps per
+// SM sub-partition on the long serial tile chain; larger blocks stream the
+// tiles even-first then odd on all 8 warps and park the even state in smem
+// at the switch.  A row's arithmetic is the same in both modes (and for every
+// row count), so the mode is a per-CTA choice.
+namespace {
+constexpr int kKsPairSlots = 3;                                  // concurrent: 3 x 2 tiles
+constexpr int kKsSeqSlots = 4;                                   // sequential: 4 tiles + stash
+constexpr int kKsStashOff = kKsSeqSlots * kTileBytes;            // sequential stash (conc: offset 0)
+constexpr int kKsStash = 68;                                     // o[16][4], m0, m1, l0, l1 per thread
+constexpr int kKsMaskOff = kKsStashOff + 256 * kKsStash * 4;
+static_assert(kKsMaskOff >= 2 * kKsPairSlots * kTileBytes, "pair ring overlaps the mask");
+constexpr int kKsSmem = kKsMaskOff + LA_MAX_ROWS * 4 * 4 + 128;
+constexpr int kKsSmemTma = kKsSmem + 1024;                      // 1024-B aligned ring (SW128 boxes)
+}  // namespace
+
+// TMA: each 64-key tile lands as 4 SW128 boxes [K d0-63 | K d64-127 | V d0-63 |
+// V d64-127] of [64 keys][128 B]; cp.async: [K | V] rows of 256 B (swz)
+template <bool TMA>
+__device__ __forceinline__ uint32_t ks_swz(int row, int ch) {
+  if constexpr (TMA) return (uint32_t)((ch >> 3) * 8192 + row * 128 + (((ch & 7) ^ (row & 7)) << 4));
+  else return swz(row, ch);
+}
+
+// one 64-key tile of QK^T -> masked online softmax -> PV for a warp's 16 rows
+template <bool TMA>
+__device__ __forceinline__ void ks_tile(const uint8_t* sK, const uint32_t (&qf)[8][4], float (&o)[16][4],
+                                        float& m0, float& m1, float& l0, float& l1, int lane, int nvalid,
+                                        const uint32_t* w0, const uint32_t* w1, float sl2) {
+  const uint8_t* sV = sK + kKeyTile * 256;   // both layouts: V at +16 KB
+  float s[8][4];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+      const int key = np * 16 + (lane & 7) + (lane >> 4) * 8;
+      const int ch = kk * 2 + ((lane >> 3) & 1);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(smem_u32(sK) + ks_swz<TMA>(key, ch), b0, b1, b2, b3);
+      mma16816(s[2 * np], qf[kk], b0, b1);
+      mma16816(s[2 * np + 1], qf[kk], b2, b3);
+    }
+  }
+  unsigned long long vm0 = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull), vm1 = vm0;
+  if (w0) {
+    vm0 &= ((unsigned long long)w0[1] << 32) | w0[0];
+    vm1 &= ((unsigned long long)w1[1] << 32) | w1[0];
+  }
+  vm0 >>= (lane & 3) * 2;
+  vm1 >>= (lane & 3) * 2;
+  float mx0 = m0, mx1 = m1;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      const unsigned long long vm = (e2 >> 1) ? vm1 : vm0;
+      const bool vis = (vm >> (n * 8 + (e2 & 1))) & 1ull;
+      s[n][e2] = vis ? s[n][e2] * sl2 : -INFINITY;
+    }
+    mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
+    mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
+  }
+#pragma unroll
+  for (int off = 1; off <= 2; off <<= 1) {
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+  }
+  const float b0 = mx0 == -INFINITY ? 0.f : mx0, b1 = mx1 == -INFINITY ? 0.f : mx1;
+  const float al0 = exp2f(m0 - b0), al1 = exp2f(m1 - b1);
+  m0 = mx0;
+  m1 = mx1;
+  float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    s[n][0] = exp2f(s[n][0] - b0);
+    s[n][1] = exp2f(s[n][1] - b0);
+    s[n][2] = exp2f(s[n][2] - b1);
+    s[n][3] = exp2f(s[n][3] - b1);
+    rs0 += s[n][0] + s[n][1];
+    rs1 += s[n][2] + s[n][3];
+  }
+  l0 = l0 * al0 + rs0;
+  l1 = l1 * al1 + rs1;
+#pragma unroll
+  for (int dd = 0; dd < 16; ++dd) {
+    o[dd][0] *= al0; o[dd][1] *= al0; o[dd][2] *= al1; o[dd][3] *= al1;
+  }
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t pa[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]), pack_bf16(s[2 * kk][2], s[2 * kk][3]),
+                      pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]), pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+    for (int dp = 0; dp < 8; ++dp) {
+      const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int ch = dp * 2 + (lane >> 4);
+      uint32_t v0, v1, v2, v3;
+      ldsm_x4_t(smem_u32(sV) + ks_swz<TMA>(key, ch), v0, v1, v2, v3);
+      mma16816(o[2 * dp], pa, v0, v1);
+      mma16816(o[2 * dp + 1], pa, v2, v3);
+    }
+  }
+}
+
+// park / restore a thread's softmax state ([element][thread] words)
+__device__ __forceinline__ void ks_stash(float* st, int stride, const float (&o)[16][4], float m0, float m1,
+                                         float l0, float l1) {
+#pragma unroll
+  for (int dd = 0; dd < 16; ++dd)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) st[(dd * 4 + c) * stride] = o[dd][c];
+  st[64 * stride] = m0;
+  st[65 * stride] = m1;
+  st[66 * stride] = l0;
+  st[67 * stride] = l1;
+}
+
+// state = even-tile state combined with odd-tile state -- always in that
+// order and with explicit roundings, whichever of the two sits in registers
+__device__ __forceinline__ void ks_combine(float (&o)[16][4], float& m0, float& m1, float& l0, float& l1,
+                                           const float* st, int stride, bool regs_odd) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float ms = st[(64 + h) * stride], ls = st[(66 + h) * stride];
+    const float mr = h ? m1 : m0, lr = h ? l1 : l0;
+    const float me = regs_odd ? ms : mr, mo = regs_odd ? mr : ms;
+    const float le = regs_odd ? ls : lr, lo = regs_odd ? lr : ls;
+    const float mn = fmaxf(me, mo);
+    const float b = mn == -INFINITY ? 0.f : mn;
+    const float se = exp2f(me - b), so = exp2f(mo - b);
+    const float ln = __fmaf_rn(le, se, __fmul_rn(lo, so));
+#pragma unroll
+    for (int dd = 0; dd < 16; ++dd)
+#pragma unroll
+      for (int c = 2 * h; c < 2 * h + 2; ++c) {
+        const float xs = st[(dd * 4 + c) * stride], xr = o[dd][c];
+        const float xe = regs_odd ? xs : xr, xo = regs_odd ? xr : xs;
+        o[dd][c] = __fmaf_rn(xe, se, __fmul_rn(xo, so));
+      }
+    if (h) { m1 = mn; l1 = ln; } else { m0 = mn; l0 = ln; }
+  }
+}
+
+template <bool TMA>
+__device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e) {
+  stamp(a, 1);
+  const FwdPlan* P = a.plan;
+  const int n_rows = P->n_rows, ctx = P->n_prefix;
+  if (n_rows == 0) return;
+  const int g = a.H / a.KVH;
+  const int nq = n_rows * g;
+  const int n_rb = (nq + 127) >> 7;
+  const int S = a.S;
+  const int kvh = e / (a.nrb_max * (S + 1));
+  const int rb = (e / (S + 1)) % a.nrb_max;
+  const int split = e % (S + 1);
+  if (rb >= n_rb) return;
+  const bool spread = a.spread_merge || (a.sms > 0 && a.KVH * n_rb * (S + 1) <= a.sms);
+  const bool step_unit = split == S;
+  int k_begin, k_end;
+  if (step_unit) {
+    k_begin = ctx;
+    k_end = ctx + P->n_global;
+  } else {
+    const int CH = chunk_keys(ctx, S);
+    k_begin = min(ctx, split * CH);
+    k_end = min(ctx, (split + 1) * CH);
+  }
+  const int nqb = min(128, nq - rb * 128);
+  const bool conc = nqb <= 64;
+
+  uint8_t* smem = TMA ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
+                      : smem_raw;
+  uint8_t* sKV = smem;
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + kKsMaskOff);   // [128][4]
+  int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
+  uint64_t* sBar = reinterpret_cast<uint64_t*>(sFlag + 4);            // TMA: one per tile slot
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t kv_ld = (size_t)a.KVH * 128;
+  const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+  const int ne = (n_tiles + 1) >> 1;                 // even tiles
+  const int par = conc ? warp >> 2 : 0;              // concurrent: this warp group's parity
+  const int wrow = conc ? warp & 3 : warp;
+  const int n_items = conc ? ne : n_tiles;
+
+  const uint64_t pol = TMA ? ptx::policy_evict_first() : 0ull;
+  auto load_tile = [&](int t, uint8_t* kb) {
+    const int t0 = k_begin + t * kKeyTile;
+    if constexpr (TMA) {
+      // keys past k_end load real (finite) cache rows; the mask drops them
+      if (tid == 0) {
+        uint64_t* bar = sBar + (kb - sKV) / kTileBytes;
+        ptx::mbar_expect_tx(bar, kTileBytes);
+        const int row = a.kv_row0 + t0;
+        ptx::tma_load_2d(kb, a.kmap, bar, kvh * 128, row, pol);
+        ptx::tma_load_2d(kb + 8192, a.kmap, bar, kvh * 128 + 64, row, pol);
+        ptx::tma_load_2d(kb + 16384, a.vmap, bar, kvh * 128, row, pol);
+        ptx::tma_load_2d(kb + 24576, a.vmap, bar, kvh * 128 + 64, row, pol);
+      }
+      return;
+    }
+    for (int i = tid; i < kKeyTile * 16; i += 256) {
+      const int row = i >> 4, ch = i & 15, key = t0 + row;
+      const bool ok = key < k_end;
+      const size_t off = ((size_t)(ok ? key : k_begin) * kv_ld) + kvh * 128 + ch * 8;
+      cp_async16(smem_u32(kb) + swz(row, ch), a.kc + off, ok);
+      cp_async16(smem_u32(kb + kKeyTile * 256) + swz(row, ch), a.vc + off, ok);
+    }
+  };
+  // item: concurrent = tiles (2i, 2i+1) in pair slot i % 3; sequential = the
+  // i-th tile of the order 0, 2, 4, ..., 1, 3, ... in slot i % 4
+  auto load_item = [&](int it) {
+    if (conc) {
+      uint8_t* kb = sKV + (it % kKsPairSlots) * 2 * kTileBytes;
+      if (2 * it < n_tiles) load_tile(2 * it, kb);
+      if (2 * it + 1 < n_tiles) load_tile(2 * it + 1, kb + kTileBytes);
+    } else {
+      load_tile(it < ne ? 2 * it : 2 * (it - ne) + 1, sKV + (it % kKsSeqSlots) * kTileBytes);
+    }
+  };
+  const int depth = conc ? kKsPairSlots - 1 : kKsSeqSlots - 1;
+  auto issue_first = [&]() {
+#pragma unroll 1
+    for (int it = 0; it < depth; ++it) {
+      if (it < n_items) load_item(it);
+      cp_commit();
+    }
+  };
+  const int qrow0 = wrow * 16 + (lane >> 2);
+  uint32_t qf[8][4];
+  {
+    const int qa = rb * 128 + qrow0, qb = qa + 8;
+    const __nv_bfloat16* pa = qa < nq ? a.q + ((size_t)(qa / g) * a.H + kvh * g + qa % g) * 128 : nullptr;
+    const __nv_bfloat16* pb = qb < nq ? a.q + ((size_t)(qb / g) * a.H + kvh * g + qb % g) * 128 : nullptr;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int col = kk * 16 + (lane & 3) * 2;
+      qf[kk][0] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col)) : 0u;
+      qf[kk][1] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col)) : 0u;
+      qf[kk][2] = pa ? __ldcg(reinterpret_cast<const unsigned*>(pa + col + 8)) : 0u;
+      qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
+    }
+  }
+  if (TMA && tid == 0) {
+    for (int i = 0; i < 2 * kKsPairSlots; ++i) ptx::mbar_init(sBar + i, 1);
+    ptx::fence_barrier_init();
+  }
+  if (!step_unit) issue_first();
+  const size_t grp = (size_t)kvh * a.nrb_max + rb;
+  if (!step_unit && TMA) __syncthreads();   // barrier inits visible before any wait
+  if (step_unit) {
+    if (tid < LA_MAX_ROWS) {
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+      const int qr = rb * 128 + tid;
+      if (qr < nq) {
+        const int r = qr / g;
+        const int n = P->chain_n[r];
+        const int own = P->slot[r] - ctx;
+        w[own >> 5] |= 1u << (own & 31);
+        for (int jj = 0; jj < n; ++jj) {
+          const int key = P->chain[r][jj] - ctx;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w[q] |= (key >> 5) == q ? 1u << (key & 31) : 0u;
+        }
+      }
+      *reinterpret_cast<uint4*>(sMask + tid * 4) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __syncthreads();
+    issue_first();
+  }
+
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float sl2 = a.scale * kLog2e;
+  const bool warp_active = rb * 128 + wrow * 16 < nq;
+  float* seq_st = reinterpret_cast<float*>(smem + kKsStashOff) + tid;
+  stamp(a, 2);
+  for (int it = 0; it < n_items; ++it) {
+    if (it + depth < n_items) load_item(it + depth);
+    cp_commit();
+    if constexpr (!TMA) {
+      if (conc) cp_wait<kKsPairSlots - 1>(); else cp_wait<kKsSeqSlots - 1>();
+      __syncthreads();
+    }
+    if (it == 0) stamp(a, 3);
+    int t, slot;
+    uint32_t phase;
+    if (conc) {
+      t = 2 * it + par;
+      slot = (it % kKsPairSlots) * 2 + par;
+      phase = (it / kKsPairSlots) & 1;
+    } else {
+      t = it < ne ? 2 * it : 2 * (it - ne) + 1;
+      slot = it % kKsSeqSlots;
+      phase = (it / kKsSeqSlots) & 1;
+    }
+    const uint8_t* sK = sKV + slot * kTileBytes;
+    if (TMA && t < n_tiles) ptx::mbar_wait(sBar + slot, phase);
+    if (!conc) {
+      if (it == ne) {   // even tiles done: park their state, start the odd ones
+        ks_stash(seq_st, 256, o, m0, m1, l0, l1);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+        m0 = m1 = -INFINITY;
+        l0 = l1 = 0.f;
+      }
+    }
+    if (warp_active && t < n_tiles) {
+      const int nvalid = min(kKeyTile, k_end - (k_begin + t * kKeyTile));
+      const uint32_t* w0 = step_unit ? sMask + qrow0 * 4 + 2 * t : nullptr;
+      const uint32_t* w1 = step_unit ? sMask + (qrow0 + 8) * 4 + 2 * t : nullptr;
+      ks_tile<TMA>(sK, qf, o, m0, m1, l0, l1, lane, nvalid, w0, w1, sl2);
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  stamp(a, 4);
+  if (conc) {
+    // odd group parks its state in the drained ring; the even group combines
+    float* st = reinterpret_cast<float*>(smem) + (tid & 127);
+    if (par) ks_stash(st, 128, o, m0, m1, l0, l1);
+    __syncthreads();
+    if (!par) ks_combine(o, m0, m1, l0, l1, st, 128, false);
+  } else {
+    if (n_items <= ne) {   // no odd tile: the registers hold the even state
+      ks_stash(seq_st, 256, o, m0, m1, l0, l1);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+    }
+    ks_combine(o, m0, m1, l0, l1, seq_st, 256, true);
+  }
+#pragma unroll
+  for (int off = 1; off <= 2; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  if (!par) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int row = qrow0 + half * 8;
+      if (rb * 128 + row >= nq) continue;
+      float* dst = a.part_o + ((grp * (S + 1) + split) * 128 + row) * 128;
+#pragma unroll
+      for (int dd = 0; dd < 16; ++dd) {
+        const int col = dd * 8 + (lane & 3) * 2;
+        __stcg(reinterpret_cast<float2*>(dst + col), make_float2(o[dd][half * 2], o[dd][half * 2 + 1]));
+      }
+      if ((lane & 3) == 0)
+        __stcg(a.part_ml + (grp * (S + 1) + split) * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
+    }
+  }
+  attn_arrive_merge(a, sFlag, grp, S, split, rb, g, nq, kvh, spread);
+  stamp(a, 6);
+}
+
+template <bool TMA>
+__global__ void __launch_bounds__(256, 1) la_attn_ks_kernel(LaAttnFusedArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  stamp(a, 0);
+  la_pdl_trigger();
+  la_l2_prefetch_gemm(a.pf);
+  attn_prefetch_kv(a, blockIdx.x);
+  if (TMA && threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(a.kmap);
+    ptx::tma_prefetch_desc(a.vmap);
+  }
+  la_pdl_wait();
+  attn_unit_ks<TMA>(a, smem, blockIdx.x);
+}
+
 cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = la_attn_fused_smem(a.tc != 0, a.cluster != 0);
+  const bool ks = a.ksplit && !a.tc && !a.cluster && !a.fuse_qkv;
+  if (ks) cfg.dynamicSmemBytes = a.ksplit == 2 ? kKsSmemTma : kKsSmem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   int n = 0;
@@ -802,6 +1196,19 @@ cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_
       attr = true;
     }
     return cudaLaunchKernelEx(&cfg, la_attn_cluster_kernel, a);
+  }
+  if (ks) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(la_attn_ks_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kKsSmem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(la_attn_ks_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKsSmemTma);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    if (a.ksplit == 2) return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<true>, a);
+    return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<false>, a);
   }
   return cudaLaunchKernelEx(&cfg, la_attn_fused_kernel, a);
 }

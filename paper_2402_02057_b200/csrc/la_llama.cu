@@ -454,6 +454,28 @@ int llama_create(la_engine* e) {
     af.cluster = af.spread_merge && !af.tc && !af.fuse_qkv && units <= 8 &&
                  getenv("LA_ATTN_CLUSTER") && atoi(getenv("LA_ATTN_CLUSTER")) == 1;
     af.dbg = getenv("LA_ATTN_DBG") ? atoi(getenv("LA_ATTN_DBG")) : 0;
+    // key tiles split by parity over the two warp groups (la_attn_ks_kernel)
+    // (2: its K/V tiles by TMA from tensor maps over the whole cache).  Default:
+    // the TMA variant when a full cache gives chunks of >= 8 key tiles (13B,
+    // 3.5K keys: attention 51 -> 45 us per layer, step -2%, greedy -5%); the
+    // plain kernel for short caches (7B, 0.5-1K keys: key-split +1-2 us per
+    // layer).  Fixed per engine, so every decode on it computes alike.
+    const int cache_tiles = ((e->slots + af.S - 1) / af.S + 63) / 64;
+    const char* ks_env = getenv("LA_ATTN_KSPLIT");
+    const int ks = ks_env ? std::max(0, std::min(2, atoi(ks_env))) : (cache_tiles >= 8 ? 2 : 0);
+    af.ksplit = (!af.tc && !af.cluster && !af.fuse_qkv) ? ks : 0;
+    af.kv_pf = getenv("LA_ATTN_KV_PF") && atoi(getenv("LA_ATTN_KV_PF")) == 1;
+    if (af.ksplit == 2) {
+      CUtensorMap maps[2];
+      const int rows = p->L * e->slots;
+      RET_IF(la_make_tmap(&maps[0], e->kc, rows, p->KVH * 128, 64));
+      RET_IF(la_make_tmap(&maps[1], e->vc, rows, p->KVH * 128, 64));
+      CUtensorMap* dm = nullptr;
+      RET_IF(lalloc(e, reinterpret_cast<uint8_t**>(&dm), sizeof(maps)));
+      CK(cudaMemcpy(dm, maps, sizeof(maps), cudaMemcpyHostToDevice));
+      af.kmap = dm;
+      af.vmap = dm + 1;
+    }
     af.scale = 1.0f / sqrtf(128.0f);
     af.q = p->q;
     af.out = p->attn;
@@ -632,6 +654,7 @@ static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
   const size_t lstride = (size_t)e->slots * p->KVH * 128;
   a.kc = reinterpret_cast<__nv_bfloat16*>(e->kc) + l * lstride;
   a.vc = reinterpret_cast<__nv_bfloat16*>(e->vc) + l * lstride;
+  a.kv_row0 = l * e->slots;
   if (a.fuse_qkv) {
     __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc) + l * lstride;
     __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc) + l * lstride;
@@ -834,6 +857,7 @@ static int prefill_chunks(la_engine* e, const int* d_tokens, int start, int n_ch
       LaAttnFusedArgs a = p->af;
       a.plan = c[i].plan; a.q = c[i].q; a.out = c[i].attn;
       a.kc = kc + l * lstride; a.vc = vc + l * lstride;
+      a.kv_row0 = l * e->slots;
       a.pf = LaPrefetch{};
       CK(la_attn_fused_launch(a, p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
     }

@@ -45,7 +45,13 @@ def _make(name, max_context=1024):
 # tcgen05 attention, attention + O projection in one persistent launch
 PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "mega": {"LA_MEGA": "1"},
          "tc_attn": {"LA_ATTN_TC": "1"}, "attn_o": {"LA_ATTN_O": "1"},
-         "cluster_attn": {"LA_ATTN_CLUSTER": "1"}, "last_merge": {"LA_ATTN_LAST_MERGE": "1"}}
+         "cluster_attn": {"LA_ATTN_CLUSTER": "1"}, "last_merge": {"LA_ATTN_LAST_MERGE": "1"},
+         # key tiles split by parity over the warp groups; the second one with
+         # one prefix chunk so chunks hold many (odd and even) tile counts
+         "ksplit": {"LA_ATTN_KSPLIT": "1"}, "ksplit_1chunk": {"LA_ATTN_KSPLIT": "1", "LA_ATTN_SPLITS": "1"},
+         # the same with K/V tiles by TMA (tensor maps over the whole cache)
+         "ksplit_tma": {"LA_ATTN_KSPLIT": "2"},
+         "ksplit_tma_1chunk": {"LA_ATTN_KSPLIT": "2", "LA_ATTN_SPLITS": "1"}}
 
 
 @pytest.fixture(scope="module", params=[(c, p) for p in PATHS for c in CONFIGS],
@@ -53,7 +59,8 @@ PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "mega": {"LA_MEGA": 
 def pair(request):
     name, path = request.param
     saved = {k: os.environ.get(k) for k in ("LA_FUSED_EPI", "LA_MEGA", "LA_ATTN_TC", "LA_ATTN_O",
-                                            "LA_ATTN_CLUSTER", "LA_ATTN_LAST_MERGE")}
+                                            "LA_ATTN_CLUSTER", "LA_ATTN_LAST_MERGE", "LA_ATTN_KSPLIT",
+                                            "LA_ATTN_SPLITS")}
     for k in saved:
         os.environ.pop(k, None)
     os.environ.update(PATHS[path])
@@ -191,3 +198,18 @@ def test_lookahead_equals_greedy_with_many_candidates(pair):
     toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=3))
     assert toks == ar, name
     assert met.total_queries > met.steps * 60, "expected candidate branches in some steps"
+
+
+def test_lookahead_equals_greedy_long_context(pair):
+    """~700 cached keys: prefix chunks of several key tiles (both parities of
+    the key-split kernel, its concurrent and sequential modes); lookahead
+    tokens must equal greedy."""
+    name, m, orc = pair
+    V = orc.vocab_size
+    motif = [int(t) for t in np.random.default_rng(23).integers(0, V, 11)]
+    prompt = (motif * 70)[:700]
+    ar = la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), 32)
+    cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=32,
+                              seed_pool_from_prompt=True)
+    toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=4))
+    assert toks == ar, name
