@@ -49,6 +49,8 @@ struct LaAttnFusedArgs {
   const CUtensorMap* kmap;       // whole K / V cache as [layers * slots][KVH * 128], SW128 boxes
   const CUtensorMap* vmap;       //   of [64 keys][64 dims] (device memory)
   int kv_row0;                   // this layer's first row in the maps (layer * slots)
+  const int* spec_ctx;           // graph-loop decode: the decode state's ctx, read before the
+                                 // dependency wait to start the first prefix tiles early
   int kv_pf;                     // bulk-prefetch the unit's prefix K/V into L2 before the
                                  // dependency wait (LA_ATTN_KV_PF=1; measured slower, off)
   LaQkvEpi qkv;                  // its arguments

@@ -465,13 +465,57 @@ __device__ __forceinline__ void attn_arrive_merge(const LaAttnFusedArgs& a, int*
   }
 }
 
+// K/V tile t of [k_begin, k_end) into ring slot t % STAGES (cp.async, rows past
+// k_end zero-filled)
+template <int STAGES>
+__device__ __forceinline__ void attn_load_kv(const LaAttnFusedArgs& a, uint8_t* sKV, int t, int k_begin,
+                                             int k_end, int kvh) {
+  uint8_t* kb = sKV + (t % STAGES) * kTileBytes;
+  const size_t kv_ld = (size_t)a.KVH * 128;
+  const int t0 = k_begin + t * kKeyTile;
+  for (int i = threadIdx.x; i < kKeyTile * 16; i += 256) {
+    const int row = i >> 4, ch = i & 15, key = t0 + row;
+    const bool ok = key < k_end;
+    const size_t off = ((size_t)(ok ? key : k_begin) * kv_ld) + kvh * 128 + ch * 8;
+    cp_async16(smem_u32(kb) + swz(row, ch), a.kc + off, ok);
+    cp_async16(smem_u32(kb + kKeyTile * 256) + swz(row, ch), a.vc + off, ok);
+  }
+}
+
+// Before the dependency wait (graph-loop decode only, a.spec_ctx set): start the
+// first STAGES-1 prefix tiles of unit e for the decode state's ctx.  ctx and the
+// prefix K/V were final when this loop iteration began (written by K10 / the KV
+// commit of the previous step); the unit checks the guess against its plan after
+// the wait and reloads on a mismatch.  Returns the guessed ctx, or -1 (no issue).
+template <int STAGES>
+__device__ __forceinline__ int attn_spec_issue(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
+  const int S = a.S;
+  const int split = e % (S + 1);
+  if (split == S || (e / (S + 1)) % a.nrb_max != 0) return -1;
+  const int ctx = *reinterpret_cast<const volatile int*>(a.spec_ctx);
+  const int kvh = e / (a.nrb_max * (S + 1));
+  const int CH = chunk_keys(ctx, S);
+  const int k_begin = min(ctx, split * CH), k_end = min(ctx, (split + 1) * CH);
+  const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+#pragma unroll 1
+  for (int t = 0; t < STAGES - 1; ++t) {
+    if (t < n_tiles) attn_load_kv<STAGES>(a, smem, t, k_begin, k_end, kvh);
+    cp_commit();
+  }
+  return ctx;
+}
+
 // One attention unit e = (KV head, row block, key chunk) after the dependency
 // wait, on a K/V ring of STAGES tiles at smem (plus the mask at mask_off).
+// spec >= 0: attn_spec_issue already started the first tiles for ctx == spec.
 template <int STAGES, bool CLUSTER = false>
-__device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
+__device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e, int spec = -1) {
   stamp(a, 1);
   const FwdPlan* P = a.plan;
   const int n_rows = P->n_rows, ctx = P->n_prefix;
+  // a wrong guess (or nothing to do): drain the speculative copies first
+  const bool spec_hit = spec >= 0 && spec == ctx && n_rows > 0;
+  if (spec >= 0 && !spec_hit) cp_wait<0>();
   if (n_rows == 0) return;
   const int g = a.H / a.KVH;
   const int nq = n_rows * g;
@@ -546,7 +590,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e) {
     }
   };
   if (active && !tc && !a.fuse_qkv) load_q();
-  if (active && !step_unit && !tc) issue_first();
+  if (active && !step_unit && !tc && !spec_hit) issue_first();
   if (a.fuse_qkv) {
     // QKV split-K epilogue (la_qkv_fix) spread over every CTA of the grid,
     // then a grid barrier: all CTAs are resident (grid <= SMs, 1 CTA / SM)
@@ -764,8 +808,9 @@ __global__ void __launch_bounds__(256, 1) la_attn_fused_kernel(LaAttnFusedArgs a
   la_pdl_trigger();
   la_l2_prefetch_gemm(a.pf);
   attn_prefetch_kv(a, blockIdx.x);
+  const int spec = a.spec_ctx && !a.tc && !a.fuse_qkv ? attn_spec_issue<kStages>(a, smem, blockIdx.x) : -1;
   la_pdl_wait();
-  attn_unit<kStages>(a, smem, blockIdx.x);
+  attn_unit<kStages>(a, smem, blockIdx.x, spec);
   if (a.dbg & 8) {   // timing experiment: 5 us of extra attention time per CTA
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));

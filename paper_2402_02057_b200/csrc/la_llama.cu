@@ -68,6 +68,8 @@ struct LlamaPath {
   int head_tiles = 0;
   int kernels_per_step = 0;
   int loop_key = 0;                       // sampler shape the loop graph was built for
+  bool spec_kv = false;                   // recording the WHILE-graph body: attention may read
+                                          // the decode ctx + prefix K/V before its PDL wait
   bool pdl = true;                        // programmatic dependent launch (LA_PDL=0: off)
   bool fused = false;                     // GEMM-fused epilogues (LA_FUSED_EPI=1)
   int attn_rows = 64;                     // query rows per attention CTA (LA_ATTN_ROWS)
@@ -465,6 +467,7 @@ int llama_create(la_engine* e) {
     const int ks = ks_env ? std::max(0, std::min(2, atoi(ks_env))) : (cache_tiles >= 8 ? 2 : 0);
     af.ksplit = (!af.tc && !af.cluster && !af.fuse_qkv) ? ks : 0;
     af.kv_pf = getenv("LA_ATTN_KV_PF") && atoi(getenv("LA_ATTN_KV_PF")) == 1;
+    af.spec_ctx = nullptr;
     if (af.ksplit == 2) {
       CUtensorMap maps[2];
       const int rows = p->L * e->slots;
@@ -655,6 +658,9 @@ static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
   a.kc = reinterpret_cast<__nv_bfloat16*>(e->kc) + l * lstride;
   a.vc = reinterpret_cast<__nv_bfloat16*>(e->vc) + l * lstride;
   a.kv_row0 = l * e->slots;
+  // each WHILE-loop iteration starts after the previous one completed, so the
+  // decode state's ctx and the committed prefix K/V are final before any wait
+  a.spec_ctx = p->spec_kv ? &e->d_dec->ctx : nullptr;
   if (a.fuse_qkv) {
     __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc) + l * lstride;
     __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc) + l * lstride;
@@ -858,6 +864,7 @@ static int prefill_chunks(la_engine* e, const int* d_tokens, int start, int n_ch
       a.plan = c[i].plan; a.q = c[i].q; a.out = c[i].attn;
       a.kc = kc + l * lstride; a.vc = vc + l * lstride;
       a.kv_row0 = l * e->slots;
+      a.spec_ctx = nullptr;
       a.pf = LaPrefetch{};
       CK(la_attn_fused_launch(a, p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
     }
@@ -981,7 +988,9 @@ static int build_loop_graph(la_engine* e) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(p->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   int nk = 0;
+  p->spec_kv = !(getenv("LA_ATTN_SPEC") && atoi(getenv("LA_ATTN_SPEC")) == 0);
   int rc = record_step(e, p->cap, true, &nk);
+  p->spec_kv = false;
   cudaError_t lce = la_launch(la_set_cond_kernel, dim3(1), dim3(1), 0, p->cap, p->pdl, handle, (const DevDecode*)e->d_dec);
   if (lce != cudaSuccess && rc == LA_OK) { la_set_error("set_cond launch: %s", cudaGetErrorString(lce)); rc = LA_ERR_CUDA; }
   cudaGraph_t captured;
