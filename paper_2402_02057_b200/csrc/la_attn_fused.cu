@@ -833,8 +833,8 @@ __global__ void __launch_bounds__(256, 1) la_attn_cluster_kernel(LaAttnFusedArgs
 // parity: every row's chunk partial is (online softmax over the even tiles)
 // combined with (online softmax over the odd tiles), in that order.  Row
 // blocks of <= 64 rows run the two parities at once on the two warp groups
-// (warps 0-3 even, 4-7 odd; 2 tiles per ring slot) -- twice the warps per
-// SM sub-partition on the long serial tile chain; larger blocks stream the
+// (one warp of each pair even tiles, the other odd; 2 tiles per ring slot) --
+// the idle half of the CTA joins the long serial tile chain; larger blocks stream the
 // tiles even-first then odd on all 8 warps and park the even state in smem
 // at the switch.  A row's arithmetic is the same in both modes (and for every
 // row count), so the mode is a per-CTA choice.
@@ -1015,8 +1015,12 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
   const size_t kv_ld = (size_t)a.KVH * 128;
   const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
   const int ne = (n_tiles + 1) >> 1;                 // even tiles
-  const int par = conc ? warp >> 2 : 0;              // concurrent: this warp group's parity
-  const int wrow = conc ? warp & 3 : warp;
+  // concurrent: blocks of <= 32 rows pair warps (2k, 2k+1) on a 16-row slice so
+  // the active warps spread over all four SM sub-partitions (warp % 4; 13B
+  // greedy step -4.5 %); 33-64 rows use warps w and w + 4 (measured faster there)
+  const bool narrow = nqb <= 32;
+  const int par = conc ? (narrow ? warp & 1 : warp >> 2) : 0;
+  const int wrow = conc ? (narrow ? warp >> 1 : warp & 3) : warp;
   const int n_items = conc ? ne : n_tiles;
 
   const uint64_t pol = TMA ? ptx::policy_evict_first() : 0ull;
@@ -1155,7 +1159,7 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
   stamp(a, 4);
   if (conc) {
     // odd group parks its state in the drained ring; the even group combines
-    float* st = reinterpret_cast<float*>(smem) + (tid & 127);
+    float* st = reinterpret_cast<float*>(smem) + wrow * 32 + lane;
     if (par) ks_stash(st, 128, o, m0, m1, l0, l1);
     __syncthreads();
     if (!par) ks_combine(o, m0, m1, l0, l1, st, 128, false);
