@@ -1237,26 +1237,20 @@ cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_
   cfg.attrs = at;
   cfg.numAttrs = n;
   if (a.cluster) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(la_attn_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)la_attn_fused_smem(false, true));
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    static std::atomic<unsigned> attr{0};
+    cudaError_t e = la_smem_attr_once(attr, la_attn_cluster_kernel, (int)la_attn_fused_smem(false, true));
+    if (e != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, la_attn_cluster_kernel, a);
   }
   if (ks) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(la_attn_ks_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kKsSmem);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(la_attn_ks_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kKsSmemTma);
+    static std::atomic<unsigned> attr_cp{0}, attr_tma{0};
+    if (a.ksplit == 2) {
+      cudaError_t e = la_smem_attr_once(attr_tma, la_attn_ks_kernel<true>, kKsSmemTma);
       if (e != cudaSuccess) return e;
-      attr = true;
+      return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<true>, a);
     }
-    if (a.ksplit == 2) return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<true>, a);
+    cudaError_t e = la_smem_attr_once(attr_cp, la_attn_ks_kernel<false>, kKsSmem);
+    if (e != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<false>, a);
   }
   return cudaLaunchKernelEx(&cfg, la_attn_fused_kernel, a);
@@ -1468,13 +1462,10 @@ __global__ void __launch_bounds__(256, 1) la_attn_o_kernel(LaAttnOArgs x) {
 }
 
 cudaError_t la_attn_o_launch(const LaAttnOArgs& x, int grid, cudaStream_t st, bool pdl) {
-  static bool attr = false;
-  const size_t smem = la_attn_o_smem(x.nst);
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(la_attn_o_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  const size_t smem = la_attn_o_smem(x.nst);   // nst is fixed per process (LA_O_STAGES)
+  cudaError_t e = la_smem_attr_once(attr, la_attn_o_kernel, (int)smem);
+  if (e != cudaSuccess) return e;
   return la_launch(la_attn_o_kernel, dim3(grid), dim3(256), smem, st, pdl, x);
 }
 

@@ -5,6 +5,7 @@
 // per-step records.  The host only uploads inputs once per decode and reads
 // outputs once at the end (SURVEY.md §8(b) "Ownership").
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -184,6 +185,20 @@ __device__ __forceinline__ void la_pdl_wait() {
   } while (0)
 
 #ifdef __CUDACC__
+// cudaFuncSetAttribute is per device: set it once on each device a launch uses
+// (a racing second setter is harmless; the bit is published after success)
+template <typename F>
+static inline cudaError_t la_smem_attr_once(std::atomic<unsigned>& done, F* kernel, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned bit = 1u << (dev & 31);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
+
 // cudaLaunchKernelEx with the PDL attribute (pdl = false: plain launch)
 template <typename... KArgs, typename... Args>
 static inline cudaError_t la_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,

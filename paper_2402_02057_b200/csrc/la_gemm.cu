@@ -469,12 +469,10 @@ int la_gemm_workspace_segs(int n_tiles, int kb, int grid, int tpc) {
 
 template <int EPI>
 static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(la_gemm_kernel<EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  static std::atomic<unsigned> attr{0};
+  {
+    cudaError_t e = la_smem_attr_once(attr, la_gemm_kernel<EPI>, (int)kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   // the ring (nst stages), barriers / TMEM slot, and the fused epilogue's staging
   const int nblk = g.args.nblk > 1 ? g.args.nblk : 1;

@@ -1181,13 +1181,9 @@ size_t la_mega_smem_bytes() { return kSmemBytes; }
 int la_mega_threads() { return kThreads; }
 
 cudaError_t la_mega_launch(const LaMegaArgs& a, int grid, cudaStream_t st, bool pdl) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(la_mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0};
+  cudaError_t e = la_smem_attr_once(attr, la_mega_kernel, (int)kSmemBytes);
+  if (e != cudaSuccess) return e;
   return la_launch(la_mega_kernel, dim3(grid), dim3(kThreads), kSmemBytes, st, pdl, a);
 }
 
