@@ -614,6 +614,9 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e, int sp
   if (!active) return;
   const size_t grp = (size_t)kvh * a.nrb_max + rb;
   if (step_unit) {
+    // the step block's K/V (written by the QKV epilogue before the wait) stream
+    // in while the mask is built
+    if (!tc && !a.fuse_qkv) issue_first();
     // structured mask: a query row sees its chain's step keys and itself;
     // one thread per row builds its 128-bit set in registers (independent loads)
     if (tid < LA_MAX_ROWS) {
@@ -639,7 +642,7 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e, int sp
     attn_tc_unit(a, P, smem, sMask, sBars, sTmem, kvh, rb, g, nq, ctx, k_begin, k_end, n_tiles, step_unit,
                  a.part_o + (grp * (S + 1) + split) * 128 * 128, a.part_ml + (grp * (S + 1) + split) * 128);
   } else {
-    if (step_unit) issue_first();
+    if (step_unit && a.fuse_qkv) issue_first();
 
     if (a.fuse_qkv) load_q();   // q is produced by the fused epilogue above
 
