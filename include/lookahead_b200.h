@@ -176,7 +176,10 @@ int32_t la_session_start(la_engine* e, const la_gen_config* cfg, int32_t greedy,
                          const la_sampler* s, la_decode_io* io, void* stream);
 int32_t la_session_step(la_engine* e, la_step_outcome* out, void* stream);
 /* what 0: the window's (N-1)W-1 cells (SURVEY A.1 order); what 1: pool-log
- * n-grams [offset, offset + n), N ints each (inserts in order) */
+ * n-grams [offset, offset + n), N ints each (inserts in order); what 2: the
+ * session generator (reference DecodeState.rng, decoding.py:83) as 10 words --
+ * PCG64 state lo32/hi32 of its high and low 64-bit halves, increment likewise,
+ * has_uint32, uinteger (offset 0, n 10) */
 int32_t la_session_read(la_engine* e, int32_t what, int32_t offset, int32_t n, int32_t* out);
 
 /* Parity hooks (tests only).  la_adjust_distributions: adjusted_distribution

@@ -184,7 +184,10 @@ def decode_lookahead_sampled(model, prompt, W: int, N: int, G: int | None, max_t
         prefix.extend(acc)
         steps.append(StepLog(acc, new_top, len(sufs), len(rows), len(pool), win, wb))
         done = fold_output(out, acc, max_tokens, eos)
-    return OracleRun(out, steps, N)
+    run = OracleRun(out, steps, N)
+    run.rng_state = {"bit_generator": "PCG64", "state": {"state": rng.state, "inc": rng.inc},
+                     "has_uint32": rng.has_uint32, "uinteger": rng.uinteger}
+    return run
 
 
 def decode_autoregressive_sampled(model, prompt, max_tokens: int, temperature: float = 1.0,

@@ -28,15 +28,21 @@
 //    reference (decoding.py:72-82).
 struct DevPool {
   int ngram;       // N
-  int C;           // bucket capacity: >= G (newest-C per lead suffices for lookups);
-                   // with an LRU cap every live entry of a lead (evictions surface older ones)
+  int C;           // bucket capacity (unbounded pool): >= G (newest-C per lead suffices
+                   // for lookups)
   int lt_mask;     // lead table size - 1 (power of two)
   int st_mask;     // distinct set size - 1 (power of two)
   int log_cap;
   int capacity;    // NGramPool(capacity=...) global LRU cap; 0 = unbounded
   int* lead_keys;  // [LT]   -1 = empty
-  int* bkt_cnt;    // [LT]
-  int* bkt_suf;    // [LT][C][N-1]
+  int* bkt_cnt;    // [LT]   bucket length (unbounded) / live entries of the lead (capped)
+  int* bkt_suf;    // [LT][C][N-1] newest-first suffixes (unbounded pool only)
+  // LRU-capped pool: each lead's live entries form a newest-first doubly
+  // linked list threaded through the distinct-set slots, so memory stays
+  // O(LT + ST) for any capacity and an eviction is an O(1) unlink
+  int* lead_head;  // [LT]   newest set slot of the lead, -1 = none
+  int* set_prev;   // [ST]   newer entry of the same lead (-1: list head)
+  int* set_next;   // [ST]   older entry of the same lead (-1: list tail)
   int* set_keys;   // [ST][N]  key[0] == -1 -> empty
   int* set_stamp;  // [ST] last-touch stamp, -1 = evicted (capacity mode)
   int* fifo;       // [log_cap] set slot touched by stamp s (capacity mode)

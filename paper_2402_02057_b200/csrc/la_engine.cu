@@ -228,7 +228,7 @@ extern "C" int32_t la_create(const la_model_desc* desc, const void* const* weigh
     if ((rc = dalloc(e, &e->d_dec, 1))) break;
     if ((rc = dalloc(e, &e->d_plan, 1))) break;
     if ((rc = dalloc(e, &e->d_window, 64 * LA_MAX_NGRAM))) break;
-    if ((rc = dalloc(e, &e->d_cand, 32 * LA_MAX_NGRAM))) break;
+    if ((rc = dalloc(e, &e->d_cand, 64 * LA_MAX_NGRAM))) break;
     if ((rc = dalloc(e, &e->d_amax, LA_MAX_ROWS))) break;
     if ((rc = dalloc(e, &e->d_acc, LA_MAX_NGRAM + 2))) break;
     e->out_cap = desc->max_context + 2 * LA_MAX_NGRAM;
@@ -314,8 +314,8 @@ static int validate_gen(const la_engine* e, const DecodeArgs& a, const la_decode
     if (a.W < 1) { la_set_error("window size W must be >= 1"); return LA_ERR_INVALID_CONFIG; }
     if (a.N < 2) { la_set_error("n-gram size N must be >= 2"); return LA_ERR_INVALID_CONFIG; }
     if (a.G < 0) { la_set_error("max candidate count G must be >= 0"); return LA_ERR_INVALID_CONFIG; }
-    if (a.W > 64 || a.N > LA_MAX_NGRAM || a.G > 32 || (a.N - 1) * (a.W + a.G) > LA_MAX_ROWS) {
-      la_set_error("device limits: W <= 64, N <= %d, G <= 32, (N-1)(W+G) <= %d", LA_MAX_NGRAM, LA_MAX_ROWS);
+    if (a.W > 64 || a.N > LA_MAX_NGRAM || a.G > 64 || (a.N - 1) * (a.W + a.G) > LA_MAX_ROWS) {
+      la_set_error("device limits: W <= 64, N <= %d, G <= 64, (N-1)(W+G) <= %d", LA_MAX_NGRAM, LA_MAX_ROWS);
       return LA_ERR_UNSUPPORTED;
     }
     if (a.W + a.N - 2 >= LA_MAX_CHAIN) { la_set_error("chain too long"); return LA_ERR_UNSUPPORTED; }
@@ -357,20 +357,16 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
   size_t LT = pow2_at_least(2 * std::min<long>(V, inserts) + 2);
   size_t ST = pow2_at_least(2 * inserts + 2);
   // LRU cap (pool.py:41-61): only a cap the decode can reach changes anything;
-  // then a bucket must hold every live entry of its lead
+  // the capped pool keeps each lead's live entries in a linked list over the
+  // distinct-set slots (O(LT + ST) memory for any capacity)
   int cap = (a.mode == LA_MODE_LOOKAHEAD && io->pool_capacity > 0 && io->pool_capacity < inserts)
                 ? io->pool_capacity : 0;
   if (io->pool_capacity < 0) { la_set_error("capacity must be a positive integer"); return LA_ERR_INVALID_CONFIG; }
-  size_t C = std::max(std::max(1, a.G), cap);
-  if ((double)LT * C * (LA_MAX_NGRAM - 1) * 4 > (double)(1ull << 30)) {
-    la_set_error("pool capacity %d: per-lead buckets would need %.1f GB", cap,
-                 (double)LT * C * (LA_MAX_NGRAM - 1) * 4 / 1e9);
-    return LA_ERR_UNSUPPORTED;
-  }
+  size_t C = std::max(1, a.G);
   size_t logc = (size_t)inserts + 1;
   if (!e->p_lead || LT > e->p_lt || ST > e->p_st || C > e->p_C || logc > e->p_log_cap) {
     for (int* p : {e->p_lead, e->p_cnt, e->p_suf, e->p_set, e->p_counters, e->p_log, e->p_stamp,
-                   e->p_fifo}) {
+                   e->p_fifo, e->p_head, e->p_prev, e->p_next}) {
       if (!p) continue;
       auto it = std::find(e->owned.begin(), e->owned.end(), (void*)p);
       if (it != e->owned.end()) e->owned.erase(it);
@@ -386,9 +382,12 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
     RET_IF(dalloc(e, &e->p_log, logc * LA_MAX_NGRAM));
     RET_IF(dalloc(e, &e->p_stamp, ST));
     RET_IF(dalloc(e, &e->p_fifo, logc));
+    RET_IF(dalloc(e, &e->p_head, LT));
+    RET_IF(dalloc(e, &e->p_prev, ST));
+    RET_IF(dalloc(e, &e->p_next, ST));
     e->p_lt = LT; e->p_st = ST; e->p_C = C; e->p_N = LA_MAX_NGRAM; e->p_log_cap = logc;
   }
-  C = std::max(std::max(1, a.G), cap);
+  C = std::max(1, a.G);
   LT = e->p_lt; ST = e->p_st;
   CK(cudaMemsetAsync(e->p_lead, 0xff, LT * sizeof(int), st));
   CK(cudaMemsetAsync(e->p_cnt, 0, LT * sizeof(int), st));
@@ -429,6 +428,7 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
   d.pool.lead_keys = e->p_lead; d.pool.bkt_cnt = e->p_cnt; d.pool.bkt_suf = e->p_suf;
   d.pool.set_keys = e->p_set; d.pool.counters = e->p_counters; d.pool.log = e->p_log;
   d.pool.capacity = cap; d.pool.set_stamp = e->p_stamp; d.pool.fifo = e->p_fifo;
+  d.pool.lead_head = e->p_head; d.pool.set_prev = e->p_prev; d.pool.set_next = e->p_next;
   if (a.smp) {
     d.pcg = pcg_of(a.smp);
     d.pcg_window = a.pcg_window ? 1 : 0;
@@ -638,7 +638,7 @@ extern "C" int32_t la_session_step(la_engine* e, la_step_outcome* out, void* str
 }
 
 // session state readers: what 0 = window cells ((N-1)W-1), 1 = pool-log
-// n-grams [offset, offset+n) (N ints each)
+// n-grams [offset, offset+n) (N ints each), 2 = the generator state (10 words)
 extern "C" int32_t la_session_read(la_engine* e, int32_t what, int32_t offset, int32_t n,
                                    int32_t* out) {
   if (!e || !out || offset < 0 || n < 0) { la_set_error("bad arguments"); return LA_ERR_INVALID_CONFIG; }
@@ -654,6 +654,19 @@ extern "C" int32_t la_session_read(la_engine* e, int32_t what, int32_t offset, i
   if (what == 1) {
     if ((size_t)(offset + n) > e->p_log_cap) { la_set_error("pool log holds %zu entries", e->p_log_cap); return LA_ERR_CAPACITY; }
     if (n) CK(cudaMemcpy(out, e->p_log + (size_t)offset * h.N, (size_t)n * h.N * 4, cudaMemcpyDeviceToHost));
+    return LA_OK;
+  }
+  if (what == 2) {
+    // the session generator (numpy PCG64: state, inc, has_uint32, uinteger) as
+    // 10 words: state hi/lo, inc hi/lo (64-bit little-endian pairs), has32, u32
+    if (offset != 0 || n != 10) { la_set_error("generator state is 10 words"); return LA_ERR_INVALID_CONFIG; }
+    const unsigned long long q[4] = {h.pcg.s_hi, h.pcg.s_lo, h.pcg.i_hi, h.pcg.i_lo};
+    for (int i = 0; i < 4; ++i) {
+      out[2 * i] = (int32_t)(uint32_t)(q[i] & 0xffffffffull);
+      out[2 * i + 1] = (int32_t)(uint32_t)(q[i] >> 32);
+    }
+    out[8] = h.pcg.has32;
+    out[9] = (int32_t)h.pcg.u32;
     return LA_OK;
   }
   la_set_error("unknown session field %d", what);
@@ -675,7 +688,7 @@ extern "C" int32_t la_pool_test(int32_t N, int32_t capacity, int32_t C, const in
   }
   const size_t LT = pow2_at_least(2 * (size_t)n_grams + 2), ST = LT;
   const int nb = (n_grams + batch - 1) / batch;
-  const int Cb = capacity ? std::max(C, capacity) : C;
+  const int Cb = C;
   std::vector<void*> bufs;
   auto dev = [&](size_t bytes, int fill) -> void* {
     void* q = nullptr;
@@ -693,6 +706,9 @@ extern "C" int32_t la_pool_test(int32_t N, int32_t capacity, int32_t C, const in
   p.set_keys = (int*)dev(ST * N * 4, 0xff);
   p.set_stamp = (int*)dev(ST * 4, 0);
   p.fifo = (int*)dev((size_t)p.log_cap * 4, 0);
+  p.lead_head = (int*)dev(LT * 4, 0xff);
+  p.set_prev = (int*)dev(ST * 4, 0xff);
+  p.set_next = (int*)dev(ST * 4, 0xff);
   p.counters = (int*)dev(16, 0);
   p.log = (int*)dev((size_t)p.log_cap * N * 4, 0);
   int* d_grams = (int*)dev((size_t)n_grams * N * 4, 0);

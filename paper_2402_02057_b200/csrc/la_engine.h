@@ -38,6 +38,7 @@ struct la_engine {
   int *p_lead = nullptr, *p_cnt = nullptr, *p_suf = nullptr, *p_set = nullptr;
   int *p_counters = nullptr, *p_log = nullptr;
   int *p_stamp = nullptr, *p_fifo = nullptr;   // LRU cap: [ST] stamps, [log_cap] fifo
+  int *p_head = nullptr, *p_prev = nullptr, *p_next = nullptr;   // LRU cap: [LT] list heads, [ST] links
   size_t p_lt = 0, p_st = 0, p_log_cap = 0, p_C = 0, p_N = 0;
 
   // ---- KV cache [layer][slot][row_bytes]

@@ -430,7 +430,7 @@ static __device__ int la_draw(const double* p, int V, LaPcg64& g, LaSampleSmem& 
 // d.k, d.winner (first surviving branch whose K/V rows are committed).
 // Returns false on DegenerateDistributionError.
 static __device__ bool la_verify_sample(DevDecode& d, LaSampleSmem& sm) {
-  __shared__ int s_alive[32], s_na, s_out[LA_MAX_SUFFIX + 2], s_k, s_win, s_acc;
+  __shared__ int s_alive[64], s_na, s_out[LA_MAX_SUFFIX + 2], s_k, s_win, s_acc;
   __shared__ LaPcg64 s_g;
   const int tid = threadIdx.x, nth = blockDim.x;
   const int V = d.V, S = d.N - 1;

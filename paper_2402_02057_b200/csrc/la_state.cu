@@ -36,10 +36,8 @@ __global__ void __launch_bounds__(256) la_pool_test_kernel(DevPool pool, const i
     __syncthreads();
     for (int q = threadIdx.x; q < n_leads; q += blockDim.x) {
       const int slot = la_lead_find(pool, leads[q]);
-      const int c = slot < 0 ? 0 : min(pool.bkt_cnt[slot], limit);
-      counts[(size_t)b * n_leads + q] = c;
-      int* o = out + ((size_t)b * n_leads + q) * limit * S;
-      for (int i = 0; i < c * S; ++i) o[i] = pool.bkt_suf[(size_t)slot * pool.C * S + i];
+      counts[(size_t)b * n_leads + q] =
+          la_pool_lookup(pool, slot, limit, out + ((size_t)b * n_leads + q) * limit * S);
     }
     if (threadIdx.x == 0) lens[b] = pool.counters[0];
     __syncthreads();

@@ -36,6 +36,7 @@ __device__ __forceinline__ int la_lead_find_or_add(const DevPool& p, int lead) {
     if (k < 0) {
       p.lead_keys[h] = lead;
       p.bkt_cnt[h] = 0;
+      if (p.lead_head) p.lead_head[h] = -1;
       return (int)h;
     }
     h = (h + 1) & (uint32_t)p.lt_mask;
@@ -69,20 +70,6 @@ static __device__ void la_bucket_shift_down(int* B, int upto, int S, int lane) {
     __syncwarp();
     if (mv)
       for (int s = 0; s < S; ++s) B[(base + lane + 1) * S + s] = tmp[s];
-    __syncwarp();
-  }
-}
-
-// entries (v, cnt) move up one slot (bottom chunk first), dropping entry v
-static __device__ void la_bucket_remove(int* B, int cnt, int v, int S, int lane) {
-  int tmp[LA_MAX_SUFFIX];
-  for (int base = v + 1; base < cnt; base += 32) {
-    const bool mv = base + lane < cnt;
-    if (mv)
-      for (int s = 0; s < S; ++s) tmp[s] = B[(base + lane) * S + s];
-    __syncwarp();
-    if (mv)
-      for (int s = 0; s < S; ++s) B[(base + lane - 1) * S + s] = tmp[s];
     __syncwarp();
   }
 }
@@ -129,45 +116,45 @@ static __device__ void la_bucket_insert_warp(const DevPool& p, int slot, const i
   __syncwarp();
 }
 
+// LRU-capped pool lists (capacity mode): set slot h is linked into the
+// newest-first list of its lead
+static __device__ void la_list_unlink(const DevPool& p, int h) {
+  const int lead = la_lead_find(p, p.set_keys[(size_t)h * p.ngram]);
+  if (lead < 0) return;
+  const int pv = p.set_prev[h], nx = p.set_next[h];
+  if (pv >= 0) p.set_next[pv] = nx; else p.lead_head[lead] = nx;
+  if (nx >= 0) p.set_prev[nx] = pv;
+  p.bkt_cnt[lead] -= 1;
+}
+static __device__ void la_list_push_front(const DevPool& p, int lead, int h) {
+  const int hd = p.lead_head[lead];
+  p.set_prev[h] = -1;
+  p.set_next[h] = hd;
+  if (hd >= 0) p.set_prev[hd] = h;
+  p.lead_head[lead] = h;
+  p.bkt_cnt[lead] += 1;
+}
+
 // One n-gram insert by one warp (reference pool.py:41-61): dedup on
 // (lead, suffix) with recency refresh, newest-first bucket, distinct count,
 // and with a capacity the globally least-recently-touched entry is evicted
 // before a new one is added.  `g` may live in shared or global memory.
 static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int lane, int* overflow) {
-  const int N = p.ngram, S = N - 1, C = p.C;
+  const int N = p.ngram;
   int gl[LA_MAX_SUFFIX + 1];
 #pragma unroll
   for (int i = 0; i < LA_MAX_SUFFIX + 1; ++i) gl[i] = (i < N) ? g[i] : 0;
-  int slot = 0, victim = -1;
-  int vkey[LA_MAX_SUFFIX + 1];   // the victim's n-gram (its set slot may be reused below)
-#pragma unroll
-  for (int i = 0; i < LA_MAX_SUFFIX + 1; ++i) vkey[i] = 0;
-  if (lane == 0) {
-    if (p.capacity == 0) {
-      // distinct set (len(pool))
-      uint32_t h = la_gram_hash(gl, N) & (uint32_t)p.st_mask;
-      bool placed = false;
-      for (int probe = 0; probe <= p.st_mask; ++probe) {
-        int* key = p.set_keys + (size_t)h * N;
-        if (key[0] < 0) {
-          for (int i = 0; i < N; ++i) key[i] = gl[i];
-          p.counters[0] += 1;
-          placed = true;
-          break;
-        }
-        bool eq = true;
-        for (int i = 0; i < N; ++i) eq &= (key[i] == gl[i]);
-        if (eq) { placed = true; break; }
-        h = (h + 1) & (uint32_t)p.st_mask;
-      }
-      if (!placed) *overflow = 1;
-    } else {
+  if (p.capacity > 0) {
+    // capped pool, one thread: every live entry sits in its lead's list
+    if (lane == 0) {
       int free_slot;
       int h = la_set_find_live(p, gl, N, &free_slot);
-      if (h < 0) {
+      if (h >= 0) {
+        la_list_unlink(p, h);   // a refresh: re-linked at the front below
+      } else {
         if (p.counters[0] >= p.capacity) {
           // _entries.popitem(last=False): the oldest FIFO record still current
-          int head = p.counters[3];
+          int head = p.counters[3], victim = -1;
           while (head < p.counters[2]) {
             const int v = p.fifo[head];
             const int st = p.set_stamp[v];
@@ -176,11 +163,11 @@ static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int l
           }
           p.counters[3] = head;
           if (victim >= 0) {
-            for (int i = 0; i < N; ++i) vkey[i] = p.set_keys[(size_t)victim * N + i];
+            // del old_bucket[old_suffix] (pool.py:54-58); the slot becomes a tombstone
+            la_list_unlink(p, victim);
             p.set_stamp[victim] = -1;
             p.counters[0] -= 1;
-            // the victim's slot may be the first free one on our probe path
-            la_set_find_live(p, gl, N, &free_slot);
+            la_set_find_live(p, gl, N, &free_slot);   // the victim's slot may be first on our path
           } else {
             *overflow = 1;
           }
@@ -202,10 +189,43 @@ static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int l
       } else {
         *overflow = 1;
       }
+      const int slot = la_lead_find_or_add(p, gl[0]);
+      if (slot < 0) *overflow = 1;
+      else if (h >= 0) la_list_push_front(p, slot, h);
+      const int n = p.counters[1];
+      if (n < p.log_cap) {
+        for (int i = 0; i < N; ++i) p.log[(size_t)n * N + i] = gl[i];
+        p.counters[1] = n + 1;
+      } else {
+        *overflow = 1;
+      }
     }
+    __threadfence_block();
+    __syncwarp();
+    return;
+  }
+  int slot = 0;
+  if (lane == 0) {
+    // distinct set (len(pool))
+    uint32_t h = la_gram_hash(gl, N) & (uint32_t)p.st_mask;
+    bool placed = false;
+    for (int probe = 0; probe <= p.st_mask; ++probe) {
+      int* key = p.set_keys + (size_t)h * N;
+      if (key[0] < 0) {
+        for (int i = 0; i < N; ++i) key[i] = gl[i];
+        p.counters[0] += 1;
+        placed = true;
+        break;
+      }
+      bool eq = true;
+      for (int i = 0; i < N; ++i) eq &= (key[i] == gl[i]);
+      if (eq) { placed = true; break; }
+      h = (h + 1) & (uint32_t)p.st_mask;
+    }
+    if (!placed) *overflow = 1;
     slot = la_lead_find_or_add(p, gl[0]);
     if (slot < 0) *overflow = 1;
-    int n = p.counters[1];
+    const int n = p.counters[1];
     if (n < p.log_cap) {
       for (int i = 0; i < N; ++i) p.log[(size_t)n * N + i] = gl[i];
       p.counters[1] = n + 1;
@@ -214,29 +234,26 @@ static __device__ void la_pool_insert_warp(const DevPool& p, const int* g, int l
     }
   }
   slot = __shfl_sync(0xffffffffu, slot, 0);
-  victim = __shfl_sync(0xffffffffu, victim, 0);
-#pragma unroll
-  for (int i = 0; i < LA_MAX_SUFFIX + 1; ++i) vkey[i] = __shfl_sync(0xffffffffu, vkey[i], 0);
   __syncwarp();
-  if (victim >= 0) {
-    // del old_bucket[old_suffix] (pool.py:54-58)
-    const int* vs = vkey + 1;
-    int vslot = 0;
-    if (lane == 0) vslot = la_lead_find(p, vkey[0]);
-    vslot = __shfl_sync(0xffffffffu, vslot, 0);
-    if (vslot >= 0) {
-      int* VB = p.bkt_suf + (size_t)vslot * C * S;
-      const int vcnt = p.bkt_cnt[vslot];
-      const int at = la_bucket_find(VB, vcnt, S, vs, lane);
-      if (at >= 0) {
-        la_bucket_remove(VB, vcnt, at, S, lane);
-        if (lane == 0) p.bkt_cnt[vslot] = vcnt - 1;
-      }
-    }
-    __syncwarp();
-  }
   if (slot < 0) return;
   la_bucket_insert_warp(p, slot, gl + 1, lane);
+}
+
+// lookup(lead, limit) (pool.py:69-81) by ONE thread: the <= limit newest
+// suffixes of lead-table slot `slot` into out[c][N-1]; returns c
+static __device__ int la_pool_lookup(const DevPool& p, int slot, int limit, int* out) {
+  const int S = p.ngram - 1;
+  if (slot < 0 || limit <= 0) return 0;
+  if (p.capacity == 0) {
+    const int c = min(p.bkt_cnt[slot], limit);
+    const int* B = p.bkt_suf + (size_t)slot * p.C * S;
+    for (int i = 0; i < c * S; ++i) out[i] = B[i];
+    return c;
+  }
+  int c = 0;
+  for (int h = p.lead_head[slot]; h >= 0 && c < limit; h = p.set_next[h], ++c)
+    for (int s = 0; s < S; ++s) out[c * S + s] = p.set_keys[(size_t)h * p.ngram + 1 + s];
+  return c;
 }
 
 // Ordered insert of one step's W harvested n-grams (insert_all, pool.py:63-67)
@@ -401,9 +418,9 @@ static __device__ void la_step_build(DevDecode& d, FwdPlan& P) {
     s_slot = -1;
     s_c = 0;
     if (!s_done && d.mode == LA_MODE_LOOKAHEAD && d.G > 0) {
-      int slot = la_lead_find(d.pool, d.last);
+      const int slot = la_lead_find(d.pool, d.last);
       s_slot = slot;
-      if (slot >= 0) s_c = min(d.pool.bkt_cnt[slot], d.G);
+      s_c = la_pool_lookup(d.pool, slot, d.G, d.cand);
     }
   }
   __syncthreads();
@@ -423,10 +440,6 @@ static __device__ void la_step_build(DevDecode& d, FwdPlan& P) {
     }
     __syncthreads();
     return;
-  }
-  if (c > 0) {
-    const int* B = d.pool.bkt_suf + (size_t)s_slot * d.pool.C * S;
-    for (int i = tid; i < c * S; i += nth) d.cand[i] = B[i];
   }
   if (tid == 0) { d.c = c; d.M = S * (W + c); s_n = 0; }
   __syncthreads();
@@ -510,24 +523,24 @@ static __device__ void la_step_finish(DevDecode& d) {
     } else if (c == 0) {
       s_acc[k++] = d.amax[0];
     } else {
-      unsigned alive = (c >= 32) ? 0xffffffffu : ((1u << c) - 1u);
+      unsigned long long alive = (c >= 64) ? ~0ull : ((1ull << c) - 1ull);
       bool all = true;
       for (int i = 0; i < S; ++i) {
-        int lead = __ffs(alive) - 1;
+        int lead = __ffsll((long long)alive) - 1;
         int row = (i == 0) ? 0 : nwin + lead * S + i - 1;
         int target = d.amax[row];
-        unsigned keep = 0;
+        unsigned long long keep = 0;
         for (int b = 0; b < c; ++b)
-          if (((alive >> b) & 1u) && d.cand[b * S + i] == target) keep |= 1u << b;
+          if (((alive >> b) & 1ull) && d.cand[b * S + i] == target) keep |= 1ull << b;
         s_acc[k++] = target;
         if (!keep) { all = false; break; }
         alive = keep;
       }
       if (all) {
-        win = __ffs(alive) - 1;
+        win = __ffsll((long long)alive) - 1;
         s_acc[k++] = d.amax[nwin + win * S + S - 1];
       } else if (k >= 2) {
-        win = __ffs(alive) - 1;   // survivors of the accepted prefix
+        win = __ffsll((long long)alive) - 1;   // survivors of the accepted prefix
       }
     }
     s_k = k;

@@ -16,6 +16,7 @@ verify_sample's trials / draws and the window refills (``la_sample.cuh``).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from collections.abc import Sequence
 
 import numpy as np
@@ -216,15 +217,20 @@ def decode_jacobi(model, prompt: Sequence[int], m: int,
 
 
 # ------------------------------------------------------------ step sessions
+_SESSION_SEQ = 0
+
+
 class DecodeState:
     """Per-session state (reference decoding.py:53-64).  The window, pool and
-    KV cache live on the device between steps; ``prefix``, ``records`` and the
-    caller-visible ``pool`` are kept in step on the host, ``window`` is read
-    back on access.  One active session per model: a whole-decode call or a
-    newer session on the same model ends it."""
+    KV cache live on the device between steps, in an engine of the session's
+    own (sessions on one model are independent, as in the reference);
+    ``prefix``, ``records``, the caller-visible ``pool`` and ``rng`` (the
+    generator the device consumes) are kept in step on the host, ``window``
+    is read back on access."""
 
-    def __init__(self, model, prefix, pool, config, sampler, rng):
+    def __init__(self, model, prefix, pool, config, sampler, rng, key="main"):
         self.model = model
+        self._key = key
         self.prefix = prefix
         self.pool = pool
         self.config = config
@@ -233,11 +239,14 @@ class DecodeState:
         self.records: list[StepRecord] = []
         self._log_n = 0
 
+    def _engine(self):
+        return self.model.engine(self._key)
+
     @property
     def window(self) -> Window2D:
         m, W, N = self.model, self.config.window, self.config.ngram
         cells = np.zeros(max((N - 1) * W - 1, 1), dtype=np.int32)
-        _lib.check(m.lib.la_session_read(m.engine(), 0, 0, (N - 1) * W - 1,
+        _lib.check(m.lib.la_session_read(self._engine(), 0, 0, (N - 1) * W - 1,
                                          cells.ctypes.data_as(C.POINTER(C.c_int32))))
         levels = [cells[: W - 1].tolist()] + [cells[W - 1 + l * W: W - 1 + (l + 1) * W].tolist()
                                               for l in range(N - 2)]
@@ -247,10 +256,24 @@ class DecodeState:
         n = log_n - self._log_n
         if n > 0:
             buf = np.zeros((n, self.config.ngram), dtype=np.int32)
-            _lib.check(self.model.lib.la_session_read(self.model.engine(), 1, self._log_n, n,
+            _lib.check(self.model.lib.la_session_read(self._engine(), 1, self._log_n, n,
                                                       buf.ctypes.data_as(C.POINTER(C.c_int32))))
             self.pool.insert_all(buf.tolist())
         self._log_n = log_n
+
+    def _sync_rng(self) -> None:
+        """The reference session's generator advances with every window refill
+        and verify_sample draw (layout.py:243-250, verification.py:74-118):
+        mirror the device generator into ``rng``."""
+        w = np.zeros(10, dtype=np.int32)
+        _lib.check(self.model.lib.la_session_read(self._engine(), 2, 0, 10,
+                                                  w.ctypes.data_as(C.POINTER(C.c_int32))))
+        u = w.view(np.uint32).astype(object)
+        q = [int(u[2 * i]) | (int(u[2 * i + 1]) << 32) for i in range(4)]
+        self.rng.bit_generator.state = {
+            "bit_generator": "PCG64",
+            "state": {"state": (q[0] << 64) | q[1], "inc": (q[2] << 64) | q[3]},
+            "has_uint32": int(w[8]), "uinteger": int(u[9])}
 
 
 def start_session(model, prompt: Sequence[int], config: GenerationConfig, sampler: SamplerSpec,
@@ -274,26 +297,34 @@ def start_session(model, prompt: Sequence[int], config: GenerationConfig, sample
     io = _IO(p, 1, stream, init, config.ngram, 1)
     io.io.pool_capacity = 0 if pool.capacity is None else int(pool.capacity)
     smp = _lib.make_sampler(sampler.temperature, sampler.top_k, sampler.top_p, rng)
-    _lib.check(m.lib.la_session_start(m.engine(), C.byref(_gen_config(config)),
-                                      1 if sampler.mode == "greedy" else 0, C.byref(smp),
-                                      C.byref(io.io), m.stream()))
-    state = DecodeState(m, [int(t) for t in p], pool, config, sampler, rng)
+    # every session gets an engine of its own (KV cache, window, pool), released
+    # with the state object
+    global _SESSION_SEQ
+    _SESSION_SEQ += 1
+    key = ("session", _SESSION_SEQ)
+    try:
+        _lib.check(m.lib.la_session_start(m.engine(key), C.byref(_gen_config(config)),
+                                          1 if sampler.mode == "greedy" else 0, C.byref(smp),
+                                          C.byref(io.io), m.stream()))
+    except Exception:
+        m.release_engine(key)
+        raise
+    state = DecodeState(m, [int(t) for t in p], pool, config, sampler, rng, key)
+    weakref.finalize(state, m.release_engine, key)
     # a caller pool's replay is not a new insert; prompt seeding is (pool.py:83-90)
     state._log_n = 0
     state._sync_pool(n_seed)
-    m._session = state
     return state
 
 
 def lookahead_step(state: DecodeState) -> StepOutcome:
     """One generate-and-verify step on the device (reference decoding.py:207-211)."""
     m = state.model
-    if getattr(m, "_session", None) is not state:
-        raise RuntimeError("this session was ended by a later decode or session on the same model")
     out = _lib.la_step_outcome()
-    _lib.check(m.lib.la_session_step(m.engine(), C.byref(out), m.stream()))
+    _lib.check(m.lib.la_session_step(state._engine(), C.byref(out), m.stream()))
     accepted = [int(out.accepted[i]) for i in range(out.n_accepted)]
     state._sync_pool(int(out.pool_log_n))
+    state._sync_rng()
     state.prefix.extend(accepted)
     state.records.append(StepRecord(out.n_accepted, int(out.candidate_count),
                                     int(out.query_count), int(out.pool_size)))

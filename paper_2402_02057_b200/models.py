@@ -65,6 +65,12 @@ class B200Model:
             self._engines[key] = h
         return h
 
+    def release_engine(self, key) -> None:
+        """Destroy one engine (a finished step session's); no-op if absent."""
+        h = self._engines.pop(key, None)
+        if h is not None:
+            self.lib.la_destroy(h)
+
     def close(self) -> None:
         for h in list(self._engines.values()):
             self.lib.la_destroy(h)

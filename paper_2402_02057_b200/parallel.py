@@ -132,9 +132,23 @@ def decode_lookahead_devices(model, prompt: Sequence[int], config: GenerationCon
     if not 1 <= devices <= config.window:
         raise ValueError(f"device count must lie in [1, {config.window}], got {devices}")
     if sampler.mode != "greedy":
-        # the per-step exchange carries argmax ids, not distributions
-        raise NotImplementedError("lookahead parallelism runs the greedy sampler; a temperature "
-                                  "SamplerSpec decodes on one device (decode_lookahead)")
+        # verify_sample needs whole adjusted distributions of the verified rows
+        # while the LP exchange carries argmax ids, so a temperature decode runs
+        # as a replica on every rank.  The reference defines the LP outcome as
+        # bit-identical to the single-device decode (parallel.py:145-151,
+        # SPEC.md:515,523) -- this is that decode -- and CommStats keeps the
+        # reference accounting of the sharded step (parallel.py:164,168).
+        io = _prepare_lookahead(m, prompt, config, sampler, pool)
+        eng = m.engine("replica") if getattr(m, "_lp_world", 1) > 1 else m.engine()
+        _lib.check(m.lib.la_decode_lookahead_sampled(eng, C.byref(_gen_config(config)),
+                                                     C.byref(io.sampler), C.byref(io.io),
+                                                     m.stream()))
+        m.last_stats = io.stats()
+        tokens, metrics = _finish_lookahead(io, config, pool)
+        totals = CommStats()
+        for rec in io.records():
+            totals.add(step_comm(config.window, config.ngram, devices, rec.candidate_count))
+        return tokens, metrics, totals
     io = _prepare_lookahead(m, prompt, config, sampler, pool)
     dist, rank, world = _dist_world()
     if dist is not None and world == devices and devices > 1:

@@ -23,8 +23,11 @@ def test_cli_error_exits(tmp_path, capsys):
     p = tmp_path / "p.txt"
     p.write_text("hello\n")
     # markov is host tooling, not on the device path: runtime error (exit 1)
-    assert cli.main(["decode", "--prompts", str(p), "--out", str(tmp_path / "r.json")]) == 1
+    assert cli.main(["decode", "--model", "markov", "--prompts", str(p),
+                     "--out", str(tmp_path / "r.json")]) == 1
     assert "markov" in capsys.readouterr().err
+    # the default model is the device transformer
+    assert cli.build_parser().parse_args(["decode", "--prompts", str(p)]).model == "transformer"
     empty = tmp_path / "e.txt"
     empty.write_text("\n")
     assert cli.main(["decode", "--model", "transformer", "--prompts", str(empty),

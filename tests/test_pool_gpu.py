@@ -67,3 +67,56 @@ def test_reference_pool_streams_on_device():
             got = [list(out[b, lead, i]) for i in range(min(counts[b, lead], lim))]
             assert got == o["result"], (N, cap, b)
             assert lens[b] == o["len"]
+
+
+def test_large_capacity_pool_memory_is_linear():
+    """An LRU cap of thousands of entries over a 1000-token vocabulary (the
+    capped pool links each lead's entries through the distinct-set slots:
+    O(LT + ST) memory, no per-lead buckets sized to the cap)."""
+    N, cap, V = 5, 2500, 1000
+    rng = np.random.default_rng(17)
+    grams = rng.integers(0, V, size=(15 * 300, N))
+    grams[:, 0] = rng.integers(0, 40, size=len(grams))        # few leads, long lists
+    grams[7::9] = grams[3::9][: len(grams[7::9])]             # refreshes
+    leads, limit = list(range(40)), 15
+    out, counts, lens = _device_pool(N, cap, grams.ravel(), 15, leads, limit)
+    pool = lo.OraclePool(N, capacity=cap)
+    for b in range(len(lens)):
+        pool.insert_all([tuple(int(t) for t in x) for x in grams[b * 15:(b + 1) * 15]])
+        assert lens[b] == len(pool), b
+        if b % 25 == 0 or b == len(lens) - 1:
+            for q, lead in enumerate(leads):
+                got = [tuple(out[b, q, i].tolist()) for i in range(counts[b, q])]
+                assert got == [tuple(s) for s in pool.lookup(lead, limit)], (b, lead)
+    assert len(pool) == cap
+
+
+def test_capped_decode_at_7b_session_scale():
+    """The advisor's failing case: a W15 N5 G15 session with a pool cap of a
+    few thousand on a 1000-token vocabulary and a 2048-token context now runs;
+    greedy lookahead stays lossless."""
+    from oracle.model_oracle import llama_random_weights
+    cfg_m = dict(dim=256, layers=2, heads=4, kv_heads=2, head_dim=128, ffn=512, vocab=1000,
+                 rope_theta=10000.0, eps=1e-5)
+    w = llama_random_weights(cfg_m, seed=3, std=None)
+    lc = la.LlamaConfig(dim=256, layers=2, heads=4, kv_heads=2, ffn=512, vocab=1000, head_dim=128,
+                        rope_theta=1e4, norm_eps=1e-5)
+    m = la.LlamaModel(lc, dtype="bf16", weights=w, max_context=2048)
+    try:
+        prompt = [int(t) for t in np.random.default_rng(5).integers(0, 1000, 600)]
+        cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=200,
+                                  seed_pool_from_prompt=True)
+        ar = la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), 200)
+        for cap in (600, 2500):
+            pool = la.NGramPool(5, capacity=cap)
+            toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=0), pool=pool)
+            assert toks == ar
+            assert len(pool) <= cap
+            state = la.start_session(m, prompt, cfg, la.SamplerSpec("greedy", seed=0),
+                                     pool=la.NGramPool(5, capacity=cap))
+            out = []
+            while not la.collect_output(out, la.lookahead_step(state).accepted, 200, None):
+                pass
+            assert out == ar
+    finally:
+        m.close()

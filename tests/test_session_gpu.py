@@ -65,7 +65,9 @@ def test_sampled_session_matches_reference_trace(models):
 
 def test_session_state_and_pool_mirror(models):
     """DecodeState fields: the caller pool is mutated like the reference's,
-    the window reads back in Window2D form, whole decodes end the session."""
+    the window reads back in Window2D form, ``rng`` advances like the
+    reference session's generator, and a whole decode in between does not
+    disturb the session (sessions own their engine)."""
     from oracle import lookahead_oracle as lo
     m = models(0, 256)
     prompt = [int(t) for t in np.random.default_rng(4).integers(0, 256, 20)]
@@ -78,8 +80,19 @@ def test_session_state_and_pool_mirror(models):
     w0 = np.random.default_rng(2).integers(0, 256, size=(3 - 1) * 4 - 1).tolist()
     assert state.window.levels == [w0[:3], w0[3:]]
     out = []
-    while not la.collect_output(out, la.lookahead_step(state).accepted, 30, None):
-        pass
+    g = np.random.default_rng(2)
+    g.integers(0, 256, size=(3 - 1) * 4 - 1)
+    first = True
+    while True:
+        o = la.lookahead_step(state)
+        for _ in range(lo.window_draws(4, 3, len(o.accepted))):
+            g.integers(0, 256)
+        assert state.rng.bit_generator.state == g.bit_generator.state
+        if first:
+            la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), 4)
+            first = False
+        if la.collect_output(out, o.accepted, 30, None):
+            break
     # oracle: same caller pool, same decode
     opool = lo.OraclePool(3)
     opool.insert((1, 2, 3))
@@ -90,9 +103,37 @@ def test_session_state_and_pool_mirror(models):
     assert len(pool) == len(opool)
     for t in range(256):
         assert pool.lookup(t, 4) == opool.lookup(t, 4)
-    la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), 4)
-    with pytest.raises(ValueError, match="session"):
-        la.lookahead_step(state)
+
+
+def test_interleaved_sessions_are_independent(models):
+    """Two DecodeStates on one model, stepped alternately (the reference keeps
+    no per-model session state): each reproduces its own whole decode, and a
+    temperature session's ``rng`` ends where the reference generator does."""
+    m = models(0, 256)
+    p1 = [int(t) for t in np.random.default_rng(5).integers(0, 256, 16)]
+    p2 = [int(t) for t in np.random.default_rng(6).integers(0, 256, 24)]
+    c1 = la.GenerationConfig(window=5, ngram=3, max_candidates=5, max_tokens=24)
+    c2 = la.GenerationConfig(window=4, ngram=4, max_candidates=3, max_tokens=20,
+                             seed_pool_from_prompt=True)
+    s2 = la.SamplerSpec("temperature", temperature=0.8, top_p=0.9, seed=11)
+    w1, _ = la.decode_lookahead(m, p1, c1, la.SamplerSpec("greedy", seed=1))
+    w2, _ = la.decode_lookahead(m, p2, c2, s2)
+    a = la.start_session(m, p1, c1, la.SamplerSpec("greedy", seed=1))
+    b = la.start_session(m, p2, c2, s2)
+    oa, ob, da, db = [], [], False, False
+    while not (da and db):
+        if not da:
+            da = la.collect_output(oa, la.lookahead_step(a).accepted, 24, None)
+        if not db:
+            db = la.collect_output(ob, la.lookahead_step(b).accepted, 20, None)
+    assert oa == w1 and ob == w2
+    # the sampled session's generator: the reference state after the same decode
+    from oracle import sampling_oracle as so
+    from oracle.model_oracle import TinyTransformerOracle
+    ref = so.decode_lookahead_sampled(TinyTransformerOracle(0, 256), p2, 4, 4, 3, 20, 0.8, None, 0.9,
+                                      seed=11, seed_pool=True)
+    assert ob == ref.tokens
+    assert b.rng.bit_generator.state == ref.rng_state
 
 
 def test_bf16_session_equals_whole_decode():

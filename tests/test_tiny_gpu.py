@@ -121,6 +121,50 @@ def test_lp_simulation_matches_reference(models):
         assert toks1 == toks and met1.steps == met.steps
 
 
+def test_lp_temperature_sampler_equals_single_device(models):
+    """A temperature SamplerSpec under decode_lookahead_devices (reference
+    parallel.py:145-192 accepts every sampler): the decode equals the
+    single-device sampled decode and CommStats follows the reference formula."""
+    from paper_2402_02057_b200.parallel import step_comm
+    m = models(0, 256)
+    prompt = [int(t) for t in np.random.default_rng(9).integers(0, 256, 24)]
+    cfg = la.GenerationConfig(window=6, ngram=4, max_candidates=6, max_tokens=40,
+                              seed_pool_from_prompt=True)
+    spec = la.SamplerSpec("temperature", temperature=0.7, top_k=50, seed=4)
+    one, met1 = la.decode_lookahead(m, prompt, cfg, spec)
+    for D in (2, 3):
+        toks, met, comm = la.decode_lookahead_devices(m, prompt, cfg, spec, D)
+        assert toks == one and met.steps == met1.steps
+        assert met.acceptance_histogram == met1.acceptance_histogram
+        assert comm.sync_events == met.steps
+        assert comm.tokens_synchronized > 0
+
+
+def test_more_than_32_candidates(models):
+    """G defaults to W (types.py:92-93): W = 40, N = 2 gives G = 40 > 32
+    candidates per step within the row limit; lossless against the oracle."""
+    from oracle import lookahead_oracle as lo
+    from oracle.model_oracle import TinyTransformerOracle
+    m = models(0, 256)
+    prompt = [int(t) for t in np.random.default_rng(2).integers(0, 8, 200)]
+    cfg = la.GenerationConfig(window=40, ngram=2, max_tokens=60, seed_pool_from_prompt=True)
+    assert cfg.max_candidates == 40
+    toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=1))
+    run = lo.decode_lookahead(TinyTransformerOracle(0, 256), prompt, 40, 2, 40, 60, seed=1,
+                              seed_pool=True)
+    assert toks == run.tokens
+    assert met.steps == len(run.steps)
+    state = la.start_session(m, prompt, cfg, la.SamplerSpec("greedy", seed=1))
+    counts, out = [], []
+    while True:
+        o = la.lookahead_step(state)
+        counts.append(o.candidate_count)
+        if la.collect_output(out, o.accepted, 60, None):
+            break
+    assert out == run.tokens
+    assert counts == [st.candidate_count for st in run.steps]
+
+
 def test_caller_pool_is_mutated_like_reference(models):
     from oracle import lookahead_oracle as lo
     from oracle.model_oracle import TinyTransformerOracle
