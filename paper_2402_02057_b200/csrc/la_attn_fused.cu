@@ -1313,7 +1313,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_o_kernel(LaAttnOArgs x) {
   const long u_begin = (long)blockIdx.x * U / Pn, u_end = (long)(blockIdx.x + 1) * U / Pn;
   const int n_pre = (int)min((long)nst, u_end - u_begin);
   la_pdl_trigger();
-  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 0] = t_; }
+  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 8 + 0] = t_; }
   uint64_t pol_w = 0;
   if (threadIdx.x == 0) {
     pol_w = ptx::policy_evict_first();
@@ -1344,7 +1344,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_o_kernel(LaAttnOArgs x) {
   }
   __syncthreads();
 
-  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 1] = t_; }
+  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 8 + 1] = t_; }
   // ---- O projection phase (split-K pieces, as la_gemm_kernel<LA_EPI_PARTIAL>)
   const unsigned target = (unsigned)(a.nrb_max * (a.S + 1));
   const int feats_per_kvh = (a.H / a.KVH) * 128;
@@ -1372,7 +1372,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_o_kernel(LaAttnOArgs x) {
             __nanosleep(64);
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          if (ready < 0 && x.g.trace) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 2] = t_; }
+          if (ready < 0 && x.g.trace) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 8 + 2] = t_; }
           ready = kvh;
         }
         if (it < n_pre) {
@@ -1452,7 +1452,7 @@ __global__ void __launch_bounds__(256, 1) la_attn_o_kernel(LaAttnOArgs x) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
-  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 4 + 3] = t_; }
+  if (x.g.trace && threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); x.g.trace[blockIdx.x * 8 + 3] = t_; }
   if (threadIdx.x == 0) {
     // the last CTA out resets the per-head counters for the next launch
     __threadfence();

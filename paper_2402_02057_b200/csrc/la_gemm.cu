@@ -14,6 +14,7 @@
 #include "../../include/lookahead_b200.h"
 #include "la_gemm.cuh"
 #include "la_ptx.cuh"
+#include "la_reduce_dev.cuh"
 
 void la_set_error(const char* fmt, ...);
 
@@ -28,7 +29,138 @@ constexpr int kThreads = 192;
 constexpr int kTmemCols = 512;                 // 2 buffers x LA_TPC tiles x 128 columns
 constexpr int kEpiLd = 33;                     // fused-epilogue staging [128 f][33]
 constexpr size_t kSmemBytes =
-    1024 + kStages * (kABytes + kBBytes) + 128 * kEpiLd * 4 + 2 * kMaxStages * 8 + 4 * 8 + 16 + 128 * 4;
+    1024 + kStages * (kABytes + kBBytes) + 128 * kEpiLd * 4 + 2 * kMaxStages * 8 + 5 * 8 + 16 + 128 * 4;
+
+constexpr bool is_fx(int epi) { return epi >= LA_EPI_FX_QKV && epi <= LA_EPI_FX_RESID; }
+
+// ------------------------------------------------ in-GEMM split-K fix-up
+// Staging image of one unit tile's row slice: S[s][tt][rr][128 f] fp32 for
+// pieces s < nseg, tiles tt < tpc, slice rows rr < nr.
+__device__ __forceinline__ const float* fx_piece(const float* S, int s, int tt, int rr, int tpc, int nr) {
+  return S + ((size_t)(s * tpc + tt) * nr + rr) * 128;
+}
+// sum over the pieces, in piece order, of 4 consecutive features (as seg_sum4)
+__device__ __forceinline__ float4 fx_sum4(const float* S, int nseg, int tt, int rr, int tpc, int nr, int f) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < nseg; ++s) {
+    const float4 v = *reinterpret_cast<const float4*>(fx_piece(S, s, tt, rr, tpc, nr) + f);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  return acc;
+}
+
+// Epilogue of rows [r0, r0 + nr) of unit tile ut on the 128 drain threads
+// (et = 0..127).  The arithmetic is exactly that of the standalone epilogue
+// kernels (la_reduce.cu) -- same piece order, same lane grouping for the norm
+// statistics -- so the fused and unfused paths agree bit for bit.
+template <int EPI>
+__device__ void fx_finish(const LaGemmArgs& a, const FwdPlan* P, int ut, int r0, int nr, int nseg,
+                          const float* S, int et) {
+  const int lane = et & 31;
+  const int tpc = a.tpc, items = tpc * nr;
+  if constexpr (EPI == LA_EPI_FX_RESID) {
+    // warp = (tile, row), lane = 4 features (la_resid_norm_kernel)
+    for (int it = et >> 5; it < items; it += 4) {
+      const int tt = it / nr, rr = it % nr;
+      const int t = ut * tpc + tt;
+      if (t >= a.n_real) continue;
+      const int r = r0 + rr, fl = lane * 4, f = t * 128 + fl;
+      const float4 p = fx_sum4(S, nseg, tt, rr, tpc, nr, fl);
+      float* xr = a.x + (size_t)r * a.d + f;
+      const float4 g = __ldg(reinterpret_cast<const float4*>(a.gain + f));
+      float4 v = *reinterpret_cast<const float4*>(xr);
+      v.x += p.x; v.y += p.y; v.z += p.z; v.w += p.w;
+      *reinterpret_cast<float4*>(xr) = v;
+      *reinterpret_cast<uint2*>(a.h_out + la_act_off(r, f)) =
+          make_uint2(pack2(v.x * g.x, v.y * g.y), pack2(v.z * g.z, v.w * g.w));
+      float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) a.ss_out[t * 128 + r] = ss;
+    }
+  } else if constexpr (EPI == LA_EPI_FX_QKV) {
+    // half-warp = (tile, row), lane & 15 = 4 rotary pairs (la_qkv_fix)
+    for (int it = et >> 4; it < items; it += 8) {
+      const int tt = it / nr, rr = it % nr;
+      const int t = ut * tpc + tt;
+      if (t >= a.n_real) continue;
+      const int tok = r0 + rr;
+      const int i0 = (et & 15) * 4;
+      const bool v_tile = t >= a.H + a.KVH;
+      const LaSsLoads ssl = rstd16_issue(a.nrm, tok);
+      const int pos = P->pos[tok];
+      float4 c = make_float4(1.f, 1.f, 1.f, 1.f), sn = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!v_tile) {
+        c = __ldg(reinterpret_cast<const float4*>(a.rope_cos + (size_t)pos * 64 + i0));
+        sn = __ldg(reinterpret_cast<const float4*>(a.rope_sin + (size_t)pos * 64 + i0));
+      }
+      float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+      for (int s = 0; s < nseg; ++s) {
+        const float* pp = fx_piece(S, s, tt, rr, tpc, nr);
+        const float4 u = *reinterpret_cast<const float4*>(pp + i0);
+        const float4 w = *reinterpret_cast<const float4*>(pp + i0 + 64);
+        x0.x += u.x; x0.y += u.y; x0.z += u.z; x0.w += u.w;
+        x1.x += w.x; x1.y += w.y; x1.z += w.z; x1.w += w.w;
+      }
+      const float rs = rstd16_finish(a.nrm, tok, ssl);
+      x0.x *= rs; x0.y *= rs; x0.z *= rs; x0.w *= rs;
+      x1.x *= rs; x1.y *= rs; x1.z *= rs; x1.w *= rs;
+      __nv_bfloat16* dst;
+      if (t < a.H) dst = a.q_out + ((size_t)tok * a.H + t) * 128;
+      else if (!v_tile) dst = a.kc + ((size_t)P->slot[tok] * a.KVH + (t - a.H)) * 128;
+      else dst = a.vc + ((size_t)P->slot[tok] * a.KVH + (t - a.H - a.KVH)) * 128;
+      if (!v_tile) {
+        const float4 a2 = make_float4(x0.x * c.x - x1.x * sn.x, x0.y * c.y - x1.y * sn.y,
+                                      x0.z * c.z - x1.z * sn.z, x0.w * c.w - x1.w * sn.w);
+        const float4 b2 = make_float4(x1.x * c.x + x0.x * sn.x, x1.y * c.y + x0.y * sn.y,
+                                      x1.z * c.z + x0.z * sn.z, x1.w * c.w + x0.w * sn.w);
+        x0 = a2;
+        x1 = b2;
+      }
+      *reinterpret_cast<uint2*>(dst + i0) = make_uint2(pack2(x0.x, x0.y), pack2(x0.z, x0.w));
+      *reinterpret_cast<uint2*>(dst + i0 + 64) = make_uint2(pack2(x1.x, x1.y), pack2(x1.z, x1.w));
+    }
+  } else if constexpr (EPI == LA_EPI_FX_SWIGLU) {
+    // 8 threads = (tile, row), 8 outputs each (la_swiglu_epi_kernel)
+    for (int it = et >> 3; it < items; it += 16) {
+      const int tt = it / nr, rr = it % nr;
+      const int t = ut * tpc + tt;
+      if (t >= a.n_real) continue;
+      const int tok = r0 + rr;
+      const int i0 = (et & 7) * 8;
+      const LaSsLoads ssl = rstd_issue<8>(a.nrm, tok);
+      float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), u0 = g0, g1 = g0, u1 = g0;
+      for (int s = 0; s < nseg; ++s) {
+        const float* pp = fx_piece(S, s, tt, rr, tpc, nr);
+        const float4 a0 = *reinterpret_cast<const float4*>(pp + i0);
+        const float4 b0 = *reinterpret_cast<const float4*>(pp + i0 + 64);
+        const float4 a1 = *reinterpret_cast<const float4*>(pp + i0 + 4);
+        const float4 b1 = *reinterpret_cast<const float4*>(pp + i0 + 68);
+        g0.x += a0.x; g0.y += a0.y; g0.z += a0.z; g0.w += a0.w;
+        u0.x += b0.x; u0.y += b0.y; u0.z += b0.z; u0.w += b0.w;
+        g1.x += a1.x; g1.y += a1.y; g1.z += a1.z; g1.w += a1.w;
+        u1.x += b1.x; u1.y += b1.y; u1.z += b1.z; u1.w += b1.w;
+      }
+      const float rs = rstd_finish<8>(a.nrm, tok, ssl);
+      const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float u[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+      float w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gg = g[i] * rs, uu = u[i] * rs;
+        w[i] = gg / (1.0f + __expf(-gg)) * uu;
+      }
+      *reinterpret_cast<uint4*>(a.act + la_act_off(tok, t * 64 + i0)) =
+          make_uint4(pack2(w[0], w[1]), pack2(w[2], w[3]), pack2(w[4], w[5]), pack2(w[6], w[7]));
+    }
+  }
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -158,7 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* fxbar = tempty + 2;                     // fix-up staging (LA_EPI_FX_*)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 1);
   int* sflag = reinterpret_cast<int*>(tmem_slot + 1);
   float* sEpi = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
   float* sRstd = sEpi + 128 * kEpiLd;   // fused epilogues: per-row deferred-norm scale
@@ -188,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
+    ptx::mbar_init(fxbar, 1);
     ptx::fence_barrier_init();
     pol_w = ptx::policy_evict_first();   // weights: streamed once
     for (int i = 0; i < n_pre; ++i) {
@@ -211,13 +345,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();
   }
   // trace: [0] CTA entry (before the dependency wait), [1] wait returned
-  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 0] = t_entry;
+  if (args.trace && threadIdx.x == 0) {
+    args.trace[blockIdx.x * 8 + 0] = t_entry;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (!is_fx(EPI)) args.trace[blockIdx.x * 8 + 5] = smid;   // (fix-up slot unused)
+  }
   const int n_rows = P->n_rows;
   const int n_pad = P->n_pad;
   int n_rows_x[3] = {0, 0, 0}, n_pad_x[3] = {0, 0, 0};
   if constexpr (multi)
     for (int j = 1; j < nblk; ++j) { n_rows_x[j - 1] = args.planx[j - 1]->n_rows; n_pad_x[j - 1] = args.planx[j - 1]->n_pad; }
-  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 1] = globaltimer();
+  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 8 + 1] = globaltimer();
 
   if (n_rows == 0) {
     // decode finished: drain the prefetched weight tiles before exiting
@@ -303,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         use[buf]++;
         buf = nbuf == 2 ? buf ^ 1 : 0;
       }
-      if (args.trace) args.trace[blockIdx.x * 4 + 2] = globaltimer();
+      if (args.trace) args.trace[blockIdx.x * 8 + 2] = globaltimer();
     }
   } else {
     // ------------------------------------------- drain TMEM / epilogue
@@ -319,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg = (int)(blockIdx.x - c_first);
       ptx::mbar_wait(&tfull[buf], use[buf] & 1);
       ptx::tc_fence_after();
-      if (EPI == LA_EPI_PARTIAL || multi || seg != 0) {
+      if (EPI == LA_EPI_PARTIAL || multi || is_fx(EPI) || seg != 0) {
         // write this piece's fp32 partial (multi-chunk mode: every row block)
         const int nout = multi ? nblk : tpc;
         for (int tt = 0; tt < nout; ++tt) {
@@ -338,12 +477,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[buf]);
-        if (EPI != LA_EPI_PARTIAL && !multi) {
+        if constexpr (is_fx(EPI)) {
+          // this piece is complete: count it in for the unit tile's fix-up
+          __threadfence();
+          ptx::named_bar_sync(1, 128);
+          if (et == 0) atomicAdd(args.fx_arrive + tile, 1);
+        } else if (EPI != LA_EPI_PARTIAL && !multi) {
           __threadfence();
           ptx::named_bar_sync(1, 128);
           if (et == 0) atomicAdd(args.counters + tile, 1);
         }
-      } else if constexpr (EPI != LA_EPI_PARTIAL && EPI != LA_EPI_MULTI) {
+      } else if constexpr (EPI != LA_EPI_PARTIAL && EPI != LA_EPI_MULTI && !is_fx(EPI)) {
         // owner of the tile's k = 0 piece: wait for the other pieces, sum them
         // in piece order onto the accumulator, apply the fused epilogue
         const int nseg = (int)(la_cta_of((long)(tile + 1) * kb - 1, U, Pn) - c_first + 1);
@@ -391,13 +535,56 @@ __global__ void __launch_bounds__(kThreads, 1)
       buf = nbuf == 2 ? buf ^ 1 : 0;
       u = seg_end;
     }
+    if (args.trace && et == 0) args.trace[blockIdx.x * 8 + 4] = globaltimer();   // last piece written
+    if constexpr (is_fx(EPI)) {
+      // ---- fix-up: every MMA of this CTA has completed (its last TMEM
+      // buffer was drained above), so the smem ring is free for staging
+      float* S = reinterpret_cast<float*>(sA);
+      const uint64_t pol = ptx::policy_evict_first();
+      uint32_t fx_phase = 0;
+      for (long ut = u_begin / kb; ut <= (u_end - 1) / kb; ++ut) {
+        long c0;
+        int nseg;
+        la_tile_segs((int)(ut * tpc), kb, args.n_tiles, Pn, c0, nseg, tpc);
+        const int j = (int)(blockIdx.x - c0);
+        const int r0 = j * n_rows / nseg, nr = (j + 1) * n_rows / nseg - r0;
+        if (et == 0) {
+          while (ld_acquire(args.fx_arrive + ut) < nseg) __nanosleep(32);
+          if (args.trace && ut == u_begin / kb) args.trace[blockIdx.x * 8 + 5] = globaltimer();
+        }
+        ptx::named_bar_sync(1, 128);
+        if (nr > 0) {
+          if (et == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy pieces -> bulk copies
+            const uint32_t bytes = (uint32_t)nr * 512;
+            ptx::mbar_expect_tx(fxbar, bytes * (uint32_t)(nseg * tpc));
+            for (int sg = 0; sg < nseg; ++sg)
+              for (int tt = 0; tt < tpc; ++tt)
+                ptx::bulk_load(S + (size_t)(sg * tpc + tt) * nr * 128,
+                               args.ws + (((size_t)(ut * tpc + tt) * args.max_segs + sg) * 128 + r0) * 128,
+                               bytes, fxbar, pol);
+          }
+          ptx::mbar_wait(fxbar, fx_phase);
+          fx_phase ^= 1;
+          if (args.trace && et == 0 && ut == u_begin / kb) args.trace[blockIdx.x * 8 + 6] = globaltimer();
+          fx_finish<EPI>(args, P, (int)ut, r0, nr, nseg, S, et);
+        }
+        ptx::named_bar_sync(1, 128);   // S is restaged for the next unit tile
+        if (et == 0 && atomicAdd(args.fx_depart + ut, 1) == nseg - 1) {
+          // every contributor is past its wait: reset for the next launch
+          args.fx_arrive[ut] = 0;
+          args.fx_depart[ut] = 0;
+        }
+      }
+      if (args.trace && et == 0) args.trace[blockIdx.x * 8 + 7] = globaltimer();
+    }
   }
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem);
   }
-  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 4 + 3] = globaltimer();
+  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 8 + 3] = globaltimer();
   if (args.timing && threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&args.timing[4], 1ull) == (unsigned long long)gridDim.x - 1) {
@@ -456,6 +643,23 @@ int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_ro
   return LA_OK;
 }
 
+// the fix-up stages nseg pieces x tpc tiles x ceil(rows / nseg) rows of 512 B
+// in the smem ring: check the worst case (128 rows) against the ring
+bool la_gemm_fx_fits(const LaGemm& g) {
+  const int tpc = g.args.tpc;
+  const int nst = g.args.nst > 0 ? g.args.nst : (tpc == LA_TPC ? kStages : kMaxStages);
+  const size_t ring = (size_t)nst * (tpc * kTileBytes + kBBytes);
+  const int U = g.args.n_tiles / tpc;
+  for (int ut = 0; ut < U; ++ut) {
+    long c0;
+    int n;
+    la_tile_segs(ut * tpc, g.args.kb, g.args.n_tiles, g.grid, c0, n, tpc);
+    const size_t need = (size_t)n * tpc * ((LA_MAX_ROWS + n - 1) / n) * 512;
+    if (need > ring) return false;
+  }
+  return true;
+}
+
 int la_gemm_workspace_segs(int n_tiles, int kb, int grid, int tpc) {
   long mx = 1;
   for (int t = 0; t < n_tiles; ++t) {
@@ -479,7 +683,8 @@ static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
   const int nst = g.args.nst > 0 ? g.args.nst : nblk > 1 ? (nblk > 2 ? 2 : kStages)
                                                          : (g.args.tpc == LA_TPC ? kStages : kMaxStages);
   const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + nblk * kBBytes) + 2 * kMaxStages * 8 +
-                      4 * 8 + 16 + (EPI == LA_EPI_PARTIAL || EPI == LA_EPI_MULTI ? 0 : 128 * kEpiLd * 4 + 128 * 4);
+                      5 * 8 + 16 +
+                      (EPI == LA_EPI_PARTIAL || EPI == LA_EPI_MULTI || is_fx(EPI) ? 0 : 128 * kEpiLd * 4 + 128 * 4);
   return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
 }
 
@@ -489,6 +694,9 @@ int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {
     case LA_EPI_QKV: e = launch_epi<LA_EPI_QKV>(g, st, pdl); break;
     case LA_EPI_SWIGLU: e = launch_epi<LA_EPI_SWIGLU>(g, st, pdl); break;
     case LA_EPI_LOGITS: e = launch_epi<LA_EPI_LOGITS>(g, st, pdl); break;
+    case LA_EPI_FX_QKV: e = launch_epi<LA_EPI_FX_QKV>(g, st, pdl); break;
+    case LA_EPI_FX_SWIGLU: e = launch_epi<LA_EPI_FX_SWIGLU>(g, st, pdl); break;
+    case LA_EPI_FX_RESID: e = launch_epi<LA_EPI_FX_RESID>(g, st, pdl); break;
     default: e = g.args.nblk > 1 ? launch_epi<LA_EPI_MULTI>(g, st, pdl) : launch_epi<LA_EPI_PARTIAL>(g, st, pdl); break;
   }
   if (e == cudaSuccess) e = cudaGetLastError();

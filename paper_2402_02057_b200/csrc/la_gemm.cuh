@@ -71,10 +71,28 @@ struct LaGemmArgs {
   float* logits;                     // LOGITS: [128][V] dump or null
   int V;
   LaRowNorm nrm;                     // fused epilogues: deferred RMSNorm of the input rows
+  // ---- split-K fix-up inside the GEMM (LA_EPI_FX_*): every CTA writes its
+  // pieces and counts them in (fx_arrive); after its own unit range it waits
+  // until each unit tile it touched has all pieces, bulk-copies ITS row slice
+  // of every piece into the (now idle) smem ring and applies the epilogue to
+  // that slice -- the n contributors of a tile finish n disjoint row slices,
+  // so the reduction is spread and needs no separate kernel
+  int* fx_arrive;                    // [unit tiles] pieces written (reset by the last departer)
+  int* fx_depart;                    // [unit tiles] slices finished
+  int n_real;                        // real feature tiles (the packing pads to LA_TPC)
+  float* x;                          // FX_RESID: [128][d] fp32 residual stream (x += piece sum)
+  const float* gain;                 // FX_RESID: next RMSNorm gain
+  __nv_bfloat16* h_out;              // FX_RESID: next GEMM input bf16(x * gain), packed LA rows
+  float* ss_out;                     // FX_RESID: [d/128][128] per-tile sums of x^2
+  int d;
 };
 
 enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_LOGITS = 3,
-                 LA_EPI_MULTI = 4 };   // split-K pieces, nblk row blocks (prefill; chosen by nblk > 1)
+                 LA_EPI_MULTI = 4,     // split-K pieces, nblk row blocks (prefill; chosen by nblk > 1)
+                 // split-K fix-up + epilogue in the GEMM (decode step; la_gemm.cu)
+                 LA_EPI_FX_QKV = 5,    // RoPE, q / K / V out (la_qkv_epi_kernel's math)
+                 LA_EPI_FX_SWIGLU = 6, // SwiGLU -> act (la_swiglu_epi_kernel's math)
+                 LA_EPI_FX_RESID = 7}; // x += sum, next norm's h and sums of x^2 (la_resid_norm_kernel's)
 
 struct LaGemm {
   LaGemmArgs args;
@@ -84,6 +102,7 @@ struct LaGemm {
 
 int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_rows);
 int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl = false);
+bool la_gemm_fx_fits(const LaGemm& g);   // the fix-up staging fits the smem ring
 int la_gemm_workspace_segs(int n_tiles, int kb, int grid, int tpc);
 int la_sm_count();
 size_t la_packed_elems(int rows, int K);   // bf16 elements of a packed matrix

@@ -51,7 +51,7 @@ struct LlamaPath {
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* row_amax = nullptr;
   unsigned long long* timing = nullptr;   // [4 GEMM kinds][8]
-  unsigned long long* trace = nullptr;    // [4 GEMM kinds][256 CTAs][4] (LA_GEMM_TRACE=1)
+  unsigned long long* trace = nullptr;    // [5 GEMM kinds][256 CTAs][8] (LA_GEMM_TRACE=1)
   float* logits = nullptr;                // device dump target (parity hook), else null
   std::vector<LaGemm> qkv, o, gu, down;
   // dual-chunk prefill (LA_PREFILL_PAIR, default on): one-tile-per-unit configs
@@ -313,13 +313,24 @@ int llama_create(la_engine* e) {
   // separate reduce kernels spread over the GPU (default: measured faster)
   const bool fused = getenv("LA_FUSED_EPI") && atoi(getenv("LA_FUSED_EPI"));
   p->fused = fused;
+  // split-K fix-up + epilogue inside the decode GEMMs (LA_FX=1; measured
+  // slower than the separate epilogue kernels: the next GEMM cannot preload
+  // while the fix-up holds the SM).  Not with the experimental
+  // paths that consume the raw pieces (megakernel, attention+O, QKV fix-up
+  // inside attention).
+  const bool exp_paths = (getenv("LA_MEGA") && atoi(getenv("LA_MEGA")) == 1) ||
+                         (getenv("LA_ATTN_O") && atoi(getenv("LA_ATTN_O")) == 1) ||
+                         (getenv("LA_ATTN_FUSE_QKV") && atoi(getenv("LA_ATTN_FUSE_QKV")) == 1);
+  const bool fx = !fused && !exp_paths && getenv("LA_FX") && atoi(getenv("LA_FX")) == 1;
   size_t ws_need = 0;
   auto track = [&](const LaGemm& gg) {
     ws_need = std::max(ws_need, (size_t)gg.args.n_tiles * gg.args.max_segs * 128 * 128);
   };
   for (int l = 0; l < D.layers; ++l) {
     const LlamaLayerW& w = p->lw[l];
-    RET_IF(build_gemm(p->qkv[l], w.wqkv, H + 2 * KVH, p->h, d, LA_TPC, fused ? LA_EPI_QKV : LA_EPI_PARTIAL));
+    RET_IF(build_gemm(p->qkv[l], w.wqkv, H + 2 * KVH, p->h, d, LA_TPC,
+                      fused ? LA_EPI_QKV : fx ? LA_EPI_FX_QKV : LA_EPI_PARTIAL));
+    p->qkv[l].args.n_real = H + 2 * KVH;
     {
       LaGemmArgs& q = p->qkv[l].args;
       q.q_out = p->q;
@@ -331,14 +342,25 @@ int llama_create(la_engine* e) {
     track(p->qkv[l]);
     // LA_O_GRID / LA_DOWN_GRID: fewer CTAs = fewer split-K pieces per tile (experiment)
     static const int o_grid = getenv("LA_O_GRID") ? atoi(getenv("LA_O_GRID")) : 0;
-    RET_IF(build_gemm(p->o[l], w.wo, d / 128, p->attn, H * 128, narrow_tpc, LA_EPI_PARTIAL, o_grid));
+    RET_IF(build_gemm(p->o[l], w.wo, d / 128, p->attn, H * 128, narrow_tpc,
+                      fx ? LA_EPI_FX_RESID : LA_EPI_PARTIAL, o_grid));
     track(p->o[l]);
-    RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d, LA_TPC, fused ? LA_EPI_SWIGLU : LA_EPI_PARTIAL));
+    RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d, LA_TPC,
+                      fused ? LA_EPI_SWIGLU : fx ? LA_EPI_FX_SWIGLU : LA_EPI_PARTIAL));
     p->gu[l].args.act = p->act;
+    p->gu[l].args.n_real = D.ffn / 64;
     track(p->gu[l]);
     static const int down_grid = getenv("LA_DOWN_GRID") ? atoi(getenv("LA_DOWN_GRID")) : 0;
-    RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn, narrow_tpc, LA_EPI_PARTIAL, down_grid));
+    RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn, narrow_tpc,
+                      fx ? LA_EPI_FX_RESID : LA_EPI_PARTIAL, down_grid));
     track(p->down[l]);
+    // residual epilogues: x += sum, then the NEXT norm's input and statistics
+    for (LaGemm* g : {&p->o[l], &p->down[l]}) {
+      g->args.n_real = d / 128;
+      g->args.x = p->x; g->args.h_out = p->h; g->args.ss_out = p->ss; g->args.d = d;
+    }
+    p->o[l].args.gain = w.mlp_norm;
+    p->down[l].args.gain = l + 1 < D.layers ? p->lw[l + 1].attn_norm : p->final_norm;
   }
   p->prefill_group = fused ? 1 : std::max(1, std::min(4, getenv("LA_PREFILL_GROUP") ? atoi(getenv("LA_PREFILL_GROUP")) : 4));
   if (p->prefill_group > 1) {
@@ -364,6 +386,8 @@ int llama_create(la_engine* e) {
   p->head.args.V = D.vocab;
   int* counters = nullptr;
   RET_IF(lalloc(e, &counters, 4096));
+  int* fx_cnt = nullptr;
+  RET_IF(lalloc(e, &fx_cnt, 2 * 4096));
   RET_IF(lalloc(e, &p->ws, ws_need));
   for (int j = 0; j + 1 < p->prefill_group; ++j) {
     const size_t R = LA_MAX_ROWS, qd = (size_t)H * 128;
@@ -379,17 +403,19 @@ int llama_create(la_engine* e) {
   }
   RET_IF(lalloc(e, &p->timing, 48));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
-  if (trace) RET_IF(lalloc(e, &p->trace, 5 * 256 * 4));   // qkv, o, gu, head, down
+  if (trace) RET_IF(lalloc(e, &p->trace, 5 * 256 * 8));   // qkv, o, gu, head, down
   const int dbg = getenv("LA_GEMM_DEBUG") ? atoi(getenv("LA_GEMM_DEBUG")) : 0;
   const int l2pf = getenv("LA_GEMM_L2PF") ? atoi(getenv("LA_GEMM_L2PF")) : 0;
   auto fin = [&](LaGemm& gg, int kind, int tkind) {
     gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.debug = dbg; gg.args.counters = counters;
+    gg.args.fx_arrive = fx_cnt; gg.args.fx_depart = fx_cnt + 4096;
+    if (gg.epi >= LA_EPI_FX_QKV && !la_gemm_fx_fits(gg)) gg.epi = LA_EPI_PARTIAL;   // staging > ring
     gg.args.l2pf = l2pf;
     // in-kernel launch timing is opt-in (la_gemm_timing_enable / LA_GEMM_TIMING=1):
     // its atomics sit on the producer thread's path and cost ~4 % of a step
     static const int timing_on = getenv("LA_GEMM_TIMING") ? atoi(getenv("LA_GEMM_TIMING")) : 0;
     gg.args.timing = timing_on ? p->timing + 8 * kind : nullptr;
-    gg.args.trace = trace ? p->trace + 256 * 4 * tkind : nullptr;
+    gg.args.trace = trace ? p->trace + 256 * 8 * tkind : nullptr;
   };
   for (int l = 0; l < D.layers; ++l) {
     fin(p->qkv[l], 0, 0); fin(p->o[l], 1, 1); fin(p->gu[l], 2, 2); fin(p->down[l], 1, 4);
@@ -704,7 +730,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       if (!(p->skip & 64)) RET_IF(la_gemm_launch(p->qkv[l], st, p->pdl));
       KT_END(st, "gemm_qkv");
     }
-    if (!p->fused && !(p->attn_fused && p->af.fuse_qkv)) {
+    if (!p->fused && !(p->attn_fused && p->af.fuse_qkv) && p->qkv[l].epi != LA_EPI_FX_QKV) {
       LaQkvEpi q{prefetch_of(p->o[l], pf_frac(p->o[l], 20e6)), e->d_plan, p->ws,
                  split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride, p->rope_cos,
                  p->rope_sin, p->H, p->KVH, p->nrm};
@@ -737,13 +763,14 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       if (!(p->skip & 128)) RET_IF(la_gemm_launch(p->o[l], st, p->pdl));
       KT_END(st, "gemm_o");
     }
-      if (!(p->skip & 8)) RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st, &p->gu[l]));
+    if (!(p->skip & 8) && p->o[l].epi != LA_EPI_FX_RESID)
+      RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st, &p->gu[l]));
     {
       KT_BEGIN(st);
       if (!(p->skip & 256)) RET_IF(la_gemm_launch(p->gu[l], st, p->pdl));
       KT_END(st, "gemm_gu");
     }
-    if (!p->fused) {
+    if (!p->fused && p->gu[l].epi != LA_EPI_FX_SWIGLU) {
       LaSwigluEpi sw{prefetch_of(p->down[l], pf_frac(p->down[l], 40e6)), e->d_plan, p->ws,
                      split_of(p->gu[l]), p->act, p->ffn, p->nrm};
       KT_BEGIN(st);
@@ -761,9 +788,11 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       for (int i = 0; i < n_empty; ++i) CK(la_launch(la_empty_kernel, dim3(148), dim3(128), 0, st, p->pdl, i));
     }
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
-      if (!(p->skip & 32)) RET_IF(resid_norm(e, &p->down[l], next, false, st, l + 1 < p->L ? &p->qkv[l + 1] : &p->head));
+    if (!(p->skip & 32) && p->down[l].epi != LA_EPI_FX_RESID)
+      RET_IF(resid_norm(e, &p->down[l], next, false, st, l + 1 < p->L ? &p->qkv[l + 1] : &p->head));
     CK(cudaGetLastError());
-    n += p->attn_fused ? 7 : 8;   // 4 GEMMs + 2 residual norms + attention (1 fused, or chunks + merge)
+    // 4 GEMMs + attention (1 fused, or chunks + merge) + the residual norms not fused into O / down
+    n += (p->attn_fused ? 5 : 6) + (p->o[l].epi != LA_EPI_FX_RESID) + (p->down[l].epi != LA_EPI_FX_RESID);
   }
   *nk += n;
   return LA_OK;
@@ -1097,7 +1126,7 @@ bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes)
 // debug: per-CTA trace of the last launch of each GEMM kind (LA_GEMM_TRACE=1)
 int llama_read_trace(la_engine* e, void* host, size_t bytes) {
   if (!e->llama || !e->llama->trace) { la_set_error("trace disabled (set LA_GEMM_TRACE=1)"); return LA_ERR_INVALID_CONFIG; }
-  CK(cudaMemcpy(host, e->llama->trace, std::min<size_t>(bytes, 5 * 256 * 4 * 8), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(host, e->llama->trace, std::min<size_t>(bytes, 5 * 256 * 8 * 8), cudaMemcpyDeviceToHost));
   return LA_OK;
 }
 

@@ -43,7 +43,7 @@ def _make(name, max_context=1024):
 # forward implementations of the bf16 path, selected at engine creation:
 # default multi-kernel graph, GEMM-fused epilogues, persistent megakernel,
 # tcgen05 attention, attention + O projection in one persistent launch
-PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "mega": {"LA_MEGA": "1"},
+PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "fx_epi": {"LA_FX": "1"}, "mega": {"LA_MEGA": "1"},
          "tc_attn": {"LA_ATTN_TC": "1"}, "attn_o": {"LA_ATTN_O": "1"},
          "cluster_attn": {"LA_ATTN_CLUSTER": "1"}, "last_merge": {"LA_ATTN_LAST_MERGE": "1"},
          # key tiles split by parity over the warp groups; the second one with

@@ -91,17 +91,34 @@ def test_large_capacity_pool_memory_is_linear():
     assert len(pool) == cap
 
 
+def _lossless_up_to_near_tie(orc, prompt, ar, toks, rel_tol=1e-2):
+    """toks == ar, or they first differ where the two tokens are the top two
+    of a near tie (oracle top-2 logit margin below rel_tol, the north_star's
+    bf16 tolerance): a lookahead row and the greedy step sum a row's keys over
+    different prefix / step-block splits, so bf16 rounding may flip a tie."""
+    i = next((k for k, (a, b) in enumerate(zip(ar, toks)) if a != b), None)
+    if i is None:
+        return len(ar) == len(toks)
+    seq = list(prompt) + list(ar[:i])
+    lg = orc.logits_rows(seq[:-1], lo.Rows([seq[-1]], [0], [[]], [], []))[0]
+    top2 = set(int(t) for t in np.argsort(lg)[-2:])
+    srt = np.sort(lg)
+    margin = (srt[-1] - srt[-2]) / max(np.abs(lg).max(), 1e-6)
+    return margin < rel_tol and {ar[i], toks[i]} <= top2
+
+
 def test_capped_decode_at_7b_session_scale():
     """The advisor's failing case: a W15 N5 G15 session with a pool cap of a
     few thousand on a 1000-token vocabulary and a 2048-token context now runs;
-    greedy lookahead stays lossless."""
-    from oracle.model_oracle import llama_random_weights
+    greedy lookahead stays lossless (up to a documented near tie)."""
+    from oracle.model_oracle import LlamaOracle, llama_random_weights
     cfg_m = dict(dim=256, layers=2, heads=4, kv_heads=2, head_dim=128, ffn=512, vocab=1000,
                  rope_theta=10000.0, eps=1e-5)
     w = llama_random_weights(cfg_m, seed=3, std=None)
     lc = la.LlamaConfig(dim=256, layers=2, heads=4, kv_heads=2, ffn=512, vocab=1000, head_dim=128,
                         rope_theta=1e4, norm_eps=1e-5)
     m = la.LlamaModel(lc, dtype="bf16", weights=w, max_context=2048)
+    orc = LlamaOracle(cfg_m, w, emulate_bf16=True)
     try:
         prompt = [int(t) for t in np.random.default_rng(5).integers(0, 1000, 600)]
         cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=200,
@@ -110,13 +127,13 @@ def test_capped_decode_at_7b_session_scale():
         for cap in (600, 2500):
             pool = la.NGramPool(5, capacity=cap)
             toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=0), pool=pool)
-            assert toks == ar
+            assert _lossless_up_to_near_tie(orc, prompt, ar, toks)
             assert len(pool) <= cap
             state = la.start_session(m, prompt, cfg, la.SamplerSpec("greedy", seed=0),
                                      pool=la.NGramPool(5, capacity=cap))
             out = []
             while not la.collect_output(out, la.lookahead_step(state).accepted, 200, None):
                 pass
-            assert out == ar
+            assert out == toks      # the session is the same decode
     finally:
         m.close()
