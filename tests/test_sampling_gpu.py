@@ -89,8 +89,13 @@ def test_sampler_errors(tiny):
     # top_k=1 under temperature == greedy (sampling.py:41-42)
     greedy = la.decode_lookahead(tiny, p, cfg, la.SamplerSpec("greedy"))[0]
     assert la.decode_lookahead(tiny, p, cfg, la.SamplerSpec("temperature", top_k=1, seed=5))[0] == greedy
-    with pytest.raises(NotImplementedError):
-        la.decode_lookahead_devices(tiny, p, cfg, la.SamplerSpec("temperature"), 2)
+    # LP with a temperature sampler: the reference defines the LP outcome as
+    # identical to the single-device decode (parallel.py:145-151)
+    spec = la.SamplerSpec("temperature", temperature=0.9, seed=4)
+    single, met1 = la.decode_lookahead(tiny, p, cfg, spec)
+    lp, met2, comm = la.decode_lookahead_devices(tiny, p, cfg, spec, 2)
+    assert lp == single and met2.steps == met1.steps
+    assert comm.sync_events > 0
 
 
 # ----------------------------------------------------------- bf16 path
