@@ -395,6 +395,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                              (uint32_t)n_pad_x[j - 1] * 128, &full[s], pol_x);
         }
       }
+      // every load of this CTA is issued: stream the following GEMMs' first
+      // units into L2 while the kernels between them run
+#pragma unroll 1
+      for (int j = 0; j < 2; ++j) {
+        const LaNextPf& q = args.npf[j];
+        if (!q.a || q.units <= 0) continue;
+        const long Uq = (long)(q.n_tiles / q.tpc) * q.kb, Pq = q.grid;
+        for (long c = blockIdx.x; c < Pq; c += gridDim.x) {
+          const long v0 = c * Uq / Pq, v1 = (c + 1) * Uq / Pq;
+          for (long v = v0 + q.skip; v < min(v1, v0 + q.skip + q.units); ++v) {
+            const char* base = reinterpret_cast<const char*>(q.a);
+            if (q.tpc == LA_TPC) {
+              ptx::bulk_prefetch_l2(base + (size_t)v * kABytes, kABytes);
+            } else {
+              const long t = v / q.kb, k = v % q.kb;
+              ptx::bulk_prefetch_l2(base + ((size_t)((t / LA_TPC) * q.kb + k) * LA_TPC + (t % LA_TPC)) * kTileBytes,
+                                    kTileBytes);
+            }
+          }
+        }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer

@@ -32,6 +32,12 @@ __host__ __device__ __forceinline__ size_t la_act_off(int r, int k) {
   return (size_t)(k >> 6) * 8192 + (size_t)r * 64 + ((((k >> 3) & 7) ^ (r & 7)) << 3) + (k & 7);
 }
 
+struct LaNextPf {
+  const void* a;   // packed weights of a following GEMM (null: none)
+  int n_tiles, kb, tpc, grid;
+  int skip, units;  // per CTA: units [skip, skip + units) of its stream-K range
+};
+
 struct LaGemmArgs {
   const __nv_bfloat16* a;   // packed weight tiles [n_tiles/2][kb][2][128*64]
   const __nv_bfloat16* b;   // packed step rows [kb][128][64]
@@ -85,6 +91,11 @@ struct LaGemmArgs {
   __nv_bfloat16* h_out;              // FX_RESID: next GEMM input bf16(x * gain), packed LA rows
   float* ss_out;                     // FX_RESID: [d/128][128] per-tile sums of x^2
   int d;
+  // ---- cross-GEMM L2 prefetch: after issuing its last weight load, CTA c
+  // pulls the units [skip, skip + units) of CTA c's range in the next GEMMs
+  // into L2, so HBM keeps streaming through the latency-bound kernels that
+  // separate two GEMMs (their data then arrives from L2)
+  LaNextPf npf[2];
 };
 
 enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_LOGITS = 3,

@@ -437,6 +437,26 @@ int llama_create(la_engine* e) {
   }
   p->head.args.nrm = p->nrm;
   fin(p->head, 3, 3);
+  {
+    // cross-GEMM L2 prefetch (LA_NPF=<MB next>[,<MB after next>]): each
+    // decode GEMM, once its own loads are issued, pulls the first units of
+    // the next GEMMs' per-CTA ranges into L2 (the head wraps to layer 0)
+    double mb[2] = {0.0, 0.0};
+    if (const char* s = getenv("LA_NPF")) sscanf(s, "%lf,%lf", &mb[0], &mb[1]);
+    std::vector<LaGemm*> seq;
+    for (int l = 0; l < D.layers; ++l) { seq.push_back(&p->qkv[l]); seq.push_back(&p->o[l]); seq.push_back(&p->gu[l]); seq.push_back(&p->down[l]); }
+    seq.push_back(&p->head);
+    for (size_t i = 0; i < seq.size(); ++i)
+      for (int j = 0; j < 2; ++j) {
+        const LaGemm& nx = *seq[(i + 1 + j) % seq.size()];
+        const double unit = (double)nx.args.tpc * 16384.0;
+        const long per_cta = (long)(nx.args.n_tiles / nx.args.tpc) * nx.args.kb / nx.grid + 1;
+        int units = (int)std::min<double>((double)per_cta, mb[j] * 1e6 / (unit * nx.grid));
+        LaNextPf& q = seq[i]->args.npf[j];
+        q = LaNextPf{nx.args.a, nx.args.n_tiles, nx.args.kb, nx.args.tpc, nx.grid, 0, units};
+        if (units <= 0) q.a = nullptr;
+      }
+  }
   CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
   p->pdl = !(getenv("LA_PDL") && !strcmp(getenv("LA_PDL"), "0"));
   p->skip = getenv("LA_SKIP") ? atoi(getenv("LA_SKIP")) : 0;

@@ -1,0 +1,97 @@
+"""In-graph timeline of one 7B lookahead step (LA_TIMELINE=1, LA_GEMM_TRACE=1).
+
+    python profiles/timeline.py [greedy]
+
+Prints, for the last complete decode step, every kernel's dependency-release
+time (block 0 passing griddepcontrol.wait) and the gap to the next release
+(= that kernel's share of the critical path), summed per kernel kind over the
+step; then the per-CTA trace of the last layer's GEMMs (entry / wait returned /
+last MMA issued / last piece written / exit, µs relative to the first entry).
+"""
+import ctypes as C
+import os
+import sys
+
+os.environ.setdefault("LA_TIMELINE", "1")
+os.environ.setdefault("LA_GEMM_TRACE", "1")
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+import paper_2402_02057_b200 as la  # noqa: E402
+from paper_2402_02057_b200.models import PRESETS  # noqa: E402
+
+preset = os.environ.get("PRESET", "llama2-7b")
+cfgm = PRESETS[preset]
+plen = int(os.environ.get("PLEN", "512"))
+m = la.LlamaModel(cfgm, dtype="bf16", seed=0, max_context=plen + 128)
+prompt = [int(t) for t in np.random.default_rng(0).integers(0, m.vocab_size, plen)]
+greedy = len(sys.argv) > 1 and sys.argv[1] == "greedy"
+steps = int(os.environ.get("STEPS", "6"))
+cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=steps)
+run = (lambda: la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), steps)) if greedy else \
+      (lambda: la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy")))
+run()
+buf = (C.c_uint64 * (1 + 2 * 8192))()
+m.lib.la_debug_read(m.engine(), 18, buf, C.sizeof(buf))   # warm-up records
+C.memset(buf, 0, C.sizeof(buf))
+# reset the device counter by running with a fresh read: the buffer is
+# cumulative, so take the records of the LAST step only
+run()
+m.lib.la_debug_read(m.engine(), 18, buf, C.sizeof(buf))
+n = min(int(buf[0]), 8192)
+recs = [(int(buf[1 + 2 * i]), int(buf[2 + 2 * i])) for i in range(n)]
+recs.sort()
+d, H, KVH, F, V = cfgm.dim, cfgm.heads, cfgm.kv_heads, cfgm.ffn, cfgm.vocab
+
+
+def name(sig):
+    grid, block = sig >> 16, sig & 0xFFFF
+    if block == 192:
+        return "gemm"
+    if block == 256 and grid == (d // 128) * 16:
+        return "resid_norm"
+    if block == 128 and grid == (H + 2 * KVH) * 16:
+        return "qkv_epi"
+    if block == 128 and grid == (F // 64) * 8:
+        return "swiglu_epi"
+    if block == 128 and grid == ((V + 127) // 128) * 16:
+        return "logits_epi"
+    if block == 256:
+        return f"attn[{grid}]"
+    return f"k[{grid}x{block}]"
+
+
+# step boundaries: the K1 build kernel (1 CTA) starts a step
+starts = [i for i in range(len(recs) - 1) if name(recs[i][1]) == "k[1x256]" and name(recs[i + 1][1]) == "resid_norm"]
+seg = recs
+if len(starts) >= 3:
+    seg = recs[starts[-3]:starts[-2] + 1]
+print(f"records {n}; step kernels {len(seg) - 1}; step time {(seg[-1][0] - seg[0][0]) / 1e3:.1f} us")
+tot = {}
+gemm_i = 0
+seq = []
+for (t0, s), (t1, _) in zip(seg, seg[1:]):
+    nm = name(s)
+    if nm == "gemm":
+        nm = ["gemm_qkv", "gemm_o", "gemm_gu", "gemm_down"][gemm_i % 4] if gemm_i < 4 * cfgm.layers else "gemm_head"
+        gemm_i += 1
+    tot[nm] = tot.get(nm, 0.0) + (t1 - t0) / 1e3
+    seq.append((nm, (t1 - t0) / 1e3))
+for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+    print(f"  {k:16s} {v:9.1f} us")
+print("layer 10 sequence:", " ".join(f"{k}:{v:.1f}" for k, v in seq[1 + 9 * 9: 1 + 10 * 9]))
+# per-CTA GEMM traces of the last launch of each kind
+tr = (C.c_uint64 * (5 * 256 * 8))()
+if m.lib.la_debug_read(m.engine(), 5, tr, C.sizeof(tr)) == 0:
+    a = np.frombuffer(tr, dtype=np.uint64).reshape(5, 256, 8).astype(np.int64)
+    for k, nm in enumerate(["qkv", "o", "gu", "head", "down"]):
+        x = a[k]
+        ok = x[:, 0] > 0
+        if not ok.any():
+            continue
+        x = x[ok]
+        base = x[:, 0].min()
+        def q(col):
+            v = (x[:, col] - base) / 1e3
+            return f"{np.min(v):6.2f}/{np.median(v):6.2f}/{np.max(v):6.2f}"
+        print(f"{nm:5s} CTAs {len(x)} (min/med/max us) entry {q(0)} wait {q(1)} mma_done {q(2)} "
+              f"pieces {q(4)} exit {q(3)}")
