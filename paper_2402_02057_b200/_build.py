@@ -40,7 +40,9 @@ def _compile(src: Path, force: bool, hdr_mtime: float, verbose: bool) -> tuple[P
     obj = OBJ / (src.stem + ".o")
     if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime):
         return obj, ""
-    cmd = [NVCC, *ARCH, *CFLAGS, "-I", str(PKG.parent / "include"), "-c", str(src), "-o", str(obj)]
+    # LA_NVCC_DEFS: extra flags for profiling builds (e.g. -DLA_GEMM_UTRACE; use --force)
+    extra = os.environ.get("LA_NVCC_DEFS", "").split()
+    cmd = [NVCC, *ARCH, *CFLAGS, *extra, "-I", str(PKG.parent / "include"), "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

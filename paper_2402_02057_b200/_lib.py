@@ -108,7 +108,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # LA_LIB_PATH: another build of the same ABI (profiling A/B runs)
+    p = Path(path or os.environ.get("LA_LIB_PATH") or LIB_PATH)
     if not p.exists():
         raise RuntimeError(
             f"CUDA library {p} is missing: build it with `python -m paper_2402_02057_b200._build` "

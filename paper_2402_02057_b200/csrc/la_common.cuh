@@ -7,6 +7,10 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -205,10 +209,33 @@ static inline cudaError_t la_smem_attr_once(std::atomic<unsigned>& done, F* kern
   return e;
 }
 
+// Every kernel of the step runs with the max-shared-memory carveout.  An SM
+// whose running CTAs were launched with another L1/smem split cannot host a
+// CTA that needs the larger smem partition until it drains, which defeats
+// programmatic dependent launch: a GEMM behind a 0-smem epilogue kernel could
+// only start (and begin streaming its weights) once the epilogue's CTAs left
+// its SM (profiles/microbench/pdl_preload.cu: 0 of 148 secondary CTAs early
+// with the default carveout, 148 of 148 with max-smem).  Opt-in
+// (LA_CARVEOUT=1): in the decode step it measured +0.8 % -- the epilogue
+// kernels' grids are larger than what fits beside a GEMM CTA anyway, and the
+// GEMM's MMA issue, not its preload, paces its first units.
+static inline void la_carveout_once(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  static const bool on = getenv("LA_CARVEOUT") && atoi(getenv("LA_CARVEOUT")) == 1;
+  if (!on) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.insert({dev, fn}).second)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
+
 // cudaLaunchKernelEx with the PDL attribute (pdl = false: plain launch)
 template <typename... KArgs, typename... Args>
 static inline cudaError_t la_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                                     cudaStream_t st, bool pdl, Args... args) {
+  la_carveout_once(reinterpret_cast<const void*>(kernel));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

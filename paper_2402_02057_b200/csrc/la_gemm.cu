@@ -28,8 +28,9 @@ constexpr int kBBytes = 128 * 128;             // <= 128 rows x 64 bf16
 constexpr int kThreads = 192;
 constexpr int kTmemCols = 512;                 // 2 buffers x LA_TPC tiles x 128 columns
 constexpr int kEpiLd = 33;                     // fused-epilogue staging [128 f][33]
+constexpr int kStageFloats = 4 * 32 * 36;      // >= 128 * kEpiLd: also the pieces' transpose staging
 constexpr size_t kSmemBytes =
-    1024 + kStages * (kABytes + kBBytes) + 128 * kEpiLd * 4 + 2 * kMaxStages * 8 + 5 * 8 + 16 + 128 * 4;
+    1024 + kStages * (kABytes + kBBytes) + kStageFloats * 4 + 2 * kMaxStages * 8 + 5 * 8 + 16 + 128 + 128 * 4;
 
 constexpr bool is_fx(int epi) { return epi >= LA_EPI_FX_QKV && epi <= LA_EPI_FX_RESID; }
 
@@ -268,6 +269,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Per-unit stream trace (LaGemmArgs::utrace): compiled in only with
+// -DLA_GEMM_UTRACE (LA_NVCC_DEFS=-DLA_GEMM_UTRACE python -m ..._build --force):
+// its checks inside the producer / MMA loops cost ~2.5 % of a decode step
+#ifdef LA_GEMM_UTRACE
+#define LA_UT(cond, idx)                                         \
+  do {                                                           \
+    if (args.utrace && (cond)) args.utrace[idx] = globaltimer(); \
+  } while (0)
+#else
+#define LA_UT(cond, idx) \
+  do {                   \
+  } while (0)
+#endif
+
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     la_gemm_kernel(const LaGemmArgs args) {
@@ -279,6 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // one 192 KB ring: nst stages of (weights a_bytes | step rows 16 KB), the
   // weight and row halves in two contiguous regions (1024-B aligned)
   constexpr bool multi = EPI == LA_EPI_MULTI;        // prefill: row blocks per weight stage
+  // decode split-K pieces: accumulate (step rows x weight rows) -- see the MMA issuer
+  constexpr bool nt = EPI == LA_EPI_PARTIAL;
   const int nblk = multi ? args.nblk : 1;
   const int nbuf = nblk > 2 ? 1 : 2;                 // TMEM accumulator buffers
   const int nst = args.nst > 0 ? args.nst : multi ? (nblk > 2 ? 2 : kStages)
@@ -293,8 +310,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* fxbar = tempty + 2;                     // fix-up staging (LA_EPI_FX_*)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 1);
   int* sflag = reinterpret_cast<int*>(tmem_slot + 1);
-  float* sEpi = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
-  float* sRstd = sEpi + 128 * kEpiLd;   // fused epilogues: per-row deferred-norm scale
+  // (pointer + offset, not an integer round trip: keeps the shared address
+  // space visible to the compiler -- STS/LDS instead of generic ST/LD)
+  uint8_t* epi_base = reinterpret_cast<uint8_t*>(tmem_slot) + 16;
+  float* sEpi = reinterpret_cast<float*>(epi_base + ((128 - (ptx::smem_u32(epi_base) & 127)) & 127));
+  float* sRstd = sEpi + kStageFloats;   // fused epilogues: per-row deferred-norm scale
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = args.kb;
@@ -328,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_expect_tx_noarrive(&full[i], a_bytes);
       ptx::bulk_load(sA + i * a_stage, a_src(u_begin + i), a_bytes, &full[i], pol_w);
     }
+    LA_UT(true, (gridDim.x + blockIdx.x) * 32 + 31);
   }
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
@@ -387,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_expect_tx(&full[s], a_bytes + bb);
           ptx::bulk_load(sA + s * a_stage, a_src(u), a_bytes, &full[s], pol_w);
         }
+        LA_UT(it < 24, (gridDim.x + blockIdx.x) * 32 + it);
         if (load_b) {
           ptx::bulk_load(sB + s * b_stage, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
           if constexpr (multi)
@@ -420,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = ptx::umma_idesc_bf16(128, (uint32_t)n_pad);
+      const uint32_t idesc = nt ? ptx::umma_idesc_bf16(128, (uint32_t)(128 * tpc)) : ptx::umma_idesc_bf16(128, (uint32_t)n_pad);
       uint32_t idesc_x[3] = {0u, 0u, 0u};
       if constexpr (multi)
         for (int j = 0; j < 3; ++j) idesc_x[j] = ptx::umma_idesc_bf16(128, (uint32_t)(n_pad_x[j] > 0 ? n_pad_x[j] : 16));
@@ -437,6 +459,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (; u < seg_end; ++u, ++it) {
           const int s = (int)(it % nst);
           ptx::mbar_wait(&full[s], (uint32_t)(it / nst) & 1);
+#ifdef LA_GEMM_UTRACE
+          {   // first 24 units, then the last 8
+            const long nu = u_end - u_begin;
+            const long slot = it < 24 ? it : it >= nu - 8 ? 24 + (it - (nu - 8)) : -1;
+            LA_UT(slot >= 0, blockIdx.x * 32 + slot);
+          }
+#endif
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sA + s * a_stage);
           const uint32_t b_addr = ptx::smem_u32(sB + s * b_stage);
@@ -444,12 +473,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_arrive(&empty[s]);
             continue;
           }
-          for (int tt = 0; tt < tpc; ++tt)
+          if constexpr (nt) {
+            // step rows x weight rows: A = the step rows' k-block (M = 128
+            // lanes; rows >= n_pad hold stale data and are never read back),
+            // B = the unit's tpc contiguous weight tiles (N = 128 tpc), so a
+            // unit is 4 MMAs instead of 4 tpc (the tensor core's per-MMA cost
+            // hardly depends on N at these sizes: profiles/microbench/mma_rate.cu)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kTileBytes + kk * 32),
-                             ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
-                             (u > seg_start || kk > 0) ? 1u : 0u);
+              ptx::umma_bf16(d_tmem, ptx::umma_desc_sw128(b_addr + kk * 32), ptx::umma_desc_sw128(a_addr + kk * 32),
+                             idesc, (u > seg_start || kk > 0) ? 1u : 0u);
+          } else {
+            for (int tt = 0; tt < tpc; ++tt)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                ptx::umma_bf16(d_tmem + tt * 128, ptx::umma_desc_sw128(a_addr + tt * kTileBytes + kk * 32),
+                               ptx::umma_desc_sw128(b_addr + kk * 32), idesc,
+                               (u > seg_start || kk > 0) ? 1u : 0u);
+          }
           if constexpr (multi)
           for (int j = 1; j < nblk; ++j)   // row block j into columns [128 j, 128 j + 128)
 #pragma unroll
@@ -458,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              ptx::umma_desc_sw128(b_addr + j * kBBytes + kk * 32), idesc_x[j - 1],
                              (u > seg_start || kk > 0) ? 1u : 0u);
           ptx::umma_commit(&empty[s]);
+          LA_UT(it < 24, (2 * gridDim.x + blockIdx.x) * 32 + it);
         }
         ptx::umma_commit(&tfull[buf]);
         use[buf]++;
@@ -479,7 +521,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int seg = (int)(blockIdx.x - c_first);
       ptx::mbar_wait(&tfull[buf], use[buf] & 1);
       ptx::tc_fence_after();
-      if (EPI == LA_EPI_PARTIAL || multi || is_fx(EPI) || seg != 0) {
+#ifdef LA_GEMM_UTRACE
+      const int dseg = use[0] + use[1];
+#endif
+      LA_UT(et == 128 - 64 && dseg < 4, (2 * gridDim.x + blockIdx.x) * 32 + 24 + 2 * dseg);   // warp 4: drain start
+      if constexpr (nt) {
+        // lane = step row, columns = the unit's 128 tpc features: each thread
+        // writes its row's 32-feature runs (128 B) of the piece
+        const int q4 = warp & 3;   // lanes 32 q4 .. 32 q4 + 31 = step rows
+        if (32 * q4 < n_rows) {
+          // transpose each 32 x 32 block through the warp's smem slice so a
+          // store instruction writes one row's 32 features (128 B, coalesced)
+          // (rows 36 floats apart: 16-B aligned, conflict-free float4 writes
+          // and reads); a store instruction then covers 4 rows x 128 B
+          float* tw = sEpi + q4 * 32 * 36;
+          const int rr = lane >> 3, cc = (lane & 7) * 4;
+          for (int tt = 0; tt < tpc; ++tt) {
+            float* wsp = args.ws + ((size_t)(tile * tpc + tt) * args.max_segs + seg) * 128 * 128;
+            const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * (LA_TPC * 128) + tt * 128;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              const int c0 = 32 * c;
+              uint32_t v[32];
+              ptx::tmem_ld32_nowait(t_base + c0, v);
+              ptx::tmem_wait_ld();
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                *reinterpret_cast<uint4*>(tw + lane * 36 + 4 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              __syncwarp();
+#pragma unroll
+              for (int p = 0; p < 8; ++p) {
+                const int i = 4 * p + rr;
+                const int row = 32 * q4 + i;
+                if (row < n_rows && !(args.debug & 4))
+                  __stcg(reinterpret_cast<float4*>(wsp + (size_t)row * 128 + c0 + cc),
+                         *reinterpret_cast<const float4*>(tw + i * 36 + cc));
+              }
+              __syncwarp();
+            }
+          }
+        }
+        LA_UT(et == 128 - 64 && dseg < 4, (2 * gridDim.x + blockIdx.x) * 32 + 25 + 2 * dseg);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[buf]);
+      } else if (EPI == LA_EPI_PARTIAL_SW || multi || is_fx(EPI) || seg != 0) {
         // write this piece's fp32 partial (multi-chunk mode: every row block)
         const int nout = multi ? nblk : tpc;
         for (int tt = 0; tt < nout; ++tt) {
@@ -496,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
           }
         }
+        LA_UT(et == 128 - 64 && dseg < 4, (2 * gridDim.x + blockIdx.x) * 32 + 25 + 2 * dseg);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[buf]);
         if constexpr (is_fx(EPI)) {
@@ -503,12 +589,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           __threadfence();
           ptx::named_bar_sync(1, 128);
           if (et == 0) atomicAdd(args.fx_arrive + tile, 1);
-        } else if (EPI != LA_EPI_PARTIAL && !multi) {
+        } else if (EPI != LA_EPI_PARTIAL_SW && !multi) {
           __threadfence();
           ptx::named_bar_sync(1, 128);
           if (et == 0) atomicAdd(args.counters + tile, 1);
         }
-      } else if constexpr (EPI != LA_EPI_PARTIAL && EPI != LA_EPI_MULTI && !is_fx(EPI)) {
+      } else if constexpr (EPI != LA_EPI_PARTIAL_SW && EPI != LA_EPI_MULTI && !is_fx(EPI)) {
         // owner of the tile's k = 0 piece: wait for the other pieces, sum them
         // in piece order onto the accumulator, apply the fused epilogue
         const int nseg = (int)(la_cta_of((long)(tile + 1) * kb - 1, U, Pn) - c_first + 1);
@@ -599,6 +685,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (args.trace && et == 0) args.trace[blockIdx.x * 8 + 7] = globaltimer();
     }
+  }
+  if (args.trace && !is_fx(EPI)) {   // which role reaches the final barrier last
+    if (threadIdx.x == 0) args.trace[blockIdx.x * 8 + 6] = globaltimer();
+    if (threadIdx.x == 96) args.trace[blockIdx.x * 8 + 7] = globaltimer();
   }
   __syncthreads();
   if (warp == 1) {
@@ -705,7 +795,7 @@ static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
                                                          : (g.args.tpc == LA_TPC ? kStages : kMaxStages);
   const size_t smem = 1024 + (size_t)nst * (g.args.tpc * kTileBytes + nblk * kBBytes) + 2 * kMaxStages * 8 +
                       5 * 8 + 16 +
-                      (EPI == LA_EPI_PARTIAL || EPI == LA_EPI_MULTI || is_fx(EPI) ? 0 : 128 * kEpiLd * 4 + 128 * 4);
+                      (EPI == LA_EPI_MULTI || EPI == LA_EPI_PARTIAL_SW || is_fx(EPI) ? 0 : 128 + kStageFloats * 4 + 128 * 4);
   return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
 }
 
@@ -718,6 +808,7 @@ int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {
     case LA_EPI_FX_QKV: e = launch_epi<LA_EPI_FX_QKV>(g, st, pdl); break;
     case LA_EPI_FX_SWIGLU: e = launch_epi<LA_EPI_FX_SWIGLU>(g, st, pdl); break;
     case LA_EPI_FX_RESID: e = launch_epi<LA_EPI_FX_RESID>(g, st, pdl); break;
+    case LA_EPI_PARTIAL_SW: e = launch_epi<LA_EPI_PARTIAL_SW>(g, st, pdl); break;
     default: e = g.args.nblk > 1 ? launch_epi<LA_EPI_MULTI>(g, st, pdl) : launch_epi<LA_EPI_PARTIAL>(g, st, pdl); break;
   }
   if (e == cudaSuccess) e = cudaGetLastError();

@@ -52,6 +52,9 @@ struct LaGemmArgs {
   unsigned long long* timing;
   // optional per-CTA trace [gridDim][4]: start, prologue done, MMA done, end
   unsigned long long* trace;
+  // optional per-CTA unit trace [gridDim][32]: when the MMA thread saw unit
+  // i's stage full (i < 32), to read the weight stream's ramp
+  unsigned long long* utrace;
   int debug;   // experiments: bit0 skip step-row loads, bit1 skip MMAs
   int l2pf;    // units beyond the smem ring prefetched to L2 before the dependency wait
   int nst;     // smem ring stages (0: the default for tpc); fewer stages = a smaller CTA
@@ -103,7 +106,11 @@ enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_L
                  // split-K fix-up + epilogue in the GEMM (decode step; la_gemm.cu)
                  LA_EPI_FX_QKV = 5,    // RoPE, q / K / V out (la_qkv_epi_kernel's math)
                  LA_EPI_FX_SWIGLU = 6, // SwiGLU -> act (la_swiglu_epi_kernel's math)
-                 LA_EPI_FX_RESID = 7}; // x += sum, next norm's h and sums of x^2 (la_resid_norm_kernel's)
+                 LA_EPI_FX_RESID = 7,  // x += sum, next norm's h and sums of x^2 (la_resid_norm_kernel's)
+                 // split-K pieces accumulated swap-AB (weight rows x step rows,
+                 // N = padded rows; LA_GEMM_NT=0) instead of the default
+                 // (step rows x weight rows, N = 128 tpc)
+                 LA_EPI_PARTIAL_SW = 8};
 
 struct LaGemm {
   LaGemmArgs args;

@@ -52,6 +52,7 @@ struct LlamaPath {
   int* row_amax = nullptr;
   unsigned long long* timing = nullptr;   // [4 GEMM kinds][8]
   unsigned long long* trace = nullptr;    // [5 GEMM kinds][256 CTAs][8] (LA_GEMM_TRACE=1)
+  unsigned long long* utrace = nullptr;   // [5][256][32] unit arrival times (LA_GEMM_TRACE=2)
   float* logits = nullptr;                // device dump target (parity hook), else null
   std::vector<LaGemm> qkv, o, gu, down;
   // dual-chunk prefill (LA_PREFILL_PAIR, default on): one-tile-per-unit configs
@@ -404,18 +405,25 @@ int llama_create(la_engine* e) {
   RET_IF(lalloc(e, &p->timing, 48));
   const bool trace = getenv("LA_GEMM_TRACE") != nullptr;
   if (trace) RET_IF(lalloc(e, &p->trace, 5 * 256 * 8));   // qkv, o, gu, head, down
+  if (trace && atoi(getenv("LA_GEMM_TRACE")) == 2) RET_IF(lalloc(e, &p->utrace, 5 * 3 * 256 * 32));
   const int dbg = getenv("LA_GEMM_DEBUG") ? atoi(getenv("LA_GEMM_DEBUG")) : 0;
   const int l2pf = getenv("LA_GEMM_L2PF") ? atoi(getenv("LA_GEMM_L2PF")) : 0;
   auto fin = [&](LaGemm& gg, int kind, int tkind) {
     gg.args.plan = e->d_plan; gg.args.ws = p->ws; gg.args.debug = dbg; gg.args.counters = counters;
     gg.args.fx_arrive = fx_cnt; gg.args.fx_depart = fx_cnt + 4096;
-    if (gg.epi >= LA_EPI_FX_QKV && !la_gemm_fx_fits(gg)) gg.epi = LA_EPI_PARTIAL;   // staging > ring
+    if (gg.epi >= LA_EPI_FX_QKV && gg.epi <= LA_EPI_FX_RESID && !la_gemm_fx_fits(gg)) gg.epi = LA_EPI_PARTIAL;   // staging > ring
+    // split-K pieces accumulated swap-AB (default) or as (step rows x weight
+    // rows) with LA_GEMM_NT=1 (4x fewer MMAs per unit, but its TMEM drain
+    // runs on half the lanes' warps at <= 64 rows; measured slower)
+    static const bool nt = getenv("LA_GEMM_NT") && atoi(getenv("LA_GEMM_NT")) == 1;
+    if (!nt && gg.epi == LA_EPI_PARTIAL) gg.epi = LA_EPI_PARTIAL_SW;
     gg.args.l2pf = l2pf;
     // in-kernel launch timing is opt-in (la_gemm_timing_enable / LA_GEMM_TIMING=1):
     // its atomics sit on the producer thread's path and cost ~4 % of a step
     static const int timing_on = getenv("LA_GEMM_TIMING") ? atoi(getenv("LA_GEMM_TIMING")) : 0;
     gg.args.timing = timing_on ? p->timing + 8 * kind : nullptr;
     gg.args.trace = trace ? p->trace + 256 * 8 * tkind : nullptr;
+    gg.args.utrace = p->utrace ? p->utrace + 3 * 256 * 32 * tkind : nullptr;
   };
   for (int l = 0; l < D.layers; ++l) {
     fin(p->qkv[l], 0, 0); fin(p->o[l], 1, 1); fin(p->gu[l], 2, 2); fin(p->down[l], 1, 4);
@@ -453,7 +461,13 @@ int llama_create(la_engine* e) {
         const long per_cta = (long)(nx.args.n_tiles / nx.args.tpc) * nx.args.kb / nx.grid + 1;
         int units = (int)std::min<double>((double)per_cta, mb[j] * 1e6 / (unit * nx.grid));
         LaNextPf& q = seq[i]->args.npf[j];
-        q = LaNextPf{nx.args.a, nx.args.n_tiles, nx.args.kb, nx.args.tpc, nx.grid, 0, units};
+        // skip what the next GEMM's own smem ring pre-loads during its early
+        // (PDL) launch -- except the O projection, which cannot become
+        // resident beside attention
+        static const int skip_env = getenv("LA_NPF_SKIP") ? atoi(getenv("LA_NPF_SKIP")) : -1;
+        const bool is_o = (i + 1 + j) % 4 == 1 && (i + 1 + j) < seq.size() - 1;
+        const int skip = skip_env >= 0 ? skip_env : (!is_o ? (nx.args.tpc == LA_TPC ? 4 : 6) : 0);
+        q = LaNextPf{nx.args.a, nx.args.n_tiles, nx.args.kb, nx.args.tpc, nx.grid, skip, units};
         if (units <= 0) q.a = nullptr;
       }
   }
@@ -730,7 +744,8 @@ static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool emb
   r.embed = embed ? p->embed : nullptr;
   r.x = p->x; r.g = g; r.h = p->h; r.d = p->d; r.eps = p->eps; r.ss = p->ss;
   KT_BEGIN(st);
-  CK(la_launch(la_resid_norm_kernel, dim3(p->d / 128, LA_MAX_ROWS / 8), dim3(256), 0, st, p->pdl, r));
+  static const int rb = getenv("LA_RESID_RB") ? atoi(getenv("LA_RESID_RB")) : LA_MAX_ROWS / 8;
+  CK(la_launch(la_resid_norm_kernel, dim3(p->d / 128, rb), dim3(256), 0, st, p->pdl, r));
   KT_END(st, from ? "resid_norm" : "embed_norm");
   CK(cudaGetLastError());
   return LA_OK;
@@ -755,7 +770,10 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
                  split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride, p->rope_cos,
                  p->rope_sin, p->H, p->KVH, p->nrm};
       KT_BEGIN(st);
-      if (!(p->skip & 1)) CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
+      if (!(p->skip & 1)) {
+        static const int rb = getenv("LA_QKV_RB") ? atoi(getenv("LA_QKV_RB")) : LA_MAX_ROWS / 8;
+        CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, rb), dim3(128), 0, st, p->pdl, q));
+      }
       KT_END(st, "qkv_epi");
       ++n;
     }
@@ -794,7 +812,10 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       LaSwigluEpi sw{prefetch_of(p->down[l], pf_frac(p->down[l], 40e6)), e->d_plan, p->ws,
                      split_of(p->gu[l]), p->act, p->ffn, p->nrm};
       KT_BEGIN(st);
-      if (!(p->skip & 16)) CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 16), dim3(128), 0, st, p->pdl, sw));
+      if (!(p->skip & 16)) {
+        static const int rb = getenv("LA_SWIGLU_RB") ? atoi(getenv("LA_SWIGLU_RB")) : LA_MAX_ROWS / 16;
+        CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, rb), dim3(128), 0, st, p->pdl, sw));
+      }
       KT_END(st, "swiglu_epi");
       ++n;
     }
@@ -885,7 +906,8 @@ static int prefill_chunks(la_engine* e, const int* d_tokens, int start, int n_ch
     r.sp = from ? split_of(*from) : LaSplit{2, 1, 1, 1, 1};
     r.embed = embed ? p->embed : nullptr;
     r.x = c[i].x; r.g = g; r.h = c[i].h; r.d = p->d; r.eps = p->eps; r.ss = c[i].ss;
-    CK(la_launch(la_resid_norm_kernel, dim3(p->d / 128, LA_MAX_ROWS / 8), dim3(256), 0, st, p->pdl, r));
+    static const int rb = getenv("LA_RESID_RB") ? atoi(getenv("LA_RESID_RB")) : LA_MAX_ROWS / 8;
+  CK(la_launch(la_resid_norm_kernel, dim3(p->d / 128, rb), dim3(256), 0, st, p->pdl, r));
     return LA_OK;
   };
   auto multi = [&](const LaGemm& g0, __nv_bfloat16* Chunk::*b) -> int {
@@ -906,7 +928,10 @@ static int prefill_chunks(la_engine* e, const int* d_tokens, int start, int n_ch
     for (int i = 0; i < n_chunks; ++i) {
       LaQkvEpi q{LaPrefetch{}, c[i].plan, c[i].ws, split_of(p->qkv1[l]), c[i].q, kc + l * lstride,
                  vc + l * lstride, p->rope_cos, p->rope_sin, p->H, p->KVH, nrm(i)};
-      CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, q));
+      {
+        static const int rb = getenv("LA_QKV_RB") ? atoi(getenv("LA_QKV_RB")) : LA_MAX_ROWS / 8;
+        CK(la_launch(la_qkv_epi_kernel, dim3(p->H + 2 * p->KVH, rb), dim3(128), 0, st, p->pdl, q));
+      }
     }
     for (int i = 0; i < n_chunks; ++i) {
       LaAttnFusedArgs a = p->af;
@@ -922,7 +947,10 @@ static int prefill_chunks(la_engine* e, const int* d_tokens, int start, int n_ch
     RET_IF(multi(p->gu1[l], &Chunk::h));
     for (int i = 0; i < n_chunks; ++i) {
       LaSwigluEpi sw{LaPrefetch{}, c[i].plan, c[i].ws, split_of(p->gu1[l]), c[i].act, p->ffn, nrm(i)};
-      CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, LA_MAX_ROWS / 16), dim3(128), 0, st, p->pdl, sw));
+      {
+        static const int rb = getenv("LA_SWIGLU_RB") ? atoi(getenv("LA_SWIGLU_RB")) : LA_MAX_ROWS / 16;
+        CK(la_launch(la_swiglu_epi_kernel, dim3(p->ffn / 64, rb), dim3(128), 0, st, p->pdl, sw));
+      }
     }
     RET_IF(multi(p->down1[l], &Chunk::act));
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
@@ -1138,6 +1166,7 @@ bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes)
     case 15: *src = p->row_amax; *bytes = R * 4; return true;
     case 17: *src = p->af.trace; *bytes = (size_t)p->KVH * p->af.nrb_max * (p->af.S + 1) * 64; return p->af.trace != nullptr;
     case 18: *src = g_tl_buf; *bytes = (1 + 2 * LA_TL_CAP) * 8; return g_tl_buf != nullptr;
+    case 20: *src = p->utrace; *bytes = 5 * 3 * 256 * 32 * 8; return p->utrace != nullptr;
     case 16: *src = a.trace; *bytes = (size_t)la_sm_count() * a.trace_slots * 64; return a.trace != nullptr;
     default: return false;
   }

@@ -37,11 +37,11 @@ int main(int argc, char** argv) {
     const int kb = s.K / 64;
     const size_t wbytes = (size_t)s.tiles * kb * 16384;
     // 4 copies of the matrix (> L2) so every launch streams from HBM
-    const int ncopy = 4;
+    const int ncopy = argc > 2 ? atoi(argv[2]) : 4;   // 1: the same matrix every launch (L2-resident when it fits)
     void* w;
     cudaMalloc(&w, wbytes * ncopy);
     cudaMemset(w, 0, wbytes * ncopy);
-    LaGemm g[ncopy];
+    LaGemm g[8];
     const int grid = sms;
     const int segs = la_gemm_workspace_segs(s.tiles, kb, grid, s.tpc);
     float* ws;
@@ -55,7 +55,10 @@ int main(int argc, char** argv) {
       g[c].args.n_tiles = s.tiles; g[c].args.tpc = s.tpc; g[c].args.kb = kb; g[c].args.max_segs = segs;
       g[c].args.plan = dp; g[c].args.ws = ws;
     }
-    for (int pdl = 0; pdl < 2; ++pdl) {
+    const int dbgs[] = {0, 1, 2, 3};
+    for (int di = 0; di < 5; ++di) {
+      const int pdl = di == 0 ? 0 : 1, dbg = di == 0 ? 0 : dbgs[di - 1];
+      for (int c = 0; c < ncopy; ++c) g[c].args.debug = dbg;
       for (int i = 0; i < 8; ++i) la_gemm_launch(g[i % ncopy], st, pdl);
       const int n = 40;
       cudaEventRecord(a, st);
@@ -65,8 +68,28 @@ int main(int argc, char** argv) {
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       const double us = ms * 1e3 / n;
-      printf("%-5s rows %3d  %6.1f MB  pdl %d  %7.2f us/launch  %7.1f GB/s\n", s.name, rows, wbytes / 1e6, pdl, us,
-             wbytes / (us * 1e-6) / 1e9);
+      printf("%-5s rows %3d  %6.1f MB  pdl %d  dbg %d (1: no B loads, 2: no MMAs)  %7.2f us/launch  %7.1f GB/s\n", s.name,
+             rows, wbytes / 1e6, pdl, dbg, us, wbytes / (us * 1e-6) / 1e9);
+    }
+    {
+      // unit-arrival cadence of one more launch (utrace: MMA thread passing
+      // each unit's full barrier), pdl 1, no debug flags
+      unsigned long long* ut;
+      cudaMalloc(&ut, 256 * 32 * 8);
+      cudaMemset(ut, 0, 256 * 32 * 8);
+      for (int c = 0; c < ncopy; ++c) { g[c].args.debug = 0; g[c].args.utrace = ut; }
+      la_gemm_launch(g[0], st, true);
+      cudaStreamSynchronize(st);
+      unsigned long long h[148 * 32];
+      cudaMemcpy(h, ut, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("  cadence (CTA 0..3, us after unit 0):");
+      for (int c = 0; c < 4; ++c) {
+        printf(" |");
+        for (int i = 1; i < 8; ++i) if (h[c * 32 + i]) printf(" %.2f", (h[c * 32 + i] - h[c * 32]) / 1e3);
+      }
+      printf("\n");
+      for (int c = 0; c < ncopy; ++c) g[c].args.utrace = nullptr;
+      cudaFree(ut);
     }
     cudaFree(w);
     cudaFree(ws);
