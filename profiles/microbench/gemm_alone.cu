@@ -6,6 +6,7 @@
 //        -I ../../paper_2402_02057_b200/csrc gemm_alone.cu -L ../../paper_2402_02057_b200/lib \
 //        -llookahead_b200 -o gemm_alone
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -48,7 +49,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&ws, (size_t)s.tiles * segs * 128 * 128 * 4);
     for (int c = 0; c < ncopy; ++c) {
       memset(&g[c], 0, sizeof(LaGemm));
-      g[c].epi = LA_EPI_PARTIAL;
+      g[c].epi = getenv("NT") && atoi(getenv("NT")) ? LA_EPI_PARTIAL : LA_EPI_PARTIAL_SW;
       g[c].grid = grid;
       g[c].args.a = reinterpret_cast<const __nv_bfloat16*>((char*)w + c * wbytes);
       g[c].args.b = reinterpret_cast<const __nv_bfloat16*>(act);
