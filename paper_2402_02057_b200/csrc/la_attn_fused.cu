@@ -1008,8 +1008,9 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
   const int nqb = min(128, nq - rb * 128);
   const bool conc = nqb <= 64;
 
-  uint8_t* smem = TMA ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
-                      : smem_raw;
+  // 1024-B alignment for the SW128 TMA boxes by pointer + offset (an integer
+  // round trip hides the shared address space: generic LD/ST for every access)
+  uint8_t* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
   uint8_t* sKV = smem;
   uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + kKsMaskOff);   // [128][4]
   int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
