@@ -586,13 +586,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive(&tempty[buf]);
         if constexpr (is_fx(EPI)) {
           // this piece is complete: count it in for the unit tile's fix-up
-          __threadfence();
+          // (one cumulative fence by the signalling thread after the barrier;
+          // a fence per thread stalls the drain -- and so the MMAs -- mid-stream)
           ptx::named_bar_sync(1, 128);
-          if (et == 0) atomicAdd(args.fx_arrive + tile, 1);
+          if (et == 0) {
+            __threadfence();
+            atomicAdd(args.fx_arrive + tile, 1);
+          }
         } else if (EPI != LA_EPI_PARTIAL_SW && !multi) {
-          __threadfence();
           ptx::named_bar_sync(1, 128);
-          if (et == 0) atomicAdd(args.counters + tile, 1);
+          if (et == 0) {
+            __threadfence();
+            atomicAdd(args.counters + tile, 1);
+          }
         }
       } else if constexpr (EPI != LA_EPI_PARTIAL_SW && EPI != LA_EPI_MULTI && !is_fx(EPI)) {
         // owner of the tile's k = 0 piece: wait for the other pieces, sum them

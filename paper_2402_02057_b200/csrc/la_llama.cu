@@ -322,7 +322,10 @@ int llama_create(la_engine* e) {
   const bool exp_paths = (getenv("LA_MEGA") && atoi(getenv("LA_MEGA")) == 1) ||
                          (getenv("LA_ATTN_O") && atoi(getenv("LA_ATTN_O")) == 1) ||
                          (getenv("LA_ATTN_FUSE_QKV") && atoi(getenv("LA_ATTN_FUSE_QKV")) == 1);
-  const bool fx = !fused && !exp_paths && getenv("LA_FX") && atoi(getenv("LA_FX")) == 1;
+  const bool fx_on = !fused && !exp_paths && getenv("LA_FX") && atoi(getenv("LA_FX")) == 1;
+  // LA_FX_MASK (with LA_FX=1): which GEMMs fix up in-kernel -- bit 0 QKV,
+  // 1 O (residual), 2 gate/up (SwiGLU), 3 down (residual); default all
+  const int fx_mask = fx_on ? (getenv("LA_FX_MASK") ? atoi(getenv("LA_FX_MASK")) : 15) : 0;
   size_t ws_need = 0;
   auto track = [&](const LaGemm& gg) {
     ws_need = std::max(ws_need, (size_t)gg.args.n_tiles * gg.args.max_segs * 128 * 128);
@@ -330,7 +333,7 @@ int llama_create(la_engine* e) {
   for (int l = 0; l < D.layers; ++l) {
     const LlamaLayerW& w = p->lw[l];
     RET_IF(build_gemm(p->qkv[l], w.wqkv, H + 2 * KVH, p->h, d, LA_TPC,
-                      fused ? LA_EPI_QKV : fx ? LA_EPI_FX_QKV : LA_EPI_PARTIAL));
+                      fused ? LA_EPI_QKV : (fx_mask & 1) ? LA_EPI_FX_QKV : LA_EPI_PARTIAL));
     p->qkv[l].args.n_real = H + 2 * KVH;
     {
       LaGemmArgs& q = p->qkv[l].args;
@@ -344,16 +347,16 @@ int llama_create(la_engine* e) {
     // LA_O_GRID / LA_DOWN_GRID: fewer CTAs = fewer split-K pieces per tile (experiment)
     static const int o_grid = getenv("LA_O_GRID") ? atoi(getenv("LA_O_GRID")) : 0;
     RET_IF(build_gemm(p->o[l], w.wo, d / 128, p->attn, H * 128, narrow_tpc,
-                      fx ? LA_EPI_FX_RESID : LA_EPI_PARTIAL, o_grid));
+                      (fx_mask & 2) ? LA_EPI_FX_RESID : LA_EPI_PARTIAL, o_grid));
     track(p->o[l]);
     RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d, LA_TPC,
-                      fused ? LA_EPI_SWIGLU : fx ? LA_EPI_FX_SWIGLU : LA_EPI_PARTIAL));
+                      fused ? LA_EPI_SWIGLU : (fx_mask & 4) ? LA_EPI_FX_SWIGLU : LA_EPI_PARTIAL));
     p->gu[l].args.act = p->act;
     p->gu[l].args.n_real = D.ffn / 64;
     track(p->gu[l]);
     static const int down_grid = getenv("LA_DOWN_GRID") ? atoi(getenv("LA_DOWN_GRID")) : 0;
     RET_IF(build_gemm(p->down[l], w.wd, d / 128, p->act, D.ffn, narrow_tpc,
-                      fx ? LA_EPI_FX_RESID : LA_EPI_PARTIAL, down_grid));
+                      (fx_mask & 8) ? LA_EPI_FX_RESID : LA_EPI_PARTIAL, down_grid));
     track(p->down[l]);
     // residual epilogues: x += sum, then the NEXT norm's input and statistics
     for (LaGemm* g : {&p->o[l], &p->down[l]}) {
