@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 print(f"== {o.name}\n{log}")
     newest = max(o.stat().st_mtime for o in objs)
     if force or not LIB.exists() or LIB.stat().st_mtime < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-ldl"]
+        cmd = [NVCC, *ARCH, "-shared", "-Xlinker", "--no-undefined", "-o", str(LIB), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

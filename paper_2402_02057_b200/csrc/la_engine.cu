@@ -119,6 +119,10 @@ static int check_desc(const la_model_desc* d) {
   }
   if (d->arch == LA_ARCH_GPT_F32 && (d->dim % 2)) { la_set_error("dim must be even"); return LA_ERR_INVALID_CONFIG; }
   if (d->arch != LA_ARCH_GPT_F32 && (d->head_dim % 2)) { la_set_error("head_dim must be even"); return LA_ERR_INVALID_CONFIG; }
+  if (d->arch != LA_ARCH_LLAMA_BF16 && d->head_dim > TINY_MAX_HD) {
+    la_set_error("fp32 SIMT path supports head_dim <= %d", TINY_MAX_HD);
+    return LA_ERR_UNSUPPORTED;
+  }
   int elt = d->arch == LA_ARCH_LLAMA_BF16 ? 2 : 4;
   if ((d->kv_heads * d->head_dim * elt) % 16) {
     la_set_error("kv_heads*head_dim*%d must be a multiple of 16 bytes", elt);
@@ -184,6 +188,39 @@ static int tiny_setup(la_engine* e) {
     CK(cudaMemcpy(ds, s.data(), s.size() * 4, cudaMemcpyHostToDevice));
     m.rope_cos = dc; m.rope_sin = ds;
   }
+  {
+    // transposed weight copies ([in][out]) for coalesced reads in la_tiny.cu
+    const int qd = m.H * m.hd, kvd = m.KVH * m.hd, nqkv = qd + 2 * kvd;
+    auto tr = [&](const float* src, int rows, int cols, float* dst, int ld, int off) -> int {
+      la_tiny_transpose<<<64, 256>>>(src, rows, cols, dst, ld, off);
+      CK(cudaGetLastError());
+      return LA_OK;
+    };
+    for (int l = 0; l < m.L; ++l) {
+      TinyLayer& L = m.layers[l];
+      float *qkv, *o, *w1, *w2, *wu = nullptr;
+      RET_IF(dalloc(e, &qkv, (size_t)m.d * nqkv));
+      RET_IF(dalloc(e, &o, (size_t)qd * m.d));
+      RET_IF(dalloc(e, &w1, (size_t)m.d * m.ff));
+      RET_IF(dalloc(e, &w2, (size_t)m.ff * m.d));
+      RET_IF(tr(L.wq, qd, m.d, qkv, nqkv, 0));
+      RET_IF(tr(L.wk, kvd, m.d, qkv, nqkv, qd));
+      RET_IF(tr(L.wv, kvd, m.d, qkv, nqkv, qd + kvd));
+      RET_IF(tr(L.wo, m.d, qd, o, m.d, 0));
+      RET_IF(tr(L.w1, m.ff, m.d, w1, m.ff, 0));
+      RET_IF(tr(L.w2, m.d, m.ff, w2, m.d, 0));
+      if (L.wu) {
+        RET_IF(dalloc(e, &wu, (size_t)m.d * m.ff));
+        RET_IF(tr(L.wu, m.ff, m.d, wu, m.ff, 0));
+      }
+      L.wqkvT = qkv; L.woT = o; L.w1T = w1; L.w2T = w2; L.wuT = wu;
+    }
+    float* ut;
+    RET_IF(dalloc(e, &ut, (size_t)m.d * m.V));
+    RET_IF(tr(m.unembed, m.V, m.d, ut, m.V, 0));
+    m.unembedT = ut;
+    CK(cudaDeviceSynchronize());
+  }
   m.kcache = reinterpret_cast<float*>(e->kc);
   m.vcache = reinterpret_cast<float*>(e->vc);
   TinyScratch& s = e->ts;
@@ -194,9 +231,13 @@ static int tiny_setup(la_engine* e) {
   RET_IF(dalloc(e, &s.q, (size_t)R * qd));
   RET_IF(dalloc(e, &s.att, (size_t)R * qd));
   RET_IF(dalloc(e, &s.ff, (size_t)R * d.ffn));
-  s.max_keys = e->slots + 1;
-  RET_IF(dalloc(e, &s.scores, (size_t)R * d.heads * s.max_keys));
   RET_IF(dalloc(e, &s.row_amax, R));
+  e->tiny_smem = la_tiny_smem_bytes(m);
+  s.smem = e->tiny_smem > 0 ? 1 : 0;
+  if (e->tiny_smem && la_tiny_set_smem(e->tiny_smem) != 0) {
+    la_set_error("fp32 path: dynamic shared memory attribute (%zu B) refused", e->tiny_smem);
+    return LA_ERR_CUDA;
+  }
   return LA_OK;
 }
 
@@ -453,7 +494,7 @@ static int setup_decode(la_engine* e, const DecodeArgs& a, const la_decode_io* i
 static int prefill(la_engine* e, int n, cudaStream_t st) {
   if (n <= 0) return LA_OK;
   if (e->is_tiny()) {
-    la_tiny_prefill<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_tokens, n);
+    la_tiny_prefill<<<1, TINY_THREADS, e->tiny_smem, st>>>(e->tm, e->ts, e->d_plan, e->d_tokens, n);
     CK(cudaGetLastError());
     return LA_OK;
   }
@@ -513,7 +554,9 @@ static int run_decode(la_engine* e, const DecodeArgs& a, la_decode_io* io, void*
   if (e->world > 1) {
     RET_IF(lp_decode_loop(e, st, &launches));
   } else if (e->is_tiny()) {
-    la_tiny_decode<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_dec,
+    static const bool tiny_prof = getenv("LA_TINY_PROF") != nullptr;
+    if (tiny_prof) la_tiny_prof(true, nullptr);
+    la_tiny_decode<<<1, TINY_THREADS, e->tiny_smem, st>>>(e->tm, e->ts, e->d_plan, e->d_dec,
                                        e->h_dec.sample ? e->d_logits : nullptr);
     CK(cudaGetLastError());
     launches = 1;
@@ -602,7 +645,7 @@ extern "C" int32_t la_session_step(la_engine* e, la_step_outcome* out, void* str
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(e->device));
   if (e->is_tiny()) {
-    la_tiny_step_forward<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_dec,
+    la_tiny_step_forward<<<1, TINY_THREADS, e->tiny_smem, st>>>(e->tm, e->ts, e->d_plan, e->d_dec,
                                              h.sample ? e->d_logits : nullptr);
     if (h.sample) {
       la_sample_adjust_kernel<<<1 + h.G * (h.N - 1), 1024, 0, st>>>(e->d_dec);
@@ -868,7 +911,7 @@ static int run_plan(la_engine* e, const FwdPlan* P, float* logits, int32_t* amax
   int rc = LA_OK;
   std::vector<float> host;
   if (e->is_tiny()) {
-    la_tiny_forward<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, d_logits);
+    la_tiny_forward<<<1, TINY_THREADS, e->tiny_smem, st>>>(e->tm, e->ts, e->d_plan, d_logits);
     if (cudaGetLastError() != cudaSuccess) { la_set_error("forward launch failed"); rc = LA_ERR_CUDA; }
   } else {
     rc = llama_forward_plan(e, d_logits, st);
@@ -1027,6 +1070,12 @@ extern "C" int32_t la_debug_read(la_engine* e, int32_t what, void* host, int64_t
     case 3: src = e->d_dec; avail = sizeof(DevDecode); break;
     case 4: src = e->d_plan; avail = sizeof(FwdPlan); break;
     case 5: return llama_read_trace(e, host, (size_t)bytes);
+    case 21: {   // la_tiny_decode per-phase cycles (LA_TINY_PROF=1)
+      unsigned long long t[16];
+      if (la_tiny_prof(false, t) != 0) { la_set_error("tiny profile read failed"); return LA_ERR_CUDA; }
+      memcpy(host, t, std::min<size_t>(sizeof(t), (size_t)bytes));
+      return LA_OK;
+    }
     default:
       if (what >= 6 && !e->is_tiny() && llama_debug_buffer(e, what, &src, &avail)) break; la_set_error("unknown debug buffer %d", what); return LA_ERR_INVALID_CONFIG;
   }

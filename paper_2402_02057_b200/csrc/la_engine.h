@@ -48,6 +48,7 @@ struct la_engine {
   // ---- fp32 tiny path
   TinyModel tm{};
   TinyScratch ts{};
+  size_t tiny_smem = 0;                // dynamic smem of the fp32 kernels (activations), 0: global
 
   // ---- bf16 path
   LlamaPath* llama = nullptr;

@@ -138,7 +138,7 @@ extern "C" int32_t la_lp_init(la_engine* e, const void* unique_id, int32_t rank,
 // forward half of a step on one replica: K1 build + forward + owned argmax
 static int step_forward(la_engine* e, cudaStream_t st) {
   if (e->is_tiny()) {
-    la_tiny_step_forward<<<1, 1024, 0, st>>>(e->tm, e->ts, e->d_plan, e->d_dec, nullptr);
+    la_tiny_step_forward<<<1, TINY_THREADS, e->tiny_smem, st>>>(e->tm, e->ts, e->d_plan, e->d_dec, nullptr);
     CK(cudaGetLastError());
     return LA_OK;
   }

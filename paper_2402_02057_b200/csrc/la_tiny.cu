@@ -55,23 +55,141 @@ __device__ void norm_rows(const TinyModel& m, const float* x, float* h, int R, c
   }
 }
 
-// out[r][o] (+)= sum_i in[r][i] * W[o][i]  (+ bias)
-__device__ void gemv_rows(const float* in, int in_ld, const float* W, const float* bias, float* out,
+// out[r][o] (+)= sum_i in[r][i] * W[o][i]  (+ bias), W given transposed (WT[i][o])
+__device__ void gemv_rows(const float* in, int in_ld, const float* WT, const float* bias, float* out,
                           int out_ld, int R, int n_out, int n_in, bool accumulate) {
   for (int idx = threadIdx.x; idx < R * n_out; idx += blockDim.x) {
     int r = idx / n_out, o = idx % n_out;
     const float* a = in + (size_t)r * in_ld;
-    const float* w = W + (size_t)o * n_in;
+    const float* w = WT + o;
     float acc = 0.f;
-    for (int i = 0; i < n_in; ++i) acc = fmaf(a[i], w[i], acc);
+    for (int i = 0; i < n_in; ++i) acc = fmaf(a[i], w[(size_t)i * n_out], acc);
     if (bias) acc += bias[o];
     float* dst = out + (size_t)r * out_ld + o;
     *dst = accumulate ? (*dst + acc) : acc;
   }
 }
 
+// Optional per-phase cycle accounting of la_tiny_decode (LA_TINY_PROF=1,
+// profiling only; read with la_debug_read(engine, 21, ...)): [0] K1 build,
+// [1] forward, [2] argmax scatter, [3] sampler, [4] K10 finish, [5] KV commit,
+// [6] steps
+__device__ unsigned long long g_tiny_prof[16];
+__device__ int g_tiny_prof_on;
+
+__device__ __forceinline__ long long tiny_clock() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+
+struct TinyProf {
+  bool on;
+  long long t;
+  __device__ TinyProf() : on(g_tiny_prof_on != 0), t(on ? tiny_clock() : 0) {}
+  __device__ void mark(int k) {
+    if (!on) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long n = tiny_clock();
+      g_tiny_prof[k] += (unsigned long long)(n - t);
+      t = n;
+    }
+  }
+};
+
+
+// Attention of R rows, one warp per (row, head).  Lane-parallel online
+// softmax: lane t takes keys t, t+32, ... of the row's key list (prefix slots,
+// chain slots in relative-position order, self) keeping a running max / sum /
+// weighted V in registers (no score buffer), then the 32 lane states combine
+// in a fixed butterfly order.  A row's arithmetic depends only on its own key
+// list, so lookahead rows compute exactly what the greedy rows do.  HD >= hd
+// bounds the register arrays (TINY_THREADS threads: 65536 / TINY_THREADS registers each).
+template <int HD>
+__device__ void attn_rows(const TinyModel& m, const TinyScratch& s, const FwdPlan& P, const float* kc,
+                          const float* vc, int R) {
+  const int H = m.H, KVH = m.KVH, hd = m.hd, qd = H * hd, kvd = KVH * hd;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const float scale = 1.0f / sqrtf((float)hd);
+  const bool vec = (hd & 3) == 0;
+  for (int job = warp; job < R * H; job += nw) {
+    const int r = job / H, hh = job % H, kvh = hh / (H / KVH);
+    const float* q = s.q + (size_t)r * qd + hh * hd;
+    const int npre = P.n_prefix, nch = P.chain_n[r];
+    const int nk = npre + nch + 1, self = P.slot[r];
+    float qr[HD];
+#pragma unroll
+    for (int i = 0; i < HD; ++i) qr[i] = i < hd ? q[i] : 0.f;
+    float mx = -INFINITY, sum = 0.f, o[HD];
+#pragma unroll
+    for (int i = 0; i < HD; ++i) o[i] = 0.f;
+    // (K / V through L1: the prefix rows stay cached across steps; this
+    // CTA's own stores keep its L1 coherent)
+    for (int j = lane; j < nk; j += 32) {
+      const int slot = (j < npre) ? j : (j < npre + nch ? P.chain[r][j - npre] : self);
+      const float* kk = kc + (size_t)slot * kvd + kvh * hd;
+      const float* vv = vc + (size_t)slot * kvd + kvh * hd;
+      float kr[HD], vr[HD];   // the key's and value's rows in flight together
+      if (vec) {
+#pragma unroll
+        for (int i4 = 0; i4 < HD / 4; ++i4)
+          if (4 * i4 < hd) {
+            const float4 a = reinterpret_cast<const float4*>(kk)[i4];
+            const float4 b = reinterpret_cast<const float4*>(vv)[i4];
+            kr[4 * i4] = a.x; kr[4 * i4 + 1] = a.y; kr[4 * i4 + 2] = a.z; kr[4 * i4 + 3] = a.w;
+            vr[4 * i4] = b.x; vr[4 * i4 + 1] = b.y; vr[4 * i4 + 2] = b.z; vr[4 * i4 + 3] = b.w;
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < HD; ++i)
+          if (i < hd) { kr[i] = kk[i]; vr[i] = vv[i]; }
+      }
+      float dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < HD; ++i)
+        if (i < hd) dot = fmaf(qr[i], kr[i], dot);
+      dot *= scale;
+      if (dot > mx) {
+        const float a = expf(mx - dot);   // 0 on the lane's first key (mx = -inf)
+        sum *= a;
+#pragma unroll
+        for (int i = 0; i < HD; ++i) o[i] *= a;
+        mx = dot;
+      }
+      const float e = expf(dot - mx);
+      sum += e;
+#pragma unroll
+      for (int i = 0; i < HD; ++i)
+        if (i < hd) o[i] = fmaf(e, vr[i], o[i]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, mx, off);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sum, off);
+      const float mn = fmaxf(mx, m2);
+      const float a = mx == -INFINITY ? 0.f : expf(mx - mn);
+      const float b = m2 == -INFINITY ? 0.f : expf(m2 - mn);
+      sum = sum * a + s2 * b;
+#pragma unroll
+      for (int i = 0; i < HD; ++i) {
+        const float o2 = __shfl_xor_sync(0xffffffffu, o[i], off);
+        o[i] = o[i] * a + o2 * b;
+      }
+      mx = mn;
+    }
+    const float inv = 1.0f / sum;
+    float v = 0.f;
+#pragma unroll
+    for (int i = 0; i < HD; ++i)
+      if (i == lane) v = o[i];
+    if (lane < hd) s.att[(size_t)r * qd + hh * hd + lane] = v * inv;
+  }
+}
+
 __device__ void forward_rows(const TinyModel& m, const TinyScratch& s, const FwdPlan& P,
-                             float* logits_out) {
+                             float* logits_out, TinyProf* pf = nullptr) {
+  auto mark = [&](int k) { if (pf) pf->mark(k); };
   const int R = P.n_rows;
   const int d = m.d, H = m.H, KVH = m.KVH, hd = m.hd;
   const int qd = H * hd, kvd = KVH * hd;
@@ -85,29 +203,27 @@ __device__ void forward_rows(const TinyModel& m, const TinyScratch& s, const Fwd
     s.x[idx] = v;
   }
   __syncthreads();
+  mark(8);
   for (int l = 0; l < m.L; ++l) {
     const TinyLayer& w = m.layers[l];
     float* kc = m.kcache + (size_t)l * m.slots * kvd;
     float* vc = m.vcache + (size_t)l * m.slots * kvd;
     norm_rows(m, s.x, s.h, R, w.ln1_g, w.ln1_b);
     __syncthreads();
+    mark(9);
     // q / k / v projections; k, v go straight to the row's cache slot
-    for (int idx = tid; idx < R * (qd + 2 * kvd); idx += nth) {
-      int r = idx / (qd + 2 * kvd), o = idx % (qd + 2 * kvd);
-      const float* Wt;
-      int oo;
-      if (o < qd) { Wt = w.wq; oo = o; }
-      else if (o < qd + kvd) { Wt = w.wk; oo = o - qd; }
-      else { Wt = w.wv; oo = o - qd - kvd; }
+    const int nqkv = qd + 2 * kvd;
+    for (int idx = tid; idx < R * nqkv; idx += nth) {
+      int r = idx / nqkv, o = idx % nqkv;
       const float* a = s.h + (size_t)r * d;
-      const float* ww = Wt + (size_t)oo * d;
       float acc = 0.f;
-      for (int i = 0; i < d; ++i) acc = fmaf(a[i], ww[i], acc);
-      if (o < qd) s.q[(size_t)r * qd + oo] = acc;
-      else if (o < qd + kvd) kc[(size_t)P.slot[r] * kvd + oo] = acc;
-      else vc[(size_t)P.slot[r] * kvd + oo] = acc;
+      for (int i = 0; i < d; ++i) acc = fmaf(a[i], w.wqkvT[(size_t)i * nqkv + o], acc);
+      if (o < qd) s.q[(size_t)r * qd + o] = acc;
+      else if (o < qd + kvd) kc[(size_t)P.slot[r] * kvd + (o - qd)] = acc;
+      else vc[(size_t)P.slot[r] * kvd + (o - qd - kvd)] = acc;
     }
     __syncthreads();
+    mark(10);
     if (m.arch == TINY_ARCH_LLAMA) {
       // rotate-half RoPE on q and on the freshly written k
       const int half = hd / 2;
@@ -126,46 +242,14 @@ __device__ void forward_rows(const TinyModel& m, const TinyScratch& s, const Fwd
       __syncthreads();
     }
     // attention: one warp per (row, head); keys = prefix slots, chain slots
-    // (relative-position order), self -- the structured mask as a chain.
-    const float scale = 1.0f / sqrtf((float)hd);
-    for (int job = warp; job < R * H; job += nw) {
-      int r = job / H, hh = job % H, kvh = hh / (H / KVH);
-      const float* q = s.q + (size_t)r * qd + hh * hd;
-      float* sc = s.scores + (size_t)job * s.max_keys;
-      const int npre = P.n_prefix, nch = P.chain_n[r];
-      const int nk = npre + nch + 1;
-      float mx = -INFINITY;
-      for (int j = lane; j < nk; j += 32) {
-        int slot = (j < npre) ? j : (j < npre + nch ? P.chain[r][j - npre] : P.slot[r]);
-        const float* kk = kc + (size_t)slot * kvd + kvh * hd;
-        float dot = 0.f;
-        for (int i = 0; i < hd; ++i) dot = fmaf(q[i], kk[i], dot);
-        dot *= scale;
-        sc[j] = dot;
-        mx = fmaxf(mx, dot);
-      }
-      mx = warp_max(mx);
-      float sum = 0.f;
-      for (int j = lane; j < nk; j += 32) {
-        float e = expf(sc[j] - mx);
-        sc[j] = e;
-        sum += e;
-      }
-      sum = warp_sum(sum);
-      __syncwarp();
-      float inv = 1.0f / sum;
-      for (int i = lane; i < hd; i += 32) {
-        float acc = 0.f;
-        for (int j = 0; j < nk; ++j) {
-          int slot = (j < npre) ? j : (j < npre + nch ? P.chain[r][j - npre] : P.slot[r]);
-          acc = fmaf(sc[j], vc[(size_t)slot * kvd + kvh * hd + i], acc);
-        }
-        s.att[(size_t)r * qd + hh * hd + i] = acc * inv;
-      }
-    }
+    // (relative-position order), self -- the structured mask as a chain
+    if (hd <= 8) attn_rows<8>(m, s, P, kc, vc, R);
+    else attn_rows<TINY_MAX_HD>(m, s, P, kc, vc, R);
     __syncthreads();
-    gemv_rows(s.att, qd, w.wo, nullptr, s.x, d, R, d, qd, true);   // x += ctx @ Wo
+    mark(11);
+    gemv_rows(s.att, qd, w.woT, nullptr, s.x, d, R, d, qd, true);   // x += ctx @ Wo
     __syncthreads();
+    mark(12);
     norm_rows(m, s.x, s.h, R, w.ln2_g, w.ln2_b);
     __syncthreads();
     if (m.arch == TINY_ARCH_GPT) {
@@ -173,9 +257,8 @@ __device__ void forward_rows(const TinyModel& m, const TinyScratch& s, const Fwd
       for (int idx = tid; idx < R * m.ff; idx += nth) {
         int r = idx / m.ff, o = idx % m.ff;
         const float* a = s.h + (size_t)r * d;
-        const float* ww = w.w1 + (size_t)o * d;
         float acc = 0.f;
-        for (int i = 0; i < d; ++i) acc = fmaf(a[i], ww[i], acc);
+        for (int i = 0; i < d; ++i) acc = fmaf(a[i], w.w1T[(size_t)i * m.ff + o], acc);
         acc += w.b1[o];
         s.ff[idx] = acc > 0.f ? acc : 0.f;
       }
@@ -183,16 +266,19 @@ __device__ void forward_rows(const TinyModel& m, const TinyScratch& s, const Fwd
       for (int idx = tid; idx < R * m.ff; idx += nth) {
         int r = idx / m.ff, o = idx % m.ff;
         const float* a = s.h + (size_t)r * d;
-        const float* wg = w.w1 + (size_t)o * d;
-        const float* wu = w.wu + (size_t)o * d;
         float g = 0.f, u = 0.f;
-        for (int i = 0; i < d; ++i) { g = fmaf(a[i], wg[i], g); u = fmaf(a[i], wu[i], u); }
+        for (int i = 0; i < d; ++i) {
+          g = fmaf(a[i], w.w1T[(size_t)i * m.ff + o], g);
+          u = fmaf(a[i], w.wuT[(size_t)i * m.ff + o], u);
+        }
         s.ff[idx] = g / (1.0f + expf(-g)) * u;
       }
     }
     __syncthreads();
-    gemv_rows(s.ff, m.ff, w.w2, w.b2, s.x, d, R, d, m.ff, true);
+    mark(13);
+    gemv_rows(s.ff, m.ff, w.w2T, w.b2, s.x, d, R, d, m.ff, true);
     __syncthreads();
+    mark(14);
   }
   // final norm + unembedding + per-row argmax (models.py:267-271, sampling.py:17-19)
   norm_rows(m, s.x, s.h, R, m.lnf_g, m.lnf_b);
@@ -202,9 +288,8 @@ __device__ void forward_rows(const TinyModel& m, const TinyScratch& s, const Fwd
     float best = -INFINITY;
     int bi = 0x7fffffff;
     for (int v = lane; v < m.V; v += 32) {
-      const float* ww = m.unembed + (size_t)v * d;
       float acc = 0.f;
-      for (int i = 0; i < d; ++i) acc = fmaf(a[i], ww[i], acc);
+      for (int i = 0; i < d; ++i) acc = fmaf(a[i], m.unembedT[(size_t)i * m.V + v], acc);
       if (logits_out) logits_out[(size_t)r * m.V + v] = acc;
       argmax_merge(best, bi, acc, v);
     }
@@ -217,6 +302,7 @@ __device__ void forward_rows(const TinyModel& m, const TinyScratch& s, const Fwd
     if (lane == 0) s.row_amax[r] = bi;
   }
   __syncthreads();
+  mark(15);
 }
 
 // copy the K/V of accepted branch rows into place.
@@ -241,9 +327,57 @@ __device__ void commit_kv(const TinyModel& m, const DevDecode& d) {
 
 }  // namespace
 
+int la_tiny_prof(bool enable, unsigned long long* out) {
+  if (out) return cudaMemcpyFromSymbol(out, g_tiny_prof, sizeof(g_tiny_prof)) == cudaSuccess ? 0 : -1;
+  int v = enable ? 1 : 0;
+  unsigned long long z[16] = {};
+  if (cudaMemcpyToSymbol(g_tiny_prof, z, sizeof(z)) != cudaSuccess) return -1;
+  return cudaMemcpyToSymbol(g_tiny_prof_on, &v, sizeof(v)) == cudaSuccess ? 0 : -1;
+}
+
+// Activations in dynamic shared memory when the host sized it (s.smem): the
+// phases' dependent reads then hit the SM instead of L2 (global stores bypass
+// L1).  Layout [x | h | q | att | ff], LA_MAX_ROWS rows each.
+__device__ __forceinline__ TinyScratch tiny_local(const TinyModel& m, TinyScratch s) {
+  if (s.smem) {
+    extern __shared__ float tiny_sm[];
+    const int R = LA_MAX_ROWS, qd = m.H * m.hd;
+    s.x = tiny_sm;
+    s.h = s.x + R * m.d;
+    s.q = s.h + R * m.d;
+    s.att = s.q + R * qd;
+    s.ff = s.att + R * qd;
+  }
+  return s;
+}
+
+__global__ void la_tiny_transpose(const float* in, int rows, int cols, float* out, int out_ld, int col_off) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)rows * cols; i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cols), c = (int)(i % cols);
+    out[(size_t)c * out_ld + col_off + r] = in[i];
+  }
+}
+
+size_t la_tiny_smem_bytes(const TinyModel& m) {
+  const size_t R = LA_MAX_ROWS, qd = (size_t)m.H * m.hd;
+  const size_t need = R * (2 * (size_t)m.d + 2 * qd + (size_t)m.ff) * sizeof(float);
+  return need <= 160 * 1024 ? need : 0;   // larger models keep the activations in global memory
+}
+
+int la_tiny_set_smem(size_t bytes) {
+  const int b = (int)bytes;
+  if (cudaFuncSetAttribute(la_tiny_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize, b) != cudaSuccess ||
+      cudaFuncSetAttribute(la_tiny_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, b) != cudaSuccess ||
+      cudaFuncSetAttribute(la_tiny_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, b) != cudaSuccess ||
+      cudaFuncSetAttribute(la_tiny_step_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, b) != cudaSuccess)
+    return -1;
+  return 0;
+}
+
 // Prefill: causal chain over prompt[0 .. n-1) in chunks of LA_MAX_ROWS rows.
-__global__ void __launch_bounds__(1024) la_tiny_prefill(TinyModel m, TinyScratch s, FwdPlan* P,
+__global__ void __launch_bounds__(TINY_THREADS) la_tiny_prefill(TinyModel m, TinyScratch sg, FwdPlan* P,
                                                        const int* tokens, int n) {
+  const TinyScratch s = tiny_local(m, sg);
   for (int start = 0; start < n; start += LA_MAX_ROWS) {
     int R = min(LA_MAX_ROWS, n - start);
     if (threadIdx.x == 0) {
@@ -268,19 +402,25 @@ __global__ void __launch_bounds__(1024) la_tiny_prefill(TinyModel m, TinyScratch
 // until done (EOS / max_tokens) -- entirely on the device.  Under a
 // temperature sampler (logits != null) the step also adjusts row 0 and the
 // branch rows and runs verify_sample, in this CTA (la_sample.cuh).
-__global__ void __launch_bounds__(1024) la_tiny_decode(TinyModel m, TinyScratch s, FwdPlan* P,
+__global__ void __launch_bounds__(TINY_THREADS) la_tiny_decode(TinyModel m, TinyScratch sg, FwdPlan* P,
                                                       DevDecode* dp, float* logits) {
   __shared__ LaSampleSmem sm;
+  const TinyScratch s = tiny_local(m, sg);
   DevDecode& d = *dp;
+  TinyProf prof;
   for (int it = 0; it < d.max_steps; ++it) {
     __syncthreads();
     if (d.done) break;
+    prof.mark(7);
     la_step_build(d, *P);
     if (P->n_rows == 0) break;
-    forward_rows(m, s, *P, d.sample ? logits : nullptr);
+    prof.mark(0);
+    forward_rows(m, s, *P, d.sample ? logits : nullptr, &prof);
+    prof.mark(1);
     for (int r = threadIdx.x; r < P->n_rows; r += blockDim.x)
       if (P->own[r]) d.amax[P->grow[r]] = s.row_amax[r];
     __syncthreads();
+    prof.mark(2);
     if (d.sample) {
       const int nr = la_sample_rows(d);
       bool ok = true;
@@ -291,23 +431,29 @@ __global__ void __launch_bounds__(1024) la_tiny_decode(TinyModel m, TinyScratch 
       if (!ok && threadIdx.x == 0) d.degenerate = 1;
       __syncthreads();
     }
+    prof.mark(3);
     la_step_finish(d);
+    prof.mark(4);
     if (d.mode == LA_MODE_LOOKAHEAD) commit_kv(m, d);
     __syncthreads();
+    prof.mark(5);
+    if (prof.on && threadIdx.x == 0) g_tiny_prof[6] += 1;
   }
 }
 
 // Parity hook: evaluate an explicit plan (prefix already cached) and dump logits.
-__global__ void __launch_bounds__(1024) la_tiny_forward(TinyModel m, TinyScratch s, FwdPlan* P,
+__global__ void __launch_bounds__(TINY_THREADS) la_tiny_forward(TinyModel m, TinyScratch sg, FwdPlan* P,
                                                        float* logits) {
+  const TinyScratch s = tiny_local(m, sg);
   forward_rows(m, s, *P, logits);
 }
 
 // Step-granular variants for lookahead parallelism (la_decode_lookahead_group):
 // phase A = K1 build + forward + owned-row argmax; the host-side group then
 // exchanges the argmax table and the winner's K/V; phase B = K10 finish.
-__global__ void __launch_bounds__(1024) la_tiny_step_forward(TinyModel m, TinyScratch s,
+__global__ void __launch_bounds__(TINY_THREADS) la_tiny_step_forward(TinyModel m, TinyScratch sg,
                                                             FwdPlan* P, DevDecode* dp, float* logits) {
+  const TinyScratch s = tiny_local(m, sg);
   DevDecode& d = *dp;
   la_step_build(d, *P);
   if (P->n_rows == 0) return;
