@@ -232,8 +232,7 @@ static int tiny_setup(la_engine* e) {
   RET_IF(dalloc(e, &s.att, (size_t)R * qd));
   RET_IF(dalloc(e, &s.ff, (size_t)R * d.ffn));
   RET_IF(dalloc(e, &s.row_amax, R));
-  e->tiny_smem = la_tiny_smem_bytes(m);
-  s.smem = e->tiny_smem > 0 ? 1 : 0;
+  e->tiny_smem = la_tiny_smem_bytes(m, &s.smem);
   if (e->tiny_smem && la_tiny_set_smem(e->tiny_smem) != 0) {
     la_set_error("fp32 path: dynamic shared memory attribute (%zu B) refused", e->tiny_smem);
     return LA_ERR_CUDA;

@@ -358,10 +358,14 @@ __global__ void la_tiny_transpose(const float* in, int rows, int cols, float* ou
   }
 }
 
-size_t la_tiny_smem_bytes(const TinyModel& m) {
+size_t la_tiny_smem_bytes(const TinyModel& m, int* mode) {
   const size_t R = LA_MAX_ROWS, qd = (size_t)m.H * m.hd;
-  const size_t need = R * (2 * (size_t)m.d + 2 * qd + (size_t)m.ff) * sizeof(float);
-  return need <= 160 * 1024 ? need : 0;   // larger models keep the activations in global memory
+  const size_t act = R * (2 * (size_t)m.d + 2 * qd + (size_t)m.ff) * sizeof(float);
+  // static smem (sampler, decode state, K1 / K10) stays below 24 KB
+  if (act + sizeof(FwdPlan) <= 196 * 1024) { *mode = 2; return act + sizeof(FwdPlan); }
+  if (act <= 160 * 1024) { *mode = 1; return act; }
+  *mode = 0;                              // larger models keep the activations in global memory
+  return 0;
 }
 
 int la_tiny_set_smem(size_t bytes) {
@@ -372,6 +376,19 @@ int la_tiny_set_smem(size_t bytes) {
       cudaFuncSetAttribute(la_tiny_step_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, b) != cudaSuccess)
     return -1;
   return 0;
+}
+
+// The step plan in dynamic shared memory (s.smem == 2: after the activations).
+__device__ __forceinline__ FwdPlan* tiny_plan(const TinyModel& m, const TinyScratch& s, FwdPlan* Pg) {
+  if (s.smem != 2) return Pg;
+  extern __shared__ float tiny_sm[];
+  const size_t R = LA_MAX_ROWS, qd = (size_t)m.H * m.hd;
+  return reinterpret_cast<FwdPlan*>(tiny_sm + R * (2 * (size_t)m.d + 2 * qd + (size_t)m.ff));
+}
+__device__ __forceinline__ void tiny_plan_store(const FwdPlan& src, FwdPlan* dst) {
+  const int* a = reinterpret_cast<const int*>(&src);
+  int* b = reinterpret_cast<int*>(dst);
+  for (size_t i = threadIdx.x; i < sizeof(FwdPlan) / sizeof(int); i += blockDim.x) b[i] = a[i];
 }
 
 // Prefill: causal chain over prompt[0 .. n-1) in chunks of LA_MAX_ROWS rows.
@@ -402,11 +419,34 @@ __global__ void __launch_bounds__(TINY_THREADS) la_tiny_prefill(TinyModel m, Tin
 // until done (EOS / max_tokens) -- entirely on the device.  Under a
 // temperature sampler (logits != null) the step also adjusts row 0 and the
 // branch rows and runs verify_sample, in this CTA (la_sample.cuh).
-__global__ void __launch_bounds__(TINY_THREADS) la_tiny_decode(TinyModel m, TinyScratch sg, FwdPlan* P,
+__global__ void __launch_bounds__(TINY_THREADS) la_tiny_decode(TinyModel m, TinyScratch sg, FwdPlan* Pg,
                                                       DevDecode* dp, float* logits) {
   __shared__ LaSampleSmem sm;
+  // the decode state (scalars, window, candidates, argmax table, accepted
+  // tokens) and -- when the host sized it -- the step plan live in shared
+  // memory for the whole decode: K1 / K10 / the forward chase them serially,
+  // so every access is an SM round trip instead of an L2 one.  Written back
+  // at the end (the host reads the state; tests read the plan).
+  __shared__ DevDecode d;
+  __shared__ int s_window[64 * LA_MAX_SUFFIX], s_cand[64 * LA_MAX_SUFFIX], s_amax[LA_MAX_ROWS],
+      s_acc[LA_MAX_SUFFIX + 2];
   const TinyScratch s = tiny_local(m, sg);
-  DevDecode& d = *dp;
+  FwdPlan* P = tiny_plan(m, s, Pg);
+  const int tid = threadIdx.x;
+  if (tid == 0) d = *dp;
+  __syncthreads();
+  const int ncell = d.mode == LA_MODE_LOOKAHEAD ? (d.N - 1) * d.W - 1 : 0;
+  const int ncand = d.mode == LA_MODE_LOOKAHEAD ? d.G * (d.N - 1) : 0;
+  int* const g_window = d.window;
+  int* const g_cand = d.cand;
+  int* const g_amax = d.amax;
+  int* const g_acc = d.accepted;
+  for (int i = tid; i < ncell; i += blockDim.x) s_window[i] = g_window[i];
+  for (int i = tid; i < ncand; i += blockDim.x) s_cand[i] = g_cand[i];
+  for (int i = tid; i < LA_MAX_ROWS; i += blockDim.x) s_amax[i] = g_amax[i];
+  for (int i = tid; i < d.N; i += blockDim.x) s_acc[i] = g_acc[i];
+  __syncthreads();
+  if (tid == 0) { d.window = s_window; d.cand = s_cand; d.amax = s_amax; d.accepted = s_acc; }
   TinyProf prof;
   for (int it = 0; it < d.max_steps; ++it) {
     __syncthreads();
@@ -438,6 +478,18 @@ __global__ void __launch_bounds__(TINY_THREADS) la_tiny_decode(TinyModel m, Tiny
     __syncthreads();
     prof.mark(5);
     if (prof.on && threadIdx.x == 0) g_tiny_prof[6] += 1;
+  }
+  __syncthreads();
+  for (int i = tid; i < ncell; i += blockDim.x) g_window[i] = s_window[i];
+  for (int i = tid; i < ncand; i += blockDim.x) g_cand[i] = s_cand[i];
+  for (int i = tid; i < LA_MAX_ROWS; i += blockDim.x) g_amax[i] = s_amax[i];
+  for (int i = tid; i < d.N; i += blockDim.x) g_acc[i] = s_acc[i];
+  if (P != Pg) tiny_plan_store(*P, Pg);
+  __syncthreads();
+  if (tid == 0) {
+    DevDecode out = d;
+    out.window = g_window; out.cand = g_cand; out.amax = g_amax; out.accepted = g_acc;
+    *dp = out;
   }
 }
 

@@ -37,11 +37,12 @@ struct TinyModel {
 
 struct TinyScratch {
   float *x, *h, *q, *att, *ff;        // [LA_MAX_ROWS][...] (global; shared memory when smem)
-  int smem;                           // 1: the kernels keep x / h / q / att / ff in dynamic smem
+  int smem;                           // 1: the kernels keep x / h / q / att / ff in dynamic smem;
+                                      // 2: and la_tiny_decode its step plan
   int* row_amax;                      // [LA_MAX_ROWS]
 };
 // dynamic shared memory the kernels need for the activations (0: keep them global)
-size_t la_tiny_smem_bytes(const TinyModel& m);
+size_t la_tiny_smem_bytes(const TinyModel& m, int* mode);
 int la_tiny_set_smem(size_t bytes);
 
 __global__ void la_tiny_prefill(TinyModel m, TinyScratch s, FwdPlan* P, const int* tokens, int n);
