@@ -714,6 +714,292 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------ data-parallel + stream-K GEMM
+// (LA_EPI_DPSK_SWIGLU: the gate/up projection when its 128-row tiles
+// outnumber the CTAs).  CTA c owns the dpc = T / P whole tiles
+// [c dpc, (c + 1) dpc) (full K in one TMEM accumulator: no split-K pieces,
+// SwiGLU straight from TMEM) and first streams its stream-K share of the
+// R = T - P dpc remaining tiles, whose pieces it writes and later fixes up (its
+// row slice of every remainder tile it touched; those pieces were all written
+// at the start of every CTA's stream, so the wait is normally already over).
+// One-tile units (16 KB weights + the k-block's step rows), 6-stage ring.
+// The stream-K split and the piece order depend on the shape only, so every
+// row's arithmetic is the same for any row count / layout / LP shard.
+__device__ __forceinline__ float dpsk_rstd(const LaRowNorm& n, int tok) {
+  // the exact summation order of rstd_issue<8> / rstd_finish<8> (la_reduce_dev.cuh),
+  // so a row's scale is bit-identical for whole and remainder tiles
+  float p[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    float v = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int t = l + 8 * i;
+      v += t < n.tiles ? __ldcg(n.ss + t * 128 + tok) : 0.f;
+    }
+    for (int t = l + 64; t < n.tiles; t += 8) v += __ldcg(n.ss + t * 128 + tok);
+    p[l] = v;
+  }
+  const float s = ((p[0] + p[4]) + (p[2] + p[6])) + ((p[1] + p[5]) + (p[3] + p[7]));
+  return rsqrtf(s * n.inv_d + n.eps);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) la_gemm_dpsk_kernel(const LaGemmArgs args) {
+  const unsigned long long t_entry = args.trace ? globaltimer() : 0ull;
+  // optional per-CTA trace [gridDim][8]: 0 entry, 1 wait returned, 2 last MMA
+  // issued, 3 exit, 4 remainder pieces written, 5 whole tile's act written,
+  // 6 fix-up pieces complete, 7 fix-up done
+  auto tr = [&](int k, bool cond) {
+    if (args.trace && cond) args.trace[blockIdx.x * 8 + k] = globaltimer();
+  };
+  extern __shared__ uint8_t smem_raw[];
+  const FwdPlan* P = args.plan;
+  uint8_t* sm = smem_raw + ((1024 - (ptx::smem_u32(smem_raw) & 1023)) & 1023);
+  constexpr int nst = kMaxStages;
+  uint8_t* sA = sm;
+  uint8_t* sB = sA + nst * kTileBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + nst * kBBytes);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* fxbar = tempty + 2;
+  uint64_t* tdp = fxbar + 1;                   // the whole tile's accumulators are complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tdp + 1);
+  uint8_t* epi_base = reinterpret_cast<uint8_t*>(tmem_slot) + 16;
+  float* sEpi = reinterpret_cast<float*>(epi_base + ((128 - (ptx::smem_u32(epi_base) & 127)) & 127));
+  float* sRstd = sEpi + kStageFloats;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = args.kb;
+  const int T = args.n_real;
+  const int Pn = gridDim.x;
+  const int dpc = T / Pn;                      // whole tiles per CTA
+  const int R = T - dpc * Pn;                  // remainder tiles [dpc Pn, T)
+  const long Ur = (long)R * kb;
+  const long ur0 = (long)blockIdx.x * Ur / Pn, ur1 = (long)(blockIdx.x + 1) * Ur / Pn;
+  const int n_rem = (int)(ur1 - ur0);
+  const int n_all = n_rem + dpc * kb;
+  auto unit_tile = [&](int it) -> int {
+    return it < n_rem ? dpc * Pn + (int)((ur0 + it) / kb) : (int)blockIdx.x * dpc + (it - n_rem) / kb;
+  };
+  auto unit_k = [&](int it) -> int { return it < n_rem ? (int)((ur0 + it) % kb) : (it - n_rem) % kb; };
+  auto a_src = [&](int t, int k) -> const __nv_bfloat16* {
+    return args.a + ((size_t)((t / LA_TPC) * kb + k) * LA_TPC + (t % LA_TPC)) * (kTileBytes / 2);
+  };
+  auto seg_end_of = [&](int it) -> int {   // units of one tile are contiguous in the sequence
+    const int t = unit_tile(it);
+    if (it < n_rem) {
+      const long tile_end = (long)(t - dpc * Pn + 1) * kb;   // remainder-space end of tile t
+      return (int)(min(ur1, tile_end) - ur0);
+    }
+    return n_rem + ((it - n_rem) / kb + 1) * kb;
+  };
+  const int n_pre = min(nst, n_all);
+  la_pdl_trigger();
+  uint64_t pol_w = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { ptx::mbar_init(&tfull[b], 1); ptx::mbar_init(&tempty[b], 128); }
+    ptx::mbar_init(fxbar, 1);
+    ptx::mbar_init(tdp, 1);
+    ptx::fence_barrier_init();
+    pol_w = ptx::policy_evict_first();
+    for (int i = 0; i < n_pre; ++i) {
+      ptx::mbar_expect_tx_noarrive(&full[i], kTileBytes);
+      ptx::bulk_load(sA + i * kTileBytes, a_src(unit_tile(i), unit_k(i)), kTileBytes, &full[i], pol_w);
+    }
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  la_pdl_wait();
+  if (args.timing && threadIdx.x == 0) {
+    if (atomicAdd(&args.timing[3], 1ull) == 0ull) args.timing[0] = globaltimer();
+  }
+  if (args.trace && threadIdx.x == 0) args.trace[blockIdx.x * 8 + 0] = t_entry;
+  tr(1, threadIdx.x == 0);
+  const int n_rows = P->n_rows;
+  const int n_pad = P->n_pad;
+  // TMEM: columns [0, 256) = two buffers for the remainder segments, [256, 512)
+  // = the whole tile's two accumulators (even / odd k-blocks: two independent
+  // MMA chains keep the tensor pipe busy; summed even + odd in the epilogue)
+  const uint32_t dp_acc = tmem + 256;
+
+  if (n_rows == 0) {
+    if (warp == 0 && lane == 0)
+      for (int i = 0; i < n_pre; ++i) {
+        ptx::mbar_arrive(&full[i]);
+        ptx::mbar_wait(&full[i], 0);
+      }
+  } else if (warp == 0) {
+    // --------------------------------------------------------- producer
+    if (lane == 0) {
+      const uint64_t pol_x = ptx::policy_evict_last();
+      const uint32_t bbytes = (uint32_t)n_pad * 128;
+      for (int it = 0; it < n_all; ++it) {
+        const int s = it % nst;
+        const uint32_t r = (uint32_t)(it / nst);
+        const int t = unit_tile(it), k = unit_k(it);
+        if (it < n_pre) {
+          ptx::mbar_expect_tx(&full[s], bbytes);
+        } else {
+          ptx::mbar_wait(&empty[s], (r - 1) & 1);
+          ptx::mbar_expect_tx(&full[s], kTileBytes + bbytes);
+          ptx::bulk_load(sA + s * kTileBytes, a_src(t, k), kTileBytes, &full[s], pol_w);
+        }
+        ptx::bulk_load(sB + s * kBBytes, args.b + (size_t)k * (kBBytes / 2), bbytes, &full[s], pol_x);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = ptx::umma_idesc_bf16(128, (uint32_t)n_pad);
+      int use[2] = {0, 0}, buf = 0;
+      for (int it = 0; it < n_all;) {
+        const int first = it, end = seg_end_of(it);
+        const bool whole = it >= n_rem;
+        if (!whole && use[buf] > 0) {
+          ptx::mbar_wait(&tempty[buf], (use[buf] - 1) & 1);
+          ptx::tc_fence_after();
+        }
+        for (; it < end; ++it) {
+          const int s = it % nst;
+          ptx::mbar_wait(&full[s], (uint32_t)(it / nst) & 1);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(sA + s * kTileBytes);
+          const uint32_t b_addr = ptx::smem_u32(sB + s * kBBytes);
+          const int q = it - first;
+          const uint32_t d_tmem = whole ? dp_acc + (q & 1) * 128 : tmem + buf * 128;
+          const bool acc = whole ? q >= 2 : q > 0;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            ptx::umma_bf16(d_tmem, ptx::umma_desc_sw128(a_addr + kk * 32), ptx::umma_desc_sw128(b_addr + kk * 32),
+                           idesc, (acc || kk > 0) ? 1u : 0u);
+          ptx::umma_commit(&empty[s]);
+        }
+        ptx::umma_commit(whole ? tdp : &tfull[buf]);
+        tr(2, whole);
+        if (!whole) {
+          use[buf]++;
+          buf ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------- drain TMEM / epilogue
+    const int et = threadIdx.x - 64;              // 0..127
+    const int row_base = 32 * (warp & 3);
+    const int f = row_base + lane;                // accumulator lane = feature in tile
+    if (et < n_rows) sRstd[et] = dpsk_rstd(args.nrm, et);
+    ptx::named_bar_sync(1, 128);
+    int use[2] = {0, 0}, buf = 0;
+    for (int it = 0; it < n_all;) {
+      const int tile = unit_tile(it), end = seg_end_of(it);
+      const bool whole = it >= n_rem;
+      if (whole) ptx::mbar_wait(tdp, 0);
+      else ptx::mbar_wait(&tfull[buf], use[buf] & 1);
+      ptx::tc_fence_after();
+      const uint32_t t_base = tmem + ((uint32_t)row_base << 16) + buf * 128;
+      if (!whole) {
+        // remainder piece of tile `tile`: its contributor index = piece order
+        const long c_first = la_cta_of((long)(tile - dpc * Pn) * kb, Ur, Pn);
+        const int seg = (int)(blockIdx.x - c_first);
+        float* wsp = args.ws + ((size_t)tile * args.max_segs + seg) * 128 * 128 + f;
+        for (int c0 = 0; c0 < n_pad; c0 += 32) {
+          float v[32];
+          ptx::tmem_ld32(t_base + c0, v);
+          const int nj = min(32, n_rows - c0);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (jj < nj) __stcg(wsp + (size_t)(c0 + jj) * 128, v[jj]);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[buf]);
+        use[buf]++;
+        buf ^= 1;
+        ptx::named_bar_sync(1, 128);
+        if (et == 0) {
+          __threadfence();
+          atomicAdd(args.fx_arrive + tile, 1);
+        }
+        tr(4, et == 0);
+      } else {
+        // whole tile: even + odd accumulators, deferred-norm scale, SwiGLU,
+        // act -- straight from TMEM
+        const uint32_t e_base = dp_acc + ((uint32_t)row_base << 16);
+        for (int c0 = 0; c0 < n_pad; c0 += 32) {
+          float v[32], w[32];
+          ptx::tmem_ld32(e_base + c0, v);
+          ptx::tmem_ld32(e_base + 128 + c0, w);
+          const int nj = min(32, n_rows - c0);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) sEpi[f * kEpiLd + jj] = jj < nj ? (v[jj] + w[jj]) * sRstd[c0 + jj] : 0.f;
+          ptx::named_bar_sync(1, 128);
+          epi_apply<LA_EPI_SWIGLU>(args, P, tile, c0, n_rows, sEpi, et);
+          ptx::named_bar_sync(1, 128);
+        }
+        tr(5, et == 0);
+      }
+      it = end;
+    }
+    // ---- fix-up of this CTA's row slice of every remainder tile it touched
+    // (every MMA of this CTA has completed: the ring is free for staging)
+    float* S = reinterpret_cast<float*>(sA);
+    const uint64_t pol = ptx::policy_evict_first();
+    uint32_t fx_phase = 0;
+    for (int it = 0; it < n_rem;) {
+      const int tile = unit_tile(it), end = seg_end_of(it);
+      it = end;
+      long c0;
+      int nseg;
+      la_tile_segs(tile - dpc * Pn, kb, R, Pn, c0, nseg, 1);
+      const int j = (int)(blockIdx.x - c0);
+      const int r0 = j * n_rows / nseg, nr = (j + 1) * n_rows / nseg - r0;
+      if (et == 0)
+        while (ld_acquire(args.fx_arrive + tile) < nseg) __nanosleep(32);
+      tr(6, et == 0);
+      ptx::named_bar_sync(1, 128);
+      if (nr > 0) {
+        if (et == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy pieces -> bulk copies
+          const uint32_t bytes = (uint32_t)nr * 512;
+          ptx::mbar_expect_tx(fxbar, bytes * (uint32_t)nseg);
+          for (int sg = 0; sg < nseg; ++sg)
+            ptx::bulk_load(S + (size_t)sg * nr * 128, args.ws + (((size_t)tile * args.max_segs + sg) * 128 + r0) * 128,
+                           bytes, fxbar, pol);
+        }
+        ptx::mbar_wait(fxbar, fx_phase);
+        fx_phase ^= 1;
+        fx_finish<LA_EPI_FX_SWIGLU>(args, P, tile, r0, nr, nseg, S, et);
+      }
+      ptx::named_bar_sync(1, 128);   // S is restaged for the next tile
+      if (et == 0 && atomicAdd(args.fx_depart + tile, 1) == nseg - 1) {
+        args.fx_arrive[tile] = 0;    // every contributor is past its wait: reset for the next launch
+        args.fx_depart[tile] = 0;
+      }
+    }
+    tr(7, et == 0);
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+  tr(3, threadIdx.x == 0);
+  if (args.timing && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&args.timing[4], 1ull) == (unsigned long long)gridDim.x - 1) {
+      unsigned long long t1 = globaltimer();
+      args.timing[1] += t1 - args.timing[0];
+      args.timing[2] += 1;
+      args.timing[3] = 0;
+      args.timing[4] = 0;
+    }
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host
@@ -777,6 +1063,21 @@ bool la_gemm_fx_fits(const LaGemm& g) {
   return true;
 }
 
+// LA_EPI_DPSK_SWIGLU geometry: pieces per remainder tile (0: not applicable,
+// fewer real tiles than CTAs); the remainder fix-up stages nseg slices of
+// ceil(128 / nseg) rows in the ring
+int la_gemm_dpsk_segs(int n_real, int kb, int grid) {
+  const int dpc = n_real / grid, R = n_real - dpc * grid;
+  if (dpc != 1) return 0;   // one whole tile per CTA (its accumulator pair is not double-buffered)
+  if (R == 0) return 1;
+  if ((long)R * kb < grid) return 0;   // every CTA needs a remainder unit: the piece count of a tile
+                                       // is the CTA span of its units (la_tile_segs)
+  const int mx = la_gemm_workspace_segs(R, kb, grid, 1);
+  const size_t ring = (size_t)kMaxStages * (kTileBytes + kBBytes);
+  if ((size_t)mx * ((LA_MAX_ROWS + mx - 1) / mx) * 512 > ring) return 0;
+  return mx;
+}
+
 int la_gemm_workspace_segs(int n_tiles, int kb, int grid, int tpc) {
   long mx = 1;
   for (int t = 0; t < n_tiles; ++t) {
@@ -805,9 +1106,19 @@ static cudaError_t launch_epi(const LaGemm& g, cudaStream_t st, bool pdl) {
   return la_launch(la_gemm_kernel<EPI>, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
 }
 
+static cudaError_t launch_dpsk(const LaGemm& g, cudaStream_t st, bool pdl) {
+  const size_t smem = 1024 + (size_t)kMaxStages * (kTileBytes + kBBytes) + 2 * kMaxStages * 8 + 6 * 8 + 16 + 128 +
+                      kStageFloats * 4 + 128 * 4;
+  static std::atomic<unsigned> attr{0};
+  cudaError_t e = la_smem_attr_once(attr, la_gemm_dpsk_kernel, (int)smem);
+  if (e != cudaSuccess) return e;
+  return la_launch(la_gemm_dpsk_kernel, dim3(g.grid), dim3(kThreads), smem, st, pdl, g.args);
+}
+
 int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl) {
   cudaError_t e;
   switch (g.epi) {
+    case LA_EPI_DPSK_SWIGLU: e = launch_dpsk(g, st, pdl); break;
     case LA_EPI_QKV: e = launch_epi<LA_EPI_QKV>(g, st, pdl); break;
     case LA_EPI_SWIGLU: e = launch_epi<LA_EPI_SWIGLU>(g, st, pdl); break;
     case LA_EPI_LOGITS: e = launch_epi<LA_EPI_LOGITS>(g, st, pdl); break;

@@ -110,7 +110,10 @@ enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_L
                  // split-K pieces accumulated swap-AB (weight rows x step rows,
                  // N = padded rows; LA_GEMM_NT=0) instead of the default
                  // (step rows x weight rows, N = 128 tpc)
-                 LA_EPI_PARTIAL_SW = 8};
+                 LA_EPI_PARTIAL_SW = 8,
+                 // whole tiles per CTA (SwiGLU from TMEM) + stream-K remainder
+                 // fixed up in-kernel (la_gemm_dpsk_kernel; gate/up)
+                 LA_EPI_DPSK_SWIGLU = 9};
 
 struct LaGemm {
   LaGemmArgs args;
@@ -122,6 +125,7 @@ int la_make_tmap(CUtensorMap* map, const void* base, int rows, int K, int box_ro
 int la_gemm_launch(const LaGemm& g, cudaStream_t st, bool pdl = false);
 bool la_gemm_fx_fits(const LaGemm& g);   // the fix-up staging fits the smem ring
 int la_gemm_workspace_segs(int n_tiles, int kb, int grid, int tpc);
+int la_gemm_dpsk_segs(int n_real, int kb, int grid);
 int la_sm_count();
 size_t la_packed_elems(int rows, int K);   // bf16 elements of a packed matrix
 

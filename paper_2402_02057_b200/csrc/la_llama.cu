@@ -349,8 +349,18 @@ int llama_create(la_engine* e) {
     RET_IF(build_gemm(p->o[l], w.wo, d / 128, p->attn, H * 128, narrow_tpc,
                       (fx_mask & 2) ? LA_EPI_FX_RESID : LA_EPI_PARTIAL, o_grid));
     track(p->o[l]);
-    RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d, LA_TPC,
-                      fused ? LA_EPI_SWIGLU : (fx_mask & 4) ? LA_EPI_FX_SWIGLU : LA_EPI_PARTIAL));
+    // gate/up: whole tiles per CTA with SwiGLU from TMEM + an in-kernel fixed-up
+    // stream-K remainder (LA_GU_DPSK=1; measured slower than split-K pieces +
+    // the SwiGLU kernel: the per-CTA epilogue / fix-up tail)
+    const bool dpsk_on = getenv("LA_GU_DPSK") && atoi(getenv("LA_GU_DPSK")) == 1;
+    const int dpsk_segs = la_gemm_dpsk_segs(D.ffn / 64, d / 64, la_sm_count());
+    if (dpsk_on && !fused && !exp_paths && !(fx_mask & 4) && dpsk_segs > 0) {
+      RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d, 1, LA_EPI_DPSK_SWIGLU));
+      p->gu[l].args.max_segs = dpsk_segs;
+    } else {
+      RET_IF(build_gemm(p->gu[l], w.wgu, D.ffn / 64, p->h, d, LA_TPC,
+                        fused ? LA_EPI_SWIGLU : (fx_mask & 4) ? LA_EPI_FX_SWIGLU : LA_EPI_PARTIAL));
+    }
     p->gu[l].args.act = p->act;
     p->gu[l].args.n_real = D.ffn / 64;
     track(p->gu[l]);
@@ -811,7 +821,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       if (!(p->skip & 256)) RET_IF(la_gemm_launch(p->gu[l], st, p->pdl));
       KT_END(st, "gemm_gu");
     }
-    if (!p->fused && p->gu[l].epi != LA_EPI_FX_SWIGLU) {
+    if (!p->fused && p->gu[l].epi != LA_EPI_FX_SWIGLU && p->gu[l].epi != LA_EPI_DPSK_SWIGLU) {
       LaSwigluEpi sw{prefetch_of(p->down[l], pf_frac(p->down[l], 40e6)), e->d_plan, p->ws,
                      split_of(p->gu[l]), p->act, p->ffn, p->nrm};
       KT_BEGIN(st);

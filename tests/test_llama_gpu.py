@@ -58,9 +58,9 @@ PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "fx_epi": {"LA_FX": 
                 ids=lambda cp: f"{cp[0]}-{cp[1]}")
 def pair(request):
     name, path = request.param
-    saved = {k: os.environ.get(k) for k in ("LA_FUSED_EPI", "LA_MEGA", "LA_ATTN_TC", "LA_ATTN_O",
+    saved = {k: os.environ.get(k) for k in ("LA_FUSED_EPI", "LA_FX", "LA_MEGA", "LA_ATTN_TC", "LA_ATTN_O",
                                             "LA_ATTN_CLUSTER", "LA_ATTN_LAST_MERGE", "LA_ATTN_KSPLIT",
-                                            "LA_ATTN_SPLITS")}
+                                            "LA_ATTN_SPLITS", "LA_GU_DPSK")}
     for k in saved:
         os.environ.pop(k, None)
     os.environ.update(PATHS[path])
@@ -213,3 +213,48 @@ def test_lookahead_equals_greedy_long_context(pair):
                               seed_pool_from_prompt=True)
     toks, met = la.decode_lookahead(m, prompt, cfg, la.SamplerSpec("greedy", seed=4))
     assert toks == ar, name
+
+
+def test_whole_tile_gate_up_matches_oracle():
+    """LA_GU_DPSK=1 (la_gemm_dpsk_kernel): with more gate/up tiles than SMs,
+    every CTA owns one tile whole (SwiGLU from TMEM) and fixes up its share of
+    the stream-K remainder -- logits vs the oracle, lookahead == greedy."""
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ffn = 64 * (sms + 13)                       # one whole tile per CTA + 13 remainder tiles
+    # dim 1024: 16 k-blocks, so the 13 x 16 remainder units cover every CTA
+    cfg = dict(dim=1024, layers=2, heads=8, kv_heads=8, head_dim=128, ffn=ffn, vocab=1000,
+               rope_theta=10000.0, eps=1e-5)
+    w = llama_random_weights(cfg, seed=2, std=None)
+    lc = la.LlamaConfig(dim=1024, layers=2, heads=8, kv_heads=8, ffn=ffn, vocab=1000, head_dim=128)
+    saved = os.environ.get("LA_GU_DPSK")
+    os.environ["LA_GU_DPSK"] = "1"
+    try:
+        m = la.LlamaModel(lc, dtype="bf16", weights=w, max_context=512)
+    finally:
+        if saved is None:
+            os.environ.pop("LA_GU_DPSK", None)
+        else:
+            os.environ["LA_GU_DPSK"] = saved
+    try:
+        orc = LlamaOracle(cfg, w, emulate_bf16=True)
+        rng = np.random.default_rng(21)
+        prompt = [int(t) for t in rng.integers(0, 1000, 120)]
+        W, N = 5, 4
+        window = [int(t) for t in rng.integers(0, 1000, (N - 1) * W - 1)]
+        sufs = [tuple(int(t) for t in rng.integers(0, 1000, N - 1)) for _ in range(2)]
+        rows = lo.build_rows(window, W, N, prompt[-1], sufs)
+        got = m.logits(prompt[:-1], _step_layout(rows))
+        ref = np.stack(orc.logits_rows(prompt[:-1], rows))
+        for i in range(len(rows)):
+            assert _rel_err(got[i], ref[i]) < REL_TOL, (i, _rel_err(got[i], ref[i]))
+        # single-chunk context (as test_lookahead_equals_greedy_on_device)
+        short = prompt[:64]
+        ar = la.decode_autoregressive(m, short, la.SamplerSpec("greedy"), 32)
+        toks, _ = la.decode_lookahead(m, short, la.GenerationConfig(window=5, ngram=3, max_candidates=5,
+                                                                     max_tokens=32),
+                                      la.SamplerSpec("greedy"))
+        assert toks == ar
+    finally:
+        m.close()
+
