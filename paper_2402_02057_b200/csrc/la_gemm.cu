@@ -386,6 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive(&full[i]);
         ptx::mbar_wait(&full[i], 0);
       }
+    // the epilogue counts every launch's contributions: count the empty pieces in
+    if (args.ready && threadIdx.x == 0)
+      for (long u = u_begin; u < u_end; u = ((u / kb) + 1) * kb) atomicAdd(args.ready + (int)(u / kb), 1);
   } else if (warp == 0) {
     // --------------------------------------------------------- producer
     if (lane == 0) {
@@ -592,6 +595,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (et == 0) {
             __threadfence();
             atomicAdd(args.fx_arrive + tile, 1);
+          }
+        } else if (EPI == LA_EPI_PARTIAL_SW && args.ready) {
+          // this unit tile's piece is written: release it to the epilogue kernel
+          ptx::named_bar_sync(1, 128);
+          if (et == 0) {
+            __threadfence();
+            atomicAdd(args.ready + tile, 1);
           }
         } else if (EPI != LA_EPI_PARTIAL_SW && !multi) {
           ptx::named_bar_sync(1, 128);

@@ -99,6 +99,9 @@ struct LaGemmArgs {
   // into L2, so HBM keeps streaming through the latency-bound kernels that
   // separate two GEMMs (their data then arrives from L2)
   LaNextPf npf[2];
+  // per-unit-tile piece counters (monotonic: + contributors per launch) that
+  // the epilogue kernel polls instead of waiting for the whole grid (null: off)
+  int* ready;
 };
 
 enum LaGemmEpi { LA_EPI_PARTIAL = 0, LA_EPI_QKV = 1, LA_EPI_SWIGLU = 2, LA_EPI_LOGITS = 3,

@@ -83,6 +83,12 @@ struct LlamaPath {
   int skip = 0;                           // LA_SKIP: debug mask of per-layer launches to omit (timing only)
   bool mega = false;                      // persistent whole-forward kernel (LA_MEGA=1; experimental)
   LaMegaArgs ma{};
+  // per-tile readiness (default; LA_TILE_READY=0: grid waits): the epilogue
+  // kernels poll their tile's piece counter instead of waiting for the whole
+  // GEMM grid (3 % per 7B lookahead step)
+  bool tile_ready = false;
+  std::vector<int*> runs_qkv, runs_o, runs_gu, runs_down;   // per layer: [epilogue grid] launch counts
+  int* runs_head = nullptr;
   cudaStream_t cap = nullptr;
   cudaGraphExec_t loop_exec = nullptr;   // while(!done) { step }
   cudaGraphExec_t fwd_exec = nullptr;    // K1 + forward + owned argmax (LP)
@@ -458,6 +464,22 @@ int llama_create(la_engine* e) {
   }
   p->head.args.nrm = p->nrm;
   fin(p->head, 3, 3);
+  p->tile_ready = !(getenv("LA_TILE_READY") && atoi(getenv("LA_TILE_READY")) == 0) && !fused && !exp_paths;
+  if (p->tile_ready) {
+    auto ready_for = [&](LaGemm& gg) -> int {
+      return lalloc(e, &gg.args.ready, (size_t)(gg.args.n_tiles / gg.args.tpc));
+    };
+    p->runs_qkv.resize(D.layers); p->runs_o.resize(D.layers); p->runs_gu.resize(D.layers); p->runs_down.resize(D.layers);
+    for (int l = 0; l < D.layers; ++l) {
+      RET_IF(ready_for(p->qkv[l])); RET_IF(ready_for(p->o[l])); RET_IF(ready_for(p->gu[l])); RET_IF(ready_for(p->down[l]));
+      RET_IF(lalloc(e, &p->runs_qkv[l], (size_t)(H + 2 * KVH) * 16));
+      RET_IF(lalloc(e, &p->runs_o[l], (size_t)(d / 128) * 16));
+      RET_IF(lalloc(e, &p->runs_gu[l], (size_t)(D.ffn / 64) * 16));
+      RET_IF(lalloc(e, &p->runs_down[l], (size_t)(d / 128) * 16));
+    }
+    RET_IF(ready_for(p->head));
+    RET_IF(lalloc(e, &p->runs_head, (size_t)((D.vocab + 127) / 128) * 16));
+  }
   {
     // cross-GEMM L2 prefetch (LA_NPF=<MB next>[,<MB after next>]): each
     // decode GEMM, once its own loads are issued, pulls the first units of
@@ -747,7 +769,7 @@ static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
 }
 
 static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool embed, cudaStream_t st,
-                      const LaGemm* next) {
+                      const LaGemm* next, int* runs = nullptr) {
   LlamaPath* p = e->llama;
   LaResidNorm r;
   r.pf = next ? prefetch_of(*next, pf_frac(*next, 40e6)) : LaPrefetch{};
@@ -756,6 +778,7 @@ static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool emb
   r.sp = from ? split_of(*from) : LaSplit{2, 1, 1, 1, 1};
   r.embed = embed ? p->embed : nullptr;
   r.x = p->x; r.g = g; r.h = p->h; r.d = p->d; r.eps = p->eps; r.ss = p->ss;
+  if (from && runs && from->args.ready) { r.ready = from->args.ready; r.runs = runs; }
   KT_BEGIN(st);
   static const int rb = getenv("LA_RESID_RB") ? atoi(getenv("LA_RESID_RB")) : LA_MAX_ROWS / 8;
   CK(la_launch(la_resid_norm_kernel, dim3(p->d / 128, rb), dim3(256), 0, st, p->pdl, r));
@@ -782,6 +805,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       LaQkvEpi q{prefetch_of(p->o[l], pf_frac(p->o[l], 20e6)), e->d_plan, p->ws,
                  split_of(p->qkv[l]), p->q, kc + l * lstride, vc + l * lstride, p->rope_cos,
                  p->rope_sin, p->H, p->KVH, p->nrm};
+      if (p->tile_ready) { q.ready = p->qkv[l].args.ready; q.runs = p->runs_qkv[l]; }
       KT_BEGIN(st);
       if (!(p->skip & 1)) {
         static const int rb = getenv("LA_QKV_RB") ? atoi(getenv("LA_QKV_RB")) : LA_MAX_ROWS / 8;
@@ -815,7 +839,8 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
       KT_END(st, "gemm_o");
     }
     if (!(p->skip & 8) && p->o[l].epi != LA_EPI_FX_RESID)
-      RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st, &p->gu[l]));
+      RET_IF(resid_norm(e, &p->o[l], p->lw[l].mlp_norm, false, st, &p->gu[l],
+                        p->tile_ready ? p->runs_o[l] : nullptr));
     {
       KT_BEGIN(st);
       if (!(p->skip & 256)) RET_IF(la_gemm_launch(p->gu[l], st, p->pdl));
@@ -824,6 +849,7 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
     if (!p->fused && p->gu[l].epi != LA_EPI_FX_SWIGLU && p->gu[l].epi != LA_EPI_DPSK_SWIGLU) {
       LaSwigluEpi sw{prefetch_of(p->down[l], pf_frac(p->down[l], 40e6)), e->d_plan, p->ws,
                      split_of(p->gu[l]), p->act, p->ffn, p->nrm};
+      if (p->tile_ready) { sw.ready = p->gu[l].args.ready; sw.runs = p->runs_gu[l]; }
       KT_BEGIN(st);
       if (!(p->skip & 16)) {
         static const int rb = getenv("LA_SWIGLU_RB") ? atoi(getenv("LA_SWIGLU_RB")) : LA_MAX_ROWS / 16;
@@ -843,7 +869,8 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
     }
     const float* next = (l + 1 < p->L) ? p->lw[l + 1].attn_norm : p->final_norm;
     if (!(p->skip & 32) && p->down[l].epi != LA_EPI_FX_RESID)
-      RET_IF(resid_norm(e, &p->down[l], next, false, st, l + 1 < p->L ? &p->qkv[l + 1] : &p->head));
+      RET_IF(resid_norm(e, &p->down[l], next, false, st, l + 1 < p->L ? &p->qkv[l + 1] : &p->head,
+                        p->tile_ready ? p->runs_down[l] : nullptr));
     CK(cudaGetLastError());
     // 4 GEMMs + attention (1 fused, or chunks + merge) + the residual norms not fused into O / down
     n += (p->attn_fused ? 5 : 6) + (p->o[l].epi != LA_EPI_FX_RESID) + (p->down[l].epi != LA_EPI_FX_RESID);
@@ -863,6 +890,7 @@ static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
   KT_BEGIN(st);
   if (!p->head_fused) {
     LaLogitsEpi lg{e->d_plan, p->ws, split_of(p->head), p->keys, p->logits, p->V, p->nrm};
+    if (p->tile_ready) { lg.ready = p->head.args.ready; lg.runs = p->runs_head; }
     CK(la_launch(la_logits_epi_kernel, dim3(p->head_tiles, LA_MAX_ROWS / 8), dim3(128), 0, st, p->pdl, lg));
     *nk += 1;
   }

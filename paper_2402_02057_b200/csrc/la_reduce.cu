@@ -43,7 +43,7 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
 
 // grid = (H + 2*KVH tiles, rows/8), block = 128: thread = (token, 4 rotary pairs)
 __global__ void __launch_bounds__(128, 8) la_qkv_epi_kernel(LaQkvEpi e) {
-  LA_PDL_ENTRY_PF(e.pf);
+  la_epi_enter(e.ready, e.runs, e.sp, blockIdx.x, e.pf);
   const FwdPlan* P = e.plan;
   const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
   if (tok >= P->n_rows) return;
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128, 8) la_qkv_epi_kernel(LaQkvEpi e) {
 // lane = 4 features.  x (+)= sum of segment partials (or := embedding row);
 // next GEMM input bf16(x * g) (deferred RMSNorm) and the tile's sum of x^2
 __global__ void __launch_bounds__(256, 4) la_resid_norm_kernel(LaResidNorm e) {
-  LA_PDL_ENTRY_PF(e.pf);
+  la_epi_enter(e.ready, e.runs, e.sp, blockIdx.x, e.pf);
   const FwdPlan* P = e.plan;
   const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (r >= P->n_rows) return;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256, 4) la_resid_norm_kernel(LaResidNorm e) {
 // grid = (ffn/64 tiles, rows/16), block = 128: thread = (token, 8 outputs),
 // 8 threads per token -- one wave over the GPU, every load issued before use
 __global__ void __launch_bounds__(128, 8) la_swiglu_epi_kernel(LaSwigluEpi e) {
-  LA_PDL_ENTRY_PF(e.pf);
+  la_epi_enter(e.ready, e.runs, e.sp, blockIdx.x, e.pf);
   const FwdPlan* P = e.plan;
   const int t = blockIdx.x;
   const int tok = blockIdx.y * 16 + (threadIdx.x >> 3);
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(128, 8) la_swiglu_epi_kernel(LaSwigluEpi e) {
 // whose key orders by value then by LOWER index (sampling.py:17-19), so the
 // result does not depend on arrival order.
 __global__ void __launch_bounds__(128, 8) la_logits_epi_kernel(LaLogitsEpi e) {
-  LA_PDL_ENTRY();
+  la_epi_enter(e.ready, e.runs, e.sp, blockIdx.x, LaPrefetch{});
   const FwdPlan* P = e.plan;
   const int tok = blockIdx.y * 8 + (threadIdx.x >> 4);
   const bool valid = tok < P->n_rows;

@@ -19,6 +19,8 @@ struct LaQkvEpi {
   const float *rope_cos, *rope_sin;
   int H, KVH;
   LaRowNorm nrm;                 // deferred RMSNorm of the projection input
+  const int* ready = nullptr;   // producing GEMM's per-unit-tile piece counters (la_gemm.cuh)
+  int* runs = nullptr;          // [grid] this kernel's launches so far, one slot per CTA
 };
 
 struct LaResidNorm {
@@ -33,6 +35,8 @@ struct LaResidNorm {
   int d;
   float eps;
   float* ss;                     // [d/128][128] per-tile sums of x^2 (LaRowNorm.ss)
+  const int* ready = nullptr;   // producing GEMM's per-unit-tile piece counters (la_gemm.cuh)
+  int* runs = nullptr;          // [grid] this kernel's launches so far, one slot per CTA
 };
 
 struct LaSwigluEpi {
@@ -43,6 +47,8 @@ struct LaSwigluEpi {
   __nv_bfloat16* act;            // packed LA rows (la_act_off)
   int act_ld;
   LaRowNorm nrm;
+  const int* ready = nullptr;   // producing GEMM's per-unit-tile piece counters (la_gemm.cuh)
+  int* runs = nullptr;          // [grid] this kernel's launches so far, one slot per CTA
 };
 
 struct LaLogitsEpi {
@@ -53,6 +59,8 @@ struct LaLogitsEpi {
   float* logits;                 // [128][V] or null
   int V;
   LaRowNorm nrm;
+  const int* ready = nullptr;   // producing GEMM's per-unit-tile piece counters (la_gemm.cuh)
+  int* runs = nullptr;          // [grid] this kernel's launches so far, one slot per CTA
 };
 
 __global__ void la_qkv_epi_kernel(LaQkvEpi e);

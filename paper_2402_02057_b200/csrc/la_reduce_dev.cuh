@@ -28,6 +28,40 @@ static __device__ __forceinline__ float4 seg_sum4(const float* ws, int t, int ma
   return acc;
 }
 
+// Entry of an epilogue kernel.  With per-tile readiness (ready != null) the
+// CTA polls its tile's piece counter instead of waiting for the whole GEMM
+// grid: the counter only grows (every contributor adds 1 per launch, also
+// when a launch has no rows), and this CTA's own launch count -- a slot only
+// it writes -- gives the target.  Every GEMM CTA passed its own dependency
+// wait before counting in, so everything before the GEMM is complete and
+// visible once the counter is reached (acquire), as after a grid wait.
+static __device__ __forceinline__ void la_epi_enter(const int* ready, int* runs, const LaSplit& sp, int tile,
+                                                    const LaPrefetch& pf) {
+  la_pdl_trigger();
+  if (!ready) {
+    la_l2_prefetch_gemm(pf);
+    la_pdl_wait();
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const int slot = blockIdx.y * gridDim.x + blockIdx.x;
+    const int r = runs[slot] + 1;
+    runs[slot] = r;
+    long c0;
+    int n;
+    la_tile_segs(tile, sp.kb, sp.n_tiles, sp.grid, c0, n, sp.tpc);
+    const int target = r * n;
+    const int* cnt = ready + tile / sp.tpc;
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+      if (v - target >= 0) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
 static __device__ __forceinline__ int tile_nseg(const LaSplit& sp, int t) {
   long c0;
   int n;
