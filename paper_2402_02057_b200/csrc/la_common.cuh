@@ -176,8 +176,8 @@ static __constant__ unsigned long long* g_la_tl;
 #define LA_TL_DEFINE_SETTER(name)                                        \
   void la_tl_set_##name(unsigned long long* p) { cudaMemcpyToSymbol(g_la_tl, &p, sizeof(p)); }
 #endif
-__device__ __forceinline__ void la_pdl_wait() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+// timeline record of this kernel's dependency release (profiling only)
+__device__ __forceinline__ void la_tl_stamp() {
   if (g_la_tl && (threadIdx.x | threadIdx.y | blockIdx.x | blockIdx.y | blockIdx.z) == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -187,6 +187,10 @@ __device__ __forceinline__ void la_pdl_wait() {
       g_la_tl[2 + 2 * i] = ((unsigned long long)(gridDim.x * gridDim.y) << 16) | blockDim.x;
     }
   }
+}
+__device__ __forceinline__ void la_pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  la_tl_stamp();
 }
 #define LA_PDL_ENTRY() \
   do {                 \

@@ -58,6 +58,7 @@ static __device__ __forceinline__ void la_epi_enter(const int* ready, int* runs,
       if (v - target >= 0) break;
       __nanosleep(64);
     }
+    la_tl_stamp();
   }
   __syncthreads();
 }
