@@ -357,7 +357,7 @@ int llama_create(la_engine* e) {
     track(p->o[l]);
     // gate/up: whole tiles per CTA with SwiGLU from TMEM + an in-kernel fixed-up
     // stream-K remainder (LA_GU_DPSK=1; measured slower than split-K pieces +
-    // the SwiGLU kernel: the per-CTA epilogue / fix-up tail, DESIGN.md 3.3)
+    // the SwiGLU kernel: the per-CTA epilogue / fix-up tail, DESIGN.md 3.4)
     const bool dpsk_on = getenv("LA_GU_DPSK") && atoi(getenv("LA_GU_DPSK")) == 1;
     const int dpsk_segs = la_gemm_dpsk_segs(D.ffn / 64, d / 64, la_sm_count());
     if (dpsk_on && !fused && !exp_paths && !(fx_mask & 4) && dpsk_segs > 0) {

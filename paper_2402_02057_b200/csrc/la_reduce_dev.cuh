@@ -53,9 +53,12 @@ static __device__ __forceinline__ void la_epi_enter(const int* ready, int* runs,
     const int target = r * n;
     const int* cnt = ready + tile / sp.tpc;
     int v;
-    for (;;) {
+    for (unsigned n = 0;; ++n) {
       asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
       if (v - target >= 0) break;
+      // a GEMM / epilogue pair out of lockstep would wait forever: fail the
+      // launch instead (seconds; a normal wait is microseconds)
+      if (n > (1u << 26)) __trap();
       __nanosleep(64);
     }
     la_tl_stamp();
