@@ -89,6 +89,11 @@ struct LlamaPath {
   bool tile_ready = false;
   std::vector<int*> runs_qkv, runs_o, runs_gu, runs_down;   // per layer: [epilogue grid] launch counts
   int* runs_head = nullptr;
+  // every readiness counter / launch-count array: zeroed together (stream-
+  // ordered) when a forward was left half-launched, so GEMMs and epilogues
+  // never run out of lockstep (ready_dirty: a forward started and did not finish)
+  std::vector<std::pair<void*, size_t>> readiness;
+  bool ready_dirty = false;
   cudaStream_t cap = nullptr;
   cudaGraphExec_t loop_exec = nullptr;   // while(!done) { step }
   cudaGraphExec_t fwd_exec = nullptr;    // K1 + forward + owned argmax (LP)
@@ -466,19 +471,22 @@ int llama_create(la_engine* e) {
   fin(p->head, 3, 3);
   p->tile_ready = !(getenv("LA_TILE_READY") && atoi(getenv("LA_TILE_READY")) == 0) && !fused && !exp_paths;
   if (p->tile_ready) {
-    auto ready_for = [&](LaGemm& gg) -> int {
-      return lalloc(e, &gg.args.ready, (size_t)(gg.args.n_tiles / gg.args.tpc));
+    auto counted = [&](int** ptr, size_t n) -> int {
+      RET_IF(lalloc(e, ptr, n));
+      p->readiness.emplace_back(*ptr, n * sizeof(int));
+      return LA_OK;
     };
+    auto ready_for = [&](LaGemm& gg) -> int { return counted(&gg.args.ready, (size_t)(gg.args.n_tiles / gg.args.tpc)); };
     p->runs_qkv.resize(D.layers); p->runs_o.resize(D.layers); p->runs_gu.resize(D.layers); p->runs_down.resize(D.layers);
     for (int l = 0; l < D.layers; ++l) {
       RET_IF(ready_for(p->qkv[l])); RET_IF(ready_for(p->o[l])); RET_IF(ready_for(p->gu[l])); RET_IF(ready_for(p->down[l]));
-      RET_IF(lalloc(e, &p->runs_qkv[l], (size_t)(H + 2 * KVH) * 16));
-      RET_IF(lalloc(e, &p->runs_o[l], (size_t)(d / 128) * 16));
-      RET_IF(lalloc(e, &p->runs_gu[l], (size_t)(D.ffn / 64) * 16));
-      RET_IF(lalloc(e, &p->runs_down[l], (size_t)(d / 128) * 16));
+      RET_IF(counted(&p->runs_qkv[l], (size_t)(H + 2 * KVH) * 16));
+      RET_IF(counted(&p->runs_o[l], (size_t)(d / 128) * 16));
+      RET_IF(counted(&p->runs_gu[l], (size_t)(D.ffn / 64) * 16));
+      RET_IF(counted(&p->runs_down[l], (size_t)(d / 128) * 16));
     }
     RET_IF(ready_for(p->head));
-    RET_IF(lalloc(e, &p->runs_head, (size_t)((D.vocab + 127) / 128) * 16));
+    RET_IF(counted(&p->runs_head, (size_t)((D.vocab + 127) / 128) * 16));
   }
   {
     // cross-GEMM L2 prefetch (LA_NPF=<MB next>[,<MB after next>]): each
@@ -787,9 +795,20 @@ static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool emb
   return LA_OK;
 }
 
+// start of a forward part (layers or head): re-zero the readiness counters if
+// the previous part was left half-launched (a launch failed mid-way)
+static int readiness_begin(la_engine* e, cudaStream_t st) {
+  LlamaPath* p = e->llama;
+  if (p->ready_dirty)
+    for (const auto& r : p->readiness) CK(cudaMemsetAsync(r.first, 0, r.second, st));
+  p->ready_dirty = !p->readiness.empty();
+  return LA_OK;
+}
+
 // all decoder layers on the rows of e->d_plan; leaves h = final-norm(x)
 static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
   LlamaPath* p = e->llama;
+  RET_IF(readiness_begin(e, st));
   __nv_bfloat16* kc = reinterpret_cast<__nv_bfloat16*>(e->kc);
   __nv_bfloat16* vc = reinterpret_cast<__nv_bfloat16*>(e->vc);
   const size_t lstride = (size_t)e->slots * p->KVH * 128;
@@ -876,11 +895,13 @@ static int forward_layers(la_engine* e, cudaStream_t st, int* nk) {
     n += (p->attn_fused ? 5 : 6) + (p->o[l].epi != LA_EPI_FX_RESID) + (p->down[l].epi != LA_EPI_FX_RESID);
   }
   *nk += n;
+  p->ready_dirty = false;
   return LA_OK;
 }
 
 static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
   LlamaPath* p = e->llama;
+  RET_IF(readiness_begin(e, st));
   p->head.args.logits = p->logits;
   {
     KT_BEGIN(st);
@@ -899,6 +920,7 @@ static int forward_head(la_engine* e, cudaStream_t st, bool scatter, int* nk) {
   KT_END(st, "logits_argmax");
   CK(cudaGetLastError());
   *nk += 2;
+  p->ready_dirty = false;
   return LA_OK;
 }
 
