@@ -567,6 +567,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         LA_UT(et == 128 - 64 && dseg < 4, (2 * gridDim.x + blockIdx.x) * 32 + 25 + 2 * dseg);
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[buf]);
+        if (args.ready) {
+          // this unit tile's piece is written: release it to the epilogue kernel
+          ptx::named_bar_sync(1, 128);
+          if (et == 0) {
+            __threadfence();
+            atomicAdd(args.ready + tile, 1);
+          }
+        }
       } else if (EPI == LA_EPI_PARTIAL_SW || multi || is_fx(EPI) || seg != 0) {
         // write this piece's fp32 partial (multi-chunk mode: every row block)
         const int nout = multi ? nblk : tpc;

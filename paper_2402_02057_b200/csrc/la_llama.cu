@@ -439,7 +439,7 @@ int llama_create(la_engine* e) {
     // split-K pieces accumulated swap-AB (default) or as (step rows x weight
     // rows) with LA_GEMM_NT=1 (4x fewer MMAs per unit, but its TMEM drain
     // runs on half the lanes' warps at <= 64 rows; measured slower)
-    static const bool nt = getenv("LA_GEMM_NT") && atoi(getenv("LA_GEMM_NT")) == 1;
+    const bool nt = getenv("LA_GEMM_NT") && atoi(getenv("LA_GEMM_NT")) == 1;
     if (!nt && gg.epi == LA_EPI_PARTIAL) gg.epi = LA_EPI_PARTIAL_SW;
     gg.args.l2pf = l2pf;
     // in-kernel launch timing is opt-in (la_gemm_timing_enable / LA_GEMM_TIMING=1):
