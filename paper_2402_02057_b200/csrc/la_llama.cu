@@ -797,10 +797,16 @@ static int resid_norm(la_engine* e, const LaGemm* from, const float* g, bool emb
 
 // start of a forward part (layers or head): re-zero the readiness counters if
 // the previous part was left half-launched (a launch failed mid-way)
-static int readiness_begin(la_engine* e, cudaStream_t st) {
+static int readiness_reset_if_dirty(la_engine* e, cudaStream_t st) {
   LlamaPath* p = e->llama;
   if (p->ready_dirty)
     for (const auto& r : p->readiness) CK(cudaMemsetAsync(r.first, 0, r.second, st));
+  p->ready_dirty = false;
+  return LA_OK;
+}
+static int readiness_begin(la_engine* e, cudaStream_t st) {
+  LlamaPath* p = e->llama;
+  RET_IF(readiness_reset_if_dirty(e, st));
   p->ready_dirty = !p->readiness.empty();
   return LA_OK;
 }
@@ -1183,6 +1189,7 @@ int llama_decode_loop(la_engine* e, cudaStream_t st, int* launches) {
   }
   if (!p->loop_exec) RET_IF(build_loop_graph(e));
   p->loop_key = key;
+  RET_IF(readiness_reset_if_dirty(e, st));   // (a graph replay records no forward on the host)
   CK(cudaGraphLaunch(p->loop_exec, st));
   // kernels launched = per-step kernels x steps; the host learns the step
   // count only at readback, so report it there (engine->h_dec is refreshed)
@@ -1204,6 +1211,7 @@ int llama_step_forward(la_engine* e, cudaStream_t st) {
     if (ce != cudaSuccess) { la_set_error("fwd instantiate: %s", cudaGetErrorString(ce)); return LA_ERR_CUDA; }
     p->fwd_graph = g;
   }
+  RET_IF(readiness_reset_if_dirty(e, st));
   CK(cudaGraphLaunch(p->fwd_exec, st));
   return LA_OK;
 }
