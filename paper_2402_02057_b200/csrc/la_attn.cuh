@@ -56,6 +56,7 @@ struct LaAttnFusedArgs {
   LaQkvEpi qkv;                  // its arguments
   unsigned* gbar;                // grid-barrier counter (monotonic; + grid per launch)
   unsigned long long* trace;     // optional [grid][8] globaltimer stamps (LA_ATTN_TRACE=1)
+  int fold_step;                 // key-split kernel: S + 1 prefix chunks, the last with the step block
 };
 
 __global__ void la_attn_fused_kernel(LaAttnFusedArgs a);

@@ -996,15 +996,20 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
   if (rb >= n_rb) return;
   const bool spread = a.spread_merge || (a.sms > 0 && a.KVH * n_rb * (S + 1) <= a.sms);
   const bool step_unit = split == S;
-  int k_begin, k_end;
-  if (step_unit) {
-    k_begin = ctx;
-    k_end = ctx + P->n_global;
-  } else {
-    const int CH = chunk_keys(ctx, S);
+  // key tiles of this unit: [k_begin, k_end) of the prefix (n_pre tiles), then
+  // -- the step-block unit -- the step block [ctx, ctx + n_global).  fold_step:
+  // the prefix is cut into S + 1 chunks and the last unit takes chunk S as well
+  // as the step block (no unit holds one lone tile); otherwise S chunks and the
+  // step block alone.  Chunking depends on ctx only either way.
+  int k_begin = ctx, k_end = ctx;
+  if (!step_unit || a.fold_step) {
+    const int nch = a.fold_step ? S + 1 : S;
+    const int CH = chunk_keys(ctx, nch);
     k_begin = min(ctx, split * CH);
     k_end = min(ctx, (split + 1) * CH);
   }
+  const int n_pre = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+  const int s_end = ctx + P->n_global;
   const int nqb = min(128, nq - rb * 128);
   const bool conc = nqb <= 64;
 
@@ -1017,8 +1022,10 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
   uint64_t* sBar = reinterpret_cast<uint64_t*>(sFlag + 4);            // TMA: one per tile slot
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t kv_ld = (size_t)a.KVH * 128;
-  const int n_tiles = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
+  const int n_tiles = n_pre + (step_unit ? (P->n_global + kKeyTile - 1) / kKeyTile : 0);
   const int ne = (n_tiles + 1) >> 1;                 // even tiles
+  auto tile_key0 = [&](int t) { return t < n_pre ? k_begin + t * kKeyTile : ctx + (t - n_pre) * kKeyTile; };
+  auto tile_end = [&](int t) { return t < n_pre ? k_end : s_end; };
   // concurrent: blocks of <= 32 rows pair warps (2k, 2k+1) on a 16-row slice so
   // the active warps spread over all four SM sub-partitions (warp % 4; 13B
   // greedy step -4.5 %); 33-64 rows use warps w and w + 4 (measured faster there)
@@ -1029,7 +1036,7 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
 
   const uint64_t pol = TMA ? ptx::policy_evict_first() : 0ull;
   auto load_tile = [&](int t, uint8_t* kb) {
-    const int t0 = k_begin + t * kKeyTile;
+    const int t0 = tile_key0(t), te = tile_end(t);
     if constexpr (TMA) {
       // keys past k_end load real (finite) cache rows; the mask drops them
       if (tid == 0) {
@@ -1045,8 +1052,8 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
     }
     for (int i = tid; i < kKeyTile * 16; i += 256) {
       const int row = i >> 4, ch = i & 15, key = t0 + row;
-      const bool ok = key < k_end;
-      const size_t off = ((size_t)(ok ? key : k_begin) * kv_ld) + kvh * 128 + ch * 8;
+      const bool ok = key < te;
+      const size_t off = ((size_t)(ok ? key : t0) * kv_ld) + kvh * 128 + ch * 8;
       cp_async16(smem_u32(kb) + swz(row, ch), a.kc + off, ok);
       cp_async16(smem_u32(kb + kKeyTile * 256) + swz(row, ch), a.vc + off, ok);
     }
@@ -1089,7 +1096,9 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
     for (int i = 0; i < 2 * kKsPairSlots; ++i) ptx::mbar_init(sBar + i, 1);
     ptx::fence_barrier_init();
   }
-  if (!step_unit) issue_first();
+  // every tile of this unit is final after the dependency wait (the step
+  // block's K / V too): start the ring now, the step unit's mask meanwhile
+  issue_first();
   const size_t grp = (size_t)kvh * a.nrb_max + rb;
   if (!step_unit && TMA) __syncthreads();   // barrier inits visible before any wait
   if (step_unit) {
@@ -1110,7 +1119,6 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
       *reinterpret_cast<uint4*>(sMask + tid * 4) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     __syncthreads();
-    issue_first();
   }
 
   float o[16][4];
@@ -1152,9 +1160,10 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
       }
     }
     if (warp_active && t < n_tiles) {
-      const int nvalid = min(kKeyTile, k_end - (k_begin + t * kKeyTile));
-      const uint32_t* w0 = step_unit ? sMask + qrow0 * 4 + 2 * t : nullptr;
-      const uint32_t* w1 = step_unit ? sMask + (qrow0 + 8) * 4 + 2 * t : nullptr;
+      const int nvalid = min(kKeyTile, tile_end(t) - tile_key0(t));
+      const bool masked = t >= n_pre;   // a step-block tile: the structured mask applies
+      const uint32_t* w0 = masked ? sMask + qrow0 * 4 + 2 * (t - n_pre) : nullptr;
+      const uint32_t* w1 = masked ? sMask + (qrow0 + 8) * 4 + 2 * (t - n_pre) : nullptr;
       ks_tile<TMA>(sK, qf, o, m0, m1, l0, l1, lane, nvalid, w0, w1, sl2);
     }
     __syncthreads();

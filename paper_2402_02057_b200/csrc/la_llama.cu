@@ -570,6 +570,13 @@ int llama_create(la_engine* e) {
     const int ks = ks_env ? std::max(0, std::min(2, atoi(ks_env))) : (cache_tiles >= 8 ? 2 : 0);
     af.ksplit = (!af.tc && !af.cluster && !af.fuse_qkv) ? ks : 0;
     af.kv_pf = getenv("LA_ATTN_KV_PF") && atoi(getenv("LA_ATTN_KV_PF")) == 1;
+    // key-split kernel: the step block rides with the last of S + 1 prefix
+    // chunks instead of being a unit of its own -- no unit holds one lone tile
+    // while the others hold 28 (13B, 3.5K keys: lookahead step 6.77 -> 6.53 ms,
+    // greedy 5.96 -> 5.73).  Default with the long-cache (TMA) choice; with
+    // short caches (7B, 0.5K keys) measured +0.6 %: LA_ATTN_FOLD=0/1 overrides.
+    const char* fold_env = getenv("LA_ATTN_FOLD");
+    af.fold_step = af.ksplit && (fold_env ? atoi(fold_env) == 1 : (!ks_env && ks == 2));
     af.spec_ctx = nullptr;
     if (af.ksplit == 2) {
       CUtensorMap maps[2];
