@@ -113,6 +113,37 @@ __device__ __forceinline__ void stamp_w4(const LaAttnFusedArgs& a, int k) {
     *reinterpret_cast<volatile unsigned long long*>(a.trace + blockIdx.x * 8 + k) = t;
   }
 }
+// A query row's visible step keys as a 128-bit set (bit k = slot ctx + k): its
+// chain and itself.  Chain entries are read 16 at a time with every load of a
+// batch in flight together -- one L2 round trip for the lookahead rows' chains
+// (<= W + N - 2 keys) instead of one dependent load per key (2.8 us of the step
+// unit's start at 13B).  Entries past chain_n are read (the row holds
+// LA_MAX_CHAIN) but never used.
+__device__ __forceinline__ void mask_add(uint32_t (&w)[4], int key) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) w[q] |= (key >> 5) == q ? 1u << (key & 31) : 0u;
+}
+__device__ __forceinline__ uint4 row_step_mask(const FwdPlan* P, int r, int ctx) {
+  const int* ch = P->chain[r];
+  int k[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) k[u] = ch[u];
+  const int n = P->chain_n[r];
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  mask_add(w, P->slot[r] - ctx);
+#pragma unroll
+  for (int u = 0; u < 16; ++u)
+    if (u < n) mask_add(w, k[u] - ctx);
+  for (int j0 = 16; j0 < n; j0 += 16) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) k[u] = ch[j0 + u];
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (j0 + u < n) mask_add(w, k[u] - ctx);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+static_assert(LA_MAX_CHAIN % 16 == 0, "chain rows are read in batches of 16");
 // per-warp progress marks (debug): trace slot 6 holds one byte per warp
 __device__ __forceinline__ void wmark(const LaAttnFusedArgs& a, int v) {
   if (a.trace && (a.dbg & 4) && (threadIdx.x & 31) == 0) {
@@ -620,20 +651,9 @@ __device__ void attn_unit(const LaAttnFusedArgs& a, uint8_t* smem, int e, int sp
     // structured mask: a query row sees its chain's step keys and itself;
     // one thread per row builds its 128-bit set in registers (independent loads)
     if (tid < LA_MAX_ROWS) {
-      uint32_t w[4] = {0u, 0u, 0u, 0u};
       const int qr = rb * 128 + tid;
-      if (qr < nq) {
-        const int r = qr / g;
-        const int n = P->chain_n[r];
-        const int own = P->slot[r] - ctx;
-        w[own >> 5] |= 1u << (own & 31);
-        for (int jj = 0; jj < n; ++jj) {
-          const int key = P->chain[r][jj] - ctx;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) w[q] |= (key >> 5) == q ? 1u << (key & 31) : 0u;
-        }
-      }
-      *reinterpret_cast<uint4*>(sMask + tid * 4) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(sMask + tid * 4) =
+          qr < nq ? row_step_mask(P, qr / g, ctx) : make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
   }
@@ -1103,20 +1123,9 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
   if (!step_unit && TMA) __syncthreads();   // barrier inits visible before any wait
   if (step_unit) {
     if (tid < LA_MAX_ROWS) {
-      uint32_t w[4] = {0u, 0u, 0u, 0u};
       const int qr = rb * 128 + tid;
-      if (qr < nq) {
-        const int r = qr / g;
-        const int n = P->chain_n[r];
-        const int own = P->slot[r] - ctx;
-        w[own >> 5] |= 1u << (own & 31);
-        for (int jj = 0; jj < n; ++jj) {
-          const int key = P->chain[r][jj] - ctx;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) w[q] |= (key >> 5) == q ? 1u << (key & 31) : 0u;
-        }
-      }
-      *reinterpret_cast<uint4*>(sMask + tid * 4) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(sMask + tid * 4) =
+          qr < nq ? row_step_mask(P, qr / g, ctx) : make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
   }

@@ -25,7 +25,8 @@ m = la.LlamaModel(cfgm, dtype="bf16", seed=0, max_context=plen + 128)
 prompt = [int(t) for t in np.random.default_rng(0).integers(0, m.vocab_size, plen)]
 greedy = len(sys.argv) > 1 and sys.argv[1] == "greedy"
 steps = int(os.environ.get("STEPS", "8"))
-cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=steps)
+W, N, G = (int(x) for x in os.environ.get("WNG", "15,5,15").split(","))
+cfg = la.GenerationConfig(window=W, ngram=N, max_candidates=G, max_tokens=steps)
 for _ in range(2):
     if greedy:
         la.decode_autoregressive(m, prompt, la.SamplerSpec("greedy"), steps)
