@@ -57,6 +57,12 @@ struct LaAttnFusedArgs {
   unsigned* gbar;                // grid-barrier counter (monotonic; + grid per launch)
   unsigned long long* trace;     // optional [grid][8] globaltimer stamps (LA_ATTN_TRACE=1)
   int fold_step;                 // key-split kernel: S + 1 prefix chunks, the last with the step block
+  int flat;                      // key-split kernel, one row block: the KVH x prefix-tile space cut
+                                 // evenly over the grid (every SM), a head's step block with the CTA
+                                 // holding its last prefix tile; partials [KVH][flat_maxp]
+  int flat_maxp;                 // partial slots per KV head (>= CTAs meeting one head)
+  unsigned* fcnt;                // [KVH] segment arrivals, re-zeroed by the head's last merger
+  unsigned* fdone;               // [KVH] mergers past their wait
 };
 
 __global__ void la_attn_fused_kernel(LaAttnFusedArgs a);

@@ -409,6 +409,8 @@ __device__ void attn_merge_cluster(const LaAttnFusedArgs& a, uint8_t* smem, int 
 // Chunk arrival + merge of a (KV head, row block) group after every chunk
 // CTA wrote its partial to global memory: spread (every chunk CTA merges a
 // share of the rows once all arrived) or last-arriver (one CTA merges all).
+__device__ __forceinline__ void attn_merge_rows(const LaAttnFusedArgs& a, size_t base, int count, int r0, int r1,
+                                                int rb, int g, int kvh);
 __device__ __forceinline__ void attn_arrive_merge(const LaAttnFusedArgs& a, int* sFlag, size_t grp, int S, int split,
                                   int rb, int g, int nq, int kvh, bool spread) {
   const int tid = threadIdx.x;
@@ -438,11 +440,19 @@ __device__ __forceinline__ void attn_arrive_merge(const LaAttnFusedArgs& a, int*
   if (!*sFlag) return;
 
   // ---- merge the S+1 chunk partials of this group in chunk order: rows
-  // [r0, r1) of the group's valid rows, 8 threads per row x 16 dims
+  // [r0, r1) of the group's valid rows
   const int nqb = min(128, nq - rb * 128);
   const int rows_per = spread ? (nqb + S) / (S + 1) : nqb;
   const int r0 = spread ? split * rows_per : 0;
   const int r1 = min(nqb, r0 + rows_per);
+  attn_merge_rows(a, grp * (S + 1), S + 1, r0, r1, rb, g, kvh);
+}
+
+// Merge partial slots [base, base + count) in slot order into the attention
+// output for rows [r0, r1) of row block rb, 8 threads per row x 16 dims
+__device__ __forceinline__ void attn_merge_rows(const LaAttnFusedArgs& a, size_t base, int count, int r0, int r1,
+                                                int rb, int g, int kvh) {
+  const int tid = threadIdx.x;
   for (int row = r0 + (tid >> 3); row < r1; row += 32) {
     const int qr = rb * 128 + row;
     const int hd = (tid & 7) * 16;
@@ -452,14 +462,14 @@ __device__ __forceinline__ void attn_arrive_merge(const LaAttnFusedArgs& a, int*
     for (int i = 0; i < 16; ++i) acc[i] = 0.f;
     // partials in batches of 4 with every load of a batch in flight together
     // (a dependent L2 round trip per partial otherwise); same combine order
-    for (int sp0 = 0; sp0 <= S; sp0 += 4) {
+    for (int sp0 = 0; sp0 < count; sp0 += 4) {
       float2 mlv[4];
       float4 pv[4][4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int sp = sp0 + j;
-        if (sp <= S) {
-          const size_t us = grp * (S + 1) + sp;
+        if (sp < count) {
+          const size_t us = base + sp;
           mlv[j] = __ldcg(a.part_ml + us * 128 + row);
           const float4* po = reinterpret_cast<const float4*>(a.part_o + (us * 128 + row) * 128 + hd);
 #pragma unroll
@@ -1000,42 +1010,18 @@ __device__ __forceinline__ void ks_combine(float (&o)[16][4], float& m0, float& 
   }
 }
 
+// One key segment of a (KV head, row block): prefix keys [k_begin, k_end) then,
+// for the step unit, the step block [ctx, ctx + n_global) under the lookahead
+// mask; its partial (o, m, l) goes to partial slot `pslot`.  reinit: a second
+// segment of the same CTA (flat mapping) re-arms the TMA barriers first.
 template <bool TMA>
-__device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e) {
-  stamp(a, 1);
-  const FwdPlan* P = a.plan;
-  const int n_rows = P->n_rows, ctx = P->n_prefix;
-  if (n_rows == 0) return;
-  const int g = a.H / a.KVH;
-  const int nq = n_rows * g;
-  const int n_rb = (nq + 127) >> 7;
-  const int S = a.S;
-  const int kvh = e / (a.nrb_max * (S + 1));
-  const int rb = (e / (S + 1)) % a.nrb_max;
-  const int split = e % (S + 1);
-  if (rb >= n_rb) return;
-  const bool spread = a.spread_merge || (a.sms > 0 && a.KVH * n_rb * (S + 1) <= a.sms);
-  const bool step_unit = split == S;
-  // key tiles of this unit: [k_begin, k_end) of the prefix (n_pre tiles), then
-  // -- the step-block unit -- the step block [ctx, ctx + n_global).  fold_step:
-  // the prefix is cut into S + 1 chunks and the last unit takes chunk S as well
-  // as the step block (no unit holds one lone tile); otherwise S chunks and the
-  // step block alone.  Chunking depends on ctx only either way.
-  int k_begin = ctx, k_end = ctx;
-  if (!step_unit || a.fold_step) {
-    const int nch = a.fold_step ? S + 1 : S;
-    const int CH = chunk_keys(ctx, nch);
-    k_begin = min(ctx, split * CH);
-    k_end = min(ctx, (split + 1) * CH);
-  }
+__device__ void ks_segment(const LaAttnFusedArgs& a, uint8_t* smem, const FwdPlan* P, int ctx, int nq, int g,
+                           int kvh, int rb, int k_begin, int k_end, bool step_unit, size_t pslot, bool reinit) {
   const int n_pre = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
   const int s_end = ctx + P->n_global;
   const int nqb = min(128, nq - rb * 128);
   const bool conc = nqb <= 64;
 
-  // 1024-B alignment for the SW128 TMA boxes by pointer + offset (an integer
-  // round trip hides the shared address space: generic LD/ST for every access)
-  uint8_t* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
   uint8_t* sKV = smem;
   uint32_t* sMask = reinterpret_cast<uint32_t*>(smem + kKsMaskOff);   // [128][4]
   int* sFlag = reinterpret_cast<int*>(sMask + LA_MAX_ROWS * 4);
@@ -1112,14 +1098,17 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
       qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
     }
   }
+  if (reinit) __syncthreads();   // the previous segment's stash reads are done
   if (TMA && tid == 0) {
-    for (int i = 0; i < 2 * kKsPairSlots; ++i) ptx::mbar_init(sBar + i, 1);
+    for (int i = 0; i < 2 * kKsPairSlots; ++i) {
+      if (reinit) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(sBar + i)) : "memory");
+      ptx::mbar_init(sBar + i, 1);
+    }
     ptx::fence_barrier_init();
   }
   // every tile of this unit is final after the dependency wait (the step
   // block's K / V too): start the ring now, the step unit's mask meanwhile
   issue_first();
-  const size_t grp = (size_t)kvh * a.nrb_max + rb;
   if (!step_unit && TMA) __syncthreads();   // barrier inits visible before any wait
   if (step_unit) {
     if (tid < LA_MAX_ROWS) {
@@ -1205,16 +1194,128 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
     for (int half = 0; half < 2; ++half) {
       const int row = qrow0 + half * 8;
       if (rb * 128 + row >= nq) continue;
-      float* dst = a.part_o + ((grp * (S + 1) + split) * 128 + row) * 128;
+      float* dst = a.part_o + (pslot * 128 + row) * 128;
 #pragma unroll
       for (int dd = 0; dd < 16; ++dd) {
         const int col = dd * 8 + (lane & 3) * 2;
         __stcg(reinterpret_cast<float2*>(dst + col), make_float2(o[dd][half * 2], o[dd][half * 2 + 1]));
       }
       if ((lane & 3) == 0)
-        __stcg(a.part_ml + (grp * (S + 1) + split) * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
+        __stcg(a.part_ml + pslot * 128 + row, make_float2(half ? m1 : m0, half ? l1 : l0));
     }
   }
+}
+
+
+// Flat mapping (a.flat): the prefix tiles of all KV heads, head-major, are cut
+// into gridDim.x (or fewer, >= 1 tile each) contiguous ranges, one per CTA --
+// every SM streams about the same number of tiles whatever KVH (13B: 40 heads
+// x 3 chunk units left 28 SMs idle).  A range spanning two heads is two
+// segments; the CTA holding a head's last prefix tile also takes its step
+// block.  The cut depends on ctx, KVH and the grid only, so every row of a
+// step -- and the same row in a greedy step -- sees the same key partition;
+// the head's partials merge in range order.  All CTAs are co-resident (grid <=
+// SMs, one CTA per SM): each waits for its heads' segments, merges its share
+// of their rows, and the head's last merger re-zeroes the head's counters.
+template <bool TMA>
+__device__ void attn_flat_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw) {
+  stamp(a, 1);
+  const FwdPlan* P = a.plan;
+  const int n_rows = P->n_rows, ctx = P->n_prefix;
+  if (n_rows == 0) return;
+  const int g = a.H / a.KVH;
+  const int nq = min(128, n_rows * g);   // one row block (flat needs nrb_max == 1)
+  const long T = max(1, (ctx + kKeyTile - 1) / kKeyTile);   // a virtual tile when ctx == 0
+  const long total = (long)a.KVH * T;
+  const long G = min((long)gridDim.x, total);
+  const int e = blockIdx.x;
+  if (e >= G) return;
+  auto owner = [&](long x) { return (int)(((x + 1) * G - 1) / total); };   // the CTA holding tile x
+  const long lo = e * total / G, hi = (e + 1) * total / G;
+  uint8_t* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
+  const int tid = threadIdx.x;
+  int hs[2], ps[2], ns[2], nseg = 0;
+  for (long x = lo; x < hi && nseg < 2;) {
+    const int h = (int)(x / T);
+    const long hend = min(hi, (h + 1) * T);
+    const int f = owner(h * T);
+    const int kb = (int)(x - h * T) * kKeyTile, ke = (int)(hend - h * T) * kKeyTile;
+    ks_segment<TMA>(a, smem, P, ctx, nq, g, h, 0, min(ctx, kb), min(ctx, ke), hend == (h + 1) * T,
+                    (size_t)h * a.flat_maxp + (e - f), nseg > 0);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(a.fcnt + h, 1u);
+    }
+    hs[nseg] = h;
+    ps[nseg] = e - f;
+    ns[nseg] = owner((h + 1) * T - 1) - f + 1;
+    ++nseg;
+    x = hend;
+  }
+  for (int i = 0; i < nseg; ++i) {
+    const int h = hs[i], n = ns[i];
+    if (tid == 0) {
+      unsigned v, spins = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.fcnt + h) : "memory");
+        if (v < (unsigned)n) {
+          __nanosleep(64);
+          if (++spins > (1u << 26)) __trap();
+        }
+      } while (v < (unsigned)n);
+      if (atomicAdd(a.fdone + h, 1u) + 1 == (unsigned)n) {   // every merger of h is past its wait
+        a.fcnt[h] = 0u;
+        a.fdone[h] = 0u;
+      }
+    }
+    __syncthreads();
+    if (i == 0) stamp(a, 5);
+    const int rows_per = (nq + n - 1) / n;
+    const int r0 = ps[i] * rows_per;
+    attn_merge_rows(a, (size_t)h * a.flat_maxp, n, r0, min(nq, r0 + rows_per), 0, g, h);
+  }
+  stamp(a, 6);
+}
+
+template <bool TMA>
+__device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e) {
+  if (a.flat) {
+    attn_flat_ks<TMA>(a, smem_raw);
+    return;
+  }
+  stamp(a, 1);
+  const FwdPlan* P = a.plan;
+  const int n_rows = P->n_rows, ctx = P->n_prefix;
+  if (n_rows == 0) return;
+  const int g = a.H / a.KVH;
+  const int nq = n_rows * g;
+  const int n_rb = (nq + 127) >> 7;
+  const int S = a.S;
+  const int kvh = e / (a.nrb_max * (S + 1));
+  const int rb = (e / (S + 1)) % a.nrb_max;
+  const int split = e % (S + 1);
+  if (rb >= n_rb) return;
+  const bool spread = a.spread_merge || (a.sms > 0 && a.KVH * n_rb * (S + 1) <= a.sms);
+  const bool step_unit = split == S;
+  // key tiles of this unit: [k_begin, k_end) of the prefix (n_pre tiles), then
+  // -- the step-block unit -- the step block [ctx, ctx + n_global).  fold_step:
+  // the prefix is cut into S + 1 chunks and the last unit takes chunk S as well
+  // as the step block (no unit holds one lone tile); otherwise S chunks and the
+  // step block alone.  Chunking depends on ctx only either way.
+  int k_begin = ctx, k_end = ctx;
+  if (!step_unit || a.fold_step) {
+    const int nch = a.fold_step ? S + 1 : S;
+    const int CH = chunk_keys(ctx, nch);
+    k_begin = min(ctx, split * CH);
+    k_end = min(ctx, (split + 1) * CH);
+  }
+  // 1024-B alignment for the SW128 TMA boxes by pointer + offset (an integer
+  // round trip hides the shared address space: generic LD/ST for every access)
+  uint8_t* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
+  int* sFlag = reinterpret_cast<int*>(smem + kKsMaskOff + LA_MAX_ROWS * 16);
+  const size_t grp = (size_t)kvh * a.nrb_max + rb;
+  ks_segment<TMA>(a, smem, P, ctx, nq, g, kvh, rb, k_begin, k_end, step_unit, grp * (S + 1) + split, false);
   attn_arrive_merge(a, sFlag, grp, S, split, rb, g, nq, kvh, spread);
   stamp(a, 6);
 }

@@ -592,10 +592,23 @@ int llama_create(la_engine* e) {
     af.scale = 1.0f / sqrtf(128.0f);
     af.q = p->q;
     af.out = p->attn;
+    // flat mapping of the key-split kernel (LA_ATTN_FLAT=1): one CTA per SM over
+    // the KVH x prefix-tile space; needs one row block and KVH <= SMs (a CTA's
+    // range then meets at most two heads)
+    af.flat = af.ksplit == 2 && af.nrb_max == 1 && p->KVH <= la_sm_count() && getenv("LA_ATTN_FLAT") &&
+              atoi(getenv("LA_ATTN_FLAT")) == 1;
+    af.flat_maxp = (la_sm_count() + p->KVH - 1) / p->KVH + 1;
     const size_t groups = (size_t)p->KVH * af.nrb_max;
-    RET_IF(lalloc(e, &af.part_o, groups * units * 128 * 128));
-    RET_IF(lalloc(e, &af.part_ml, groups * units * 128));
+    const size_t slots_per = af.flat ? std::max<size_t>(units, af.flat_maxp) : units;
+    RET_IF(lalloc(e, &af.part_o, groups * slots_per * 128 * 128));
+    RET_IF(lalloc(e, &af.part_ml, groups * slots_per * 128));
     RET_IF(lalloc(e, &af.cnt, groups));
+    if (af.flat) {
+      RET_IF(lalloc(e, &af.fcnt, (size_t)p->KVH));
+      RET_IF(lalloc(e, &af.fdone, (size_t)p->KVH));
+      p->readiness.emplace_back(af.fcnt, (size_t)p->KVH * sizeof(unsigned));
+      p->readiness.emplace_back(af.fdone, (size_t)p->KVH * sizeof(unsigned));
+    }
     // attention + O in one persistent launch: needs every attention unit and
     // every O CTA co-resident (one CTA per SM) and the O GEMM on all SMs
     p->attn_o = getenv("LA_ATTN_O") && atoi(getenv("LA_ATTN_O")) == 1 && af.spread_merge && !af.tc &&
@@ -606,15 +619,16 @@ int llama_create(la_engine* e) {
       RET_IF(lalloc(e, &p->ao_err, 1));
     }
     if (getenv("LA_ATTN_TRACE")) {
+      const size_t ctas = std::max(groups * units, (size_t)la_sm_count());
       if (atoi(getenv("LA_ATTN_TRACE")) == 2) {
         // mapped host memory: readable by a host watchdog while a kernel hangs
         void* hp = nullptr;
-        CK(cudaHostAlloc(&hp, groups * units * 64, cudaHostAllocMapped));
-        memset(hp, 0, groups * units * 64);
+        CK(cudaHostAlloc(&hp, ctas * 64, cudaHostAllocMapped));
+        memset(hp, 0, ctas * 64);
         g_attn_trace_host = hp;
         CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&af.trace), hp, 0));
       } else {
-        RET_IF(lalloc(e, &af.trace, groups * units * 8));
+        RET_IF(lalloc(e, &af.trace, ctas * 8));
       }
     }
     ce = cudaFuncSetAttribute(la_attn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -778,7 +792,7 @@ static int launch_attn_fused(la_engine* e, int l, cudaStream_t st) {
                      p->rope_sin, p->H, p->KVH, p->nrm};
   }
   KT_BEGIN(st);
-  CK(la_attn_fused_launch(a, p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
+  CK(la_attn_fused_launch(a, a.flat ? la_sm_count() : p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
   KT_END(st, "attn_fused");
   return LA_OK;
 }
@@ -1016,7 +1030,7 @@ static int prefill_chunks(la_engine* e, const int* d_tokens, int start, int n_ch
       a.kv_row0 = l * e->slots;
       a.spec_ctx = nullptr;
       a.pf = LaPrefetch{};
-      CK(la_attn_fused_launch(a, p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
+      CK(la_attn_fused_launch(a, a.flat ? la_sm_count() : p->KVH * a.nrb_max * (a.S + 1), st, p->pdl));
     }
     RET_IF(multi(p->o1[l], &Chunk::attn));
     for (int i = 0; i < n_chunks; ++i) RET_IF(resid(i, &p->o1[l], p->lw[l].mlp_norm, false));
@@ -1242,7 +1256,10 @@ bool llama_debug_buffer(la_engine* e, int what, const void** src, size_t* bytes)
     case 13: *src = a.ss_mlp; *bytes = (size_t)p->d * 4; return a.ss_mlp != nullptr;
     case 14: *src = p->act; *bytes = R * p->ffn * 2; return true;
     case 15: *src = p->row_amax; *bytes = R * 4; return true;
-    case 17: *src = p->af.trace; *bytes = (size_t)p->KVH * p->af.nrb_max * (p->af.S + 1) * 64; return p->af.trace != nullptr;
+    case 17:
+      *src = p->af.trace;
+      *bytes = std::max((size_t)p->KVH * p->af.nrb_max * (p->af.S + 1), (size_t)la_sm_count()) * 64;
+      return p->af.trace != nullptr;
     case 18: *src = g_tl_buf; *bytes = (1 + 2 * LA_TL_CAP) * 8; return g_tl_buf != nullptr;
     case 20: *src = p->utrace; *bytes = 5 * 3 * 256 * 32 * 8; return p->utrace != nullptr;
     case 16: *src = a.trace; *bytes = (size_t)la_sm_count() * a.trace_slots * 64; return a.trace != nullptr;

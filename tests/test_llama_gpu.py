@@ -55,6 +55,8 @@ PATHS = {"kernels": {}, "fused_epi": {"LA_FUSED_EPI": "1"}, "fx_epi": {"LA_FX": 
          # the step block folded into the last of S + 1 prefix chunks
          "ksplit_fold": {"LA_ATTN_KSPLIT": "1", "LA_ATTN_FOLD": "1"},
          "ksplit_tma_fold": {"LA_ATTN_KSPLIT": "2", "LA_ATTN_FOLD": "1"},
+         # the KVH x prefix-tile space cut evenly over one CTA per SM
+         "ksplit_tma_flat": {"LA_ATTN_KSPLIT": "2", "LA_ATTN_FLAT": "1"},
          # split-K pieces accumulated as (step rows x weight rows); the epilogues
          # waiting for the whole GEMM grid instead of their tile's piece counter
          "nt_gemm": {"LA_GEMM_NT": "1"}, "grid_wait": {"LA_TILE_READY": "0"}}
@@ -67,7 +69,7 @@ def pair(request):
     saved = {k: os.environ.get(k) for k in ("LA_FUSED_EPI", "LA_FX", "LA_MEGA", "LA_ATTN_TC", "LA_ATTN_O",
                                             "LA_ATTN_CLUSTER", "LA_ATTN_LAST_MERGE", "LA_ATTN_KSPLIT",
                                             "LA_ATTN_SPLITS", "LA_GU_DPSK", "LA_GEMM_NT", "LA_TILE_READY",
-                                            "LA_ATTN_FOLD")}
+                                            "LA_ATTN_FOLD", "LA_ATTN_FLAT")}
     for k in saved:
         os.environ.pop(k, None)
     os.environ.update(PATHS[path])
