@@ -1014,7 +1014,7 @@ __device__ __forceinline__ void ks_combine(float (&o)[16][4], float& m0, float& 
 // for the step unit, the step block [ctx, ctx + n_global) under the lookahead
 // mask; its partial (o, m, l) goes to partial slot `pslot`.  reinit: a second
 // segment of the same CTA (flat mapping) re-arms the TMA barriers first.
-template <bool TMA>
+template <bool TMA, bool FLAT>
 __device__ void ks_segment(const LaAttnFusedArgs& a, uint8_t* smem, const FwdPlan* P, int ctx, int nq, int g,
                            int kvh, int rb, int k_begin, int k_end, bool step_unit, size_t pslot, bool reinit) {
   const int n_pre = (k_end - k_begin + kKeyTile - 1) / kKeyTile;
@@ -1098,10 +1098,10 @@ __device__ void ks_segment(const LaAttnFusedArgs& a, uint8_t* smem, const FwdPla
       qf[kk][3] = pb ? __ldcg(reinterpret_cast<const unsigned*>(pb + col + 8)) : 0u;
     }
   }
-  if (reinit) __syncthreads();   // the previous segment's stash reads are done
+  if (FLAT && reinit) __syncthreads();   // the previous segment's stash reads are done
   if (TMA && tid == 0) {
     for (int i = 0; i < 2 * kKsPairSlots; ++i) {
-      if (reinit) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(sBar + i)) : "memory");
+      if (FLAT && reinit) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(sBar + i)) : "memory");
       ptx::mbar_init(sBar + i, 1);
     }
     ptx::fence_barrier_init();
@@ -1240,7 +1240,7 @@ __device__ void attn_flat_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw) {
     const long hend = min(hi, (h + 1) * T);
     const int f = owner(h * T);
     const int kb = (int)(x - h * T) * kKeyTile, ke = (int)(hend - h * T) * kKeyTile;
-    ks_segment<TMA>(a, smem, P, ctx, nq, g, h, 0, min(ctx, kb), min(ctx, ke), hend == (h + 1) * T,
+    ks_segment<TMA, true>(a, smem, P, ctx, nq, g, h, 0, min(ctx, kb), min(ctx, ke), hend == (h + 1) * T,
                     (size_t)h * a.flat_maxp + (e - f), nseg > 0);
     __syncthreads();
     if (tid == 0) {
@@ -1280,10 +1280,6 @@ __device__ void attn_flat_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw) {
 
 template <bool TMA>
 __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e) {
-  if (a.flat) {
-    attn_flat_ks<TMA>(a, smem_raw);
-    return;
-  }
   stamp(a, 1);
   const FwdPlan* P = a.plan;
   const int n_rows = P->n_rows, ctx = P->n_prefix;
@@ -1315,12 +1311,14 @@ __device__ void attn_unit_ks(const LaAttnFusedArgs& a, uint8_t* smem_raw, int e)
   uint8_t* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
   int* sFlag = reinterpret_cast<int*>(smem + kKsMaskOff + LA_MAX_ROWS * 16);
   const size_t grp = (size_t)kvh * a.nrb_max + rb;
-  ks_segment<TMA>(a, smem, P, ctx, nq, g, kvh, rb, k_begin, k_end, step_unit, grp * (S + 1) + split, false);
+  ks_segment<TMA, false>(a, smem, P, ctx, nq, g, kvh, rb, k_begin, k_end, step_unit, grp * (S + 1) + split, false);
   attn_arrive_merge(a, sFlag, grp, S, split, rb, g, nq, kvh, spread);
   stamp(a, 6);
 }
 
-template <bool TMA>
+// FLAT: the flat mapping (a separate instantiation: its second segment and
+// per-head merge cost the default kernel 20 registers and ~1-2 % when inlined)
+template <bool TMA, bool FLAT>
 __global__ void __launch_bounds__(256, 1) la_attn_ks_kernel(LaAttnFusedArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   stamp(a, 0);
@@ -1332,7 +1330,10 @@ __global__ void __launch_bounds__(256, 1) la_attn_ks_kernel(LaAttnFusedArgs a) {
     ptx::tma_prefetch_desc(a.vmap);
   }
   la_pdl_wait();
-  attn_unit_ks<TMA>(a, smem, blockIdx.x);
+  if constexpr (FLAT)
+    attn_flat_ks<TMA>(a, smem);
+  else
+    attn_unit_ks<TMA>(a, smem, blockIdx.x);
 }
 
 cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_t st, bool pdl) {
@@ -1366,15 +1367,20 @@ cudaError_t la_attn_fused_launch(const LaAttnFusedArgs& a, int grid, cudaStream_
     return cudaLaunchKernelEx(&cfg, la_attn_cluster_kernel, a);
   }
   if (ks) {
-    static std::atomic<unsigned> attr_cp{0}, attr_tma{0};
-    if (a.ksplit == 2) {
-      cudaError_t e = la_smem_attr_once(attr_tma, la_attn_ks_kernel<true>, kKsSmemTma);
+    static std::atomic<unsigned> attr_cp{0}, attr_tma{0}, attr_flat{0};
+    if (a.ksplit == 2 && a.flat) {
+      cudaError_t e = la_smem_attr_once(attr_flat, la_attn_ks_kernel<true, true>, kKsSmemTma);
       if (e != cudaSuccess) return e;
-      return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<true>, a);
+      return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<true, true>, a);
     }
-    cudaError_t e = la_smem_attr_once(attr_cp, la_attn_ks_kernel<false>, kKsSmem);
+    if (a.ksplit == 2) {
+      cudaError_t e = la_smem_attr_once(attr_tma, la_attn_ks_kernel<true, false>, kKsSmemTma);
+      if (e != cudaSuccess) return e;
+      return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<true, false>, a);
+    }
+    cudaError_t e = la_smem_attr_once(attr_cp, la_attn_ks_kernel<false, false>, kKsSmem);
     if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<false>, a);
+    return cudaLaunchKernelEx(&cfg, la_attn_ks_kernel<false, false>, a);
   }
   return cudaLaunchKernelEx(&cfg, la_attn_fused_kernel, a);
 }
