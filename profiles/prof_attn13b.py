@@ -8,7 +8,8 @@ from paper_2402_02057_b200.models import PRESETS
 plen = int(os.environ.get("PLEN", "3500"))
 m = la.LlamaModel(PRESETS[os.environ.get("PRESET", "llama2-13b")], dtype="bf16", seed=0, max_context=plen + 400)
 prompt = [int(t) for t in np.random.default_rng(0).integers(0, m.vocab_size, plen)]
-cfg = la.GenerationConfig(window=15, ngram=5, max_candidates=15, max_tokens=64)
+W, N, G = (int(x) for x in os.environ.get("WNG", "15,5,15").split(","))
+cfg = la.GenerationConfig(window=W, ngram=N, max_candidates=G, max_tokens=64)
 st = la.start_session(m, prompt, cfg, la.SamplerSpec("greedy"))
 for _ in range(3):
     la.lookahead_step(st)
