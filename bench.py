@@ -74,10 +74,10 @@ PRESET = "llama2-7b"
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum of one gate/up GEMM launch from
-# the committed ncu --set full capture (profiles/r02_gemm_gu.ncu-rep, cfg2
-# decode step 1, layer 1; profiles/capture_r02.sh): the dominant kernel's
+# the committed ncu --set full capture (profiles/r02e_gemm_gu.ncu-rep, cfg2
+# decode step 1, layer 1; profiles/capture_r02e.sh): the dominant kernel's
 # measured traffic per launch
-GU_TRAFFIC_BYTES = {"llama2-7b": 180.945152e6 + 5.587456e6}
+GU_TRAFFIC_BYTES = {"llama2-7b": 180.946944e6 + 5.064192e6}
 
 
 def _peaks():
@@ -449,7 +449,7 @@ def run_ours(args):
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None,
                      "traffic": GU_TRAFFIC_BYTES.get(PRESET) if PRESET == "llama2-7b" and W == 15 else None,
-                     "traffic_unit": "bytes per launch (ncu, profiles/r02_gemm_gu.ncu-rep)",
+                     "traffic_unit": "bytes per launch (ncu, profiles/r02e_gemm_gu.ncu-rep)",
                      "algorithmic_bytes": gu_bytes,
                      "avg_launch_ms": gu_ms, "launches": int(gu_n), "peak_source": peak_src,
                      "timing": "in-kernel globaltimer per launch over one instrumented decode of the "
