@@ -73,11 +73,15 @@ WORKLOAD = CONFIGS["cfg2"]["name"]
 PRESET = "llama2-7b"
 
 
-# dram__bytes_read.sum + dram__bytes_write.sum of one gate/up GEMM launch from
-# the committed ncu --set full capture (profiles/r02e_gemm_gu.ncu-rep, cfg2
-# decode step 1, layer 1; profiles/capture_r02e.sh): the dominant kernel's
-# measured traffic per launch
-GU_TRAFFIC_BYTES = {"llama2-7b": 180.946944e6 + 5.064192e6}
+# dram__bytes_read.sum + dram__bytes_write.sum of one gate/up GEMM launch (layer
+# 1 of a lookahead step) from the committed ncu --set full captures, keyed by
+# the workload they were taken on (profiles/capture_r02e.sh, capture_r02e_gu.sh):
+# the dominant kernel's measured traffic per launch
+GU_TRAFFIC = {
+    ("llama2-7b", 15): (180.946944e6 + 5.064192e6, "profiles/r02e_gemm_gu.ncu-rep"),
+    ("llama2-13b", 10): (283.674368e6 + 5.119744e6, "profiles/r02e_gemm_gu13b.ncu-rep"),
+    ("llama2-70b", 15): (940.639488e6 + 7.178496e6, "profiles/r02e_gemm_gu70b.ncu-rep"),
+}
 
 
 def _peaks():
@@ -448,8 +452,8 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": "la_gemm_kernel<SWIGLU> (gate/up, tcgen05)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None,
-                     "traffic": GU_TRAFFIC_BYTES.get(PRESET) if PRESET == "llama2-7b" and W == 15 else None,
-                     "traffic_unit": "bytes per launch (ncu, profiles/r02e_gemm_gu.ncu-rep)",
+                     "traffic": GU_TRAFFIC.get((PRESET, W), (None, None))[0],
+                     "traffic_unit": "bytes per launch (ncu, %s)" % GU_TRAFFIC.get((PRESET, W), (None, "none"))[1],
                      "algorithmic_bytes": gu_bytes,
                      "avg_launch_ms": gu_ms, "launches": int(gu_n), "peak_source": peak_src,
                      "timing": "in-kernel globaltimer per launch over one instrumented decode of the "
